@@ -1,0 +1,198 @@
+/*
+ * hz.h — C ABI of libhz, the B200 (sm_100a) wavelength-adaptive 27-point Helmholtz hot path.
+ *
+ * Method: Aghamiry, Gholami, Combe & Operto, "Accurate 3D frequency-domain seismic wave modeling
+ * with the wavelength-adaptive 27-point finite-difference stencil" (arXiv 2108.08730).
+ * Citations "P:n" are lines of that paper's text; readings "An" are listed in
+ * DESIGN.md §2 (same numbering as SURVEY.md §8(c)).
+ *
+ * The four calls of the north star:
+ *   build_weight_table(G range, dG, lambda)  -> hz_build_weight_table
+ *   assemble_coeffs(v, f, h, pml)             -> hz_assemble_coeffs
+ *   apply_impedance(u -> Au)                  -> hz_apply_impedance
+ *   solve(b[nrhs] -> u)                       -> hz_solve
+ *
+ * Conventions
+ *   - Grids are C-ordered [z][y][x] (x fastest).  A rank owns the z-slab [z0, z0+nz_local) of a
+ *     global nx*ny*nz_global grid whose dimensions INCLUDE the PML pad (A18).
+ *   - Complex fields are interleaved (re, im): complex64 = 2 x float, complex128 = 2 x double.
+ *     Field buffers have one halo plane at each end: [nrhs][nz_local+2][ny][nx]; local plane k
+ *     lives at index k+1.  The halo planes are owned by the library during a call (see each
+ *     function); the caller allocates them.
+ *   - Real model arrays (velocity) are float for HZ_C64 and double for HZ_C128, [nz_local][ny][nx].
+ *   - Pointers may be device or host memory: the library inspects each pointer
+ *     (cudaPointerGetAttributes) and stages host buffers through device memory itself.  The
+ *     caller owns every buffer it passes; the library owns hz_ctx / hz_table / hz_coeffs objects
+ *     and all solver workspace.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *   - Errors: a negative hz_status means nothing was written and hz_last_error() (thread-local)
+ *     explains; a positive status means the call completed and its outputs are valid, with a
+ *     warning (read the stats).  There is no CPU fallback: without a CUDA device every compute
+ *     call returns HZ_ERR_CUDA.
+ */
+#ifndef HZ_H_
+#define HZ_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HZ_OK = 0,
+  HZ_NOT_CONVERGED = 1,    /* solve: max_iter reached; x holds the best (last) iterate   */
+  HZ_BREAKDOWN = 2,        /* solve: BiCGSTAB breakdown persisted after restarts                 */
+  HZ_WARN_CLAMPED = 3,     /* assemble: some points had G outside the table range (clamped)      */
+  HZ_ERR_INVALID_ARG = -1, /* bad sizes / NULL pointers / inconsistent grid                          */
+  HZ_ERR_DOMAIN = -2,      /* v <= 0 or non-finite, f <= 0, h <= 0       */
+  HZ_ERR_RANK = -3,        /* weight LS singular (e.g. lambda = 0 with rank-3 blocks, A14)          */
+  HZ_ERR_OOM = -4,
+  HZ_ERR_CUDA = -5,
+  HZ_ERR_NCCL = -6,
+  HZ_ERR_SOURCE_IN_PML = -7 /* point source inside the PML                              */
+} hz_status;
+
+typedef enum { HZ_C64 = 0, HZ_C128 = 1 } hz_dtype;
+
+/* Mass formulation: Eq. 8 (per-neighbour kappa, default A5) or the collocation-kappa
+ * variant "Eq. 10". */
+typedef enum { HZ_MASS_EQ8 = 0, HZ_MASS_COLLOC = 1 } hz_mass;
+
+typedef struct hz_ctx hz_ctx;
+typedef struct hz_table hz_table;
+typedef struct hz_coeffs hz_coeffs;
+
+const char* hz_last_error(void);
+const char* hz_version(void);
+
+/* ---------------------------------------------------------------------------------------------
+ * Context: one per rank (process).  nranks > 1 creates an NCCL communicator from `id` (obtained
+ * on rank 0 with hz_get_unique_id and broadcast by the caller, e.g. through torch.distributed);
+ * the library owns the communicator and its streams.  nranks == 1 needs no id (may be NULL).
+ * ------------------------------------------------------------------------------------------- */
+hz_status hz_get_unique_id(unsigned char id[128]);
+hz_status hz_ctx_create(int cuda_device, int nranks, int rank, const unsigned char* id, hz_ctx** out);
+void hz_ctx_destroy(hz_ctx* ctx);
+
+/* ---------------------------------------------------------------------------------------------
+ * (1) build_weight_table — host, fp64 inputs, long-double arithmetic, deterministic.
+ * Tabulates G_i = g_min + i*dg, i = 0..n_g-1 (n_g = round((g_max-g_min)/dg)+1) and solves
+ *   min_w ||H w - g||^2 + lambda ||D P w||^2
+ * with per-G blocks of rows H_l(G_i, theta_j, phi_k), g (Eq. linear_basic; H2 with the
+ * "+1" of reading A1), phi outer / theta inner, D = first differences along G with no
+ * boundary rows (A11).  Unknowns per G: (ws1, ws2, mu0, mu1, mu2) (A2).
+ * angles == NULL: theta, phi in {0,10,20,30,40} degrees (A10).
+ * Errors: HZ_ERR_INVALID_ARG (n_g < 2, dg <= 0, g_min <= 2), HZ_ERR_RANK (singular system).
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  int n_theta, n_phi;
+  const double* theta_rad; /* [n_theta] */
+  const double* phi_rad;   /* [n_phi]   */
+} hz_angles;
+
+hz_status hz_build_weight_table(double g_min, double g_max, double dg, double lambda,
+                                const hz_angles* angles, hz_table** out);
+
+/* Import a table from rows (ws1, ws2, mu0, mu1, mu2) [n_g][5] at G_i = g_min + i*dg (shared-table
+ * parity; n_g == 1 gives the non-adaptive G4 / Gm stencils of P:273 as one-row tables). */
+hz_status hz_table_import(double g_min, double dg, int n_g, const double* rows5, hz_table** out);
+
+/* Export: n_g, and optionally rows5 [n_g][5] and class weights rows7 [n_g][7] =
+ * (ws1, ws2, ws3, wm0, wm1, wm2, wm3) with ws3 = 1-ws1-ws2, wm_k = (mu0, 6 mu1, 12 mu2),
+ * wm3 = 1 - wm0 - wm1 - wm2.  Either array may be NULL. */
+hz_status hz_table_rows(const hz_table* t, int* n_g, double* rows5, double* rows7);
+void hz_table_destroy(hz_table* t);
+
+/* ---------------------------------------------------------------------------------------------
+ * (2) assemble_coeffs — device.  Copies v (with one halo plane per side, exchanged with the
+ * neighbouring ranks) into library memory, validates it, counts clamped points, builds the 1-D
+ * PML arrays (profile A7, per-axis stretching A8) and uploads the table.  The per-point
+ * coefficients (G = v/(f h), lookup + interpolation, t0..t2, mu0..mu3) are
+ * NOT stored: every apply recomputes them from v (fused mode, 4 bytes/point).
+ * grid: this rank's slab of the global grid.  pml->v_pml <= 0 selects max(v) over all ranks.
+ * With nranks > 1 the table rows of rank 0 are broadcast so every rank uses identical weights.
+ * Returns HZ_WARN_CLAMPED (outputs valid) when *n_clamped > 0.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  int nx, ny, nz_global; /* global grid including the PML pad                  */
+  int z0, nz_local;      /* this rank's planes [z0, z0 + nz_local)               */
+  double h;              /* grid interval (m)                                    */
+  int v_halo;            /* 0: v is [nz_local][ny][nx] and its halo planes come from the neighbour
+                            ranks (NCCL); 1: v is [nz_local+2][ny][nx] and already holds planes
+                            z0-1 and z0+nz_local (ignored where they fall outside the grid) — lets
+                            one process emulate a z-slab decomposition                          */
+} hz_grid;
+
+typedef struct {
+  int npml;        /* PML width in nodes on every face (0 = no PML)                         */
+  double r_coeff;  /* target reflection coefficient R (A7); 1 => gamma = 0 (transparent)   */
+  double v_pml;    /* velocity in the gamma profile; <= 0 => max(v)                         */
+} hz_pml;
+
+hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, const void* v,
+                             double freq_hz, const hz_pml* pml, const hz_table* table, hz_mass mass,
+                             hz_coeffs** out, long long* n_clamped);
+
+/* Parity export (not on the hot path).  record: [8][nz_local][ny][nx] real (float for C64, double
+ * for C128) = (k^2 = (2 pi f / v)^2, t0, t1, t2, mu0, mu1, mu2, mu3) per point (may be NULL).
+ * pml: complex128 host array [3 axes x,y,z][2 (a-, a+)][nmax] with a-(i) = 1/(h^2 xi(i) xi(i-1/2)),
+ * a+(i) = 1/(h^2 xi(i) xi(i+1/2)); nmax >= max(nx, ny, nz_global) (may be NULL). */
+hz_status hz_coeffs_export(const hz_coeffs* c, void* record, void* pml_host, int nmax);
+void hz_coeffs_destroy(hz_coeffs* c);
+
+/* ---------------------------------------------------------------------------------------------
+ * (3) apply_impedance — Au = [M + S] u for nrhs fields, matrix-free, asynchronous on
+ * `stream`.  u and au: [nrhs][nz_local+2][ny][nx] complex of the coeffs' dtype.  u's halo planes
+ * are overwritten with the neighbouring ranks' boundary planes (nranks > 1); planes outside the
+ * global grid are treated as zero (Dirichlet, A9) and never read.  au's halo planes are not written.
+ * Row n of the operator (interior class-sum form; PML rows add the stretched per-axis terms):
+ *   (Au)_n = omega^2 sum_d mu_{|d|}(w_n) u_{n+d} / v_{n+d}^2                 (Eq. 8)
+ *          + sum_a sum_e D_a(n_a, e) sum_{p,q} T(p,q; w_n) u_{n + e e_a + p e_b + q e_c}   (A6, A8)
+ * ------------------------------------------------------------------------------------------- */
+hz_status hz_apply_impedance(const hz_coeffs* c, void* u, void* au, int nrhs, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * (4) solve — batched BiCGSTAB for A x_r = b_r, r = 0..nrhs-1 (north star (3)); blocking.
+ * b, x: [nrhs][nz_local+2][ny][nx]; x holds the initial guess on entry (zeros OK) and the final
+ * iterate on exit.  Each RHS iterates independently (per-RHS scalars on the device, fp64 dot
+ * accumulation, residual replacement every replace_every iterations) and stops when its
+ * recomputed TRUE residual ||b - A x|| / ||b|| <= rtol (A21).  relres_out[nrhs] receives the true
+ * relative residual and iters_out[nrhs] the iteration count (either may be NULL).
+ * Returns HZ_OK, HZ_NOT_CONVERGED or HZ_BREAKDOWN (outputs valid), or an error.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  double rtol;       /* default 1e-6                                               */
+  int max_iter;      /* default 20000                                              */
+  int replace_every; /* residual replacement period, default 50                    */
+  int check_every;   /* host convergence poll period, default 10                   */
+  int timing;        /* 1 = time every operator-apply launch with CUDA events      */
+} hz_solve_opts;
+
+typedef struct {
+  double apply_ms_total;   /* sum of operator-apply kernel durations (timing = 1)        */
+  long long apply_launches;/* number of operator-apply kernel launches                    */
+  long long kernel_launches;/* all libhz kernel launches during the call                  */
+  double bytes_per_apply;  /* algorithmic bytes of one apply launch (all active RHS)       */
+  int replacements;        /* residual replacements performed                             */
+  int restarts;            /* breakdown restarts                                          */
+} hz_solve_stats;
+
+hz_status hz_solve(const hz_coeffs* c, const void* b, void* x, int nrhs, const hz_solve_opts* opts,
+                   double* relres_out, int* iters_out, hz_solve_stats* stats, void* stream);
+
+/* Point-source RHS (reading A15).  node_xyz: GLOBAL node indices [nsrc][3] (x, y, z);
+ * amp_re_im: [nsrc][2] (NULL = unit amplitudes).  consistent = 1: b_n = amp mu_{|n-s|}(w_n)/h^3 on
+ * the 27 nodes around s (row n's own weights); 0: nodal amp/h^3.  b: [nsrc][nz_local+2][ny][nx],
+ * zero-filled by the call, entries outside this rank's slab skipped.  HZ_ERR_SOURCE_IN_PML if a
+ * source lies inside the PML. */
+hz_status hz_point_sources(const hz_coeffs* c, int nsrc, const long long* node_xyz,
+                           const double* amp_re_im, int consistent, void* b, void* stream);
+
+/* Number of libhz kernels launched since process start (evidence for the bench's gpu_launches). */
+long long hz_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HZ_H_ */

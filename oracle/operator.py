@@ -129,42 +129,50 @@ class Problem:
                 pml_axis(nz, self.npml, self.h, self.omega, vp, self.r_coeff))
 
 
-def assemble(prob: Problem, coef: Optional[PointCoefficients] = None) -> sp.csr_matrix:
-    """Explicit sparse impedance matrix A = M + S, one row per node, ≤ 27 entries.
-
-    Entry (n, n+d) = ω² mu_{class(d)}(w_n) / v²_{n+d}                      (Eq. 8)
-                   + Σ_a D_a(n_a, d_a) · T(d_⊥1, d_⊥2; t(w_n))               (reading A6/A8)
+def _entry(prob: Problem, coef: PointCoefficients, pml, K, J, I, d):
+    """Value of A[n, n+d] for the nodes n = (K, J, I) (arrays) and one offset d = (dz, dy, dx):
+         ω² mu_{class(d)}(w_n) / v²_{n+d}                                   (Eq. 8)
+       + Σ_a D_a(n_a, d_a) · T(d_⊥1, d_⊥2; t(w_n))                          (readings A6, A8)
     with D_a(i, −1) = a⁻_a(i), D_a(i, +1) = a⁺_a(i), D_a(i, 0) = −a⁻_a(i) − a⁺_a(i).
-    Out-of-grid neighbours are dropped (Dirichlet, A9).  Node index n = (z·ny + y)·nx + x.
-    """
-    if coef is None:
-        coef = prob.coefficients()
-    v = np.asarray(prob.v, dtype=np.float64)
+    `coef` holds the row coefficients at the same nodes.  Also returns the in-grid mask."""
+    dz, dy, dx = d
+    v = prob.v
     nz, ny, nx = v.shape
-    N = nx * ny * nz
-    w2 = prob.omega ** 2
-    (amx, apx), (amy, apy), (amz, apz) = prob.pml()
+    (amx, apx), (amy, apy), (amz, apz) = pml
     Dx = {-1: amx, 1: apx, 0: -amx - apx}
     Dy = {-1: amy, 1: apy, 0: -amy - apy}
     Dz = {-1: amz, 1: apz, 0: -amz - apz}
+    kk, jj, ii = K + dz, J + dy, I + dx
+    ok = (kk >= 0) & (kk < nz) & (jj >= 0) & (jj < ny) & (ii >= 0) & (ii < nx)
+    c = mass_class(d)
+    kk_c, jj_c, ii_c = np.clip(kk, 0, nz - 1), np.clip(jj, 0, ny - 1), np.clip(ii, 0, nx - 1)
+    w2 = prob.omega ** 2
+    if prob.mass == "eq8":
+        mass = w2 * coef.mu[..., c] / v[kk_c, jj_c, ii_c] ** 2
+    elif prob.mass == "colloc":
+        mass = w2 * coef.mu[..., c] / v[K, J, I] ** 2          # Eq. "10" (P:124), κ0 for all 27
+    else:
+        raise ValueError(prob.mass)
+    stiff = (Dx[dx][I] * T_weight(dy, dz, coef.t0, coef.t1, coef.t2)
+             + Dy[dy][J] * T_weight(dx, dz, coef.t0, coef.t1, coef.t2)
+             + Dz[dz][K] * T_weight(dx, dy, coef.t0, coef.t1, coef.t2))
+    return mass + stiff, ok, (kk, jj, ii)
+
+
+def assemble(prob: Problem, coef: Optional[PointCoefficients] = None) -> sp.csr_matrix:
+    """Explicit sparse impedance matrix A = M + S, one row per node, ≤ 27 entries
+    (values from `_entry`).  Out-of-grid neighbours are dropped (Dirichlet, A9).
+    Node index n = (z·ny + y)·nx + x."""
+    if coef is None:
+        coef = prob.coefficients()
+    nz, ny, nx = prob.v.shape
+    N = nx * ny * nz
+    pml = prob.pml()
     K, J, I = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
     rows_all, cols_all, vals_all = [], [], []
     n_idx = (K * ny + J) * nx + I
-    for (dz, dy, dx) in OFFSETS:
-        kk, jj, ii = K + dz, J + dy, I + dx
-        ok = (kk >= 0) & (kk < nz) & (jj >= 0) & (jj < ny) & (ii >= 0) & (ii < nx)
-        c = mass_class((dz, dy, dx))
-        kk_c, jj_c, ii_c = np.clip(kk, 0, nz - 1), np.clip(jj, 0, ny - 1), np.clip(ii, 0, nx - 1)
-        if prob.mass == "eq8":
-            mass = w2 * coef.mu[..., c] / v[kk_c, jj_c, ii_c] ** 2
-        elif prob.mass == "colloc":
-            mass = w2 * coef.mu[..., c] / v ** 2          # Eq. "10" (P:124), κ0 for all 27
-        else:
-            raise ValueError(prob.mass)
-        stiff = (Dx[dx][I] * T_weight(dy, dz, coef.t0, coef.t1, coef.t2)
-                 + Dy[dy][J] * T_weight(dx, dz, coef.t0, coef.t1, coef.t2)
-                 + Dz[dz][K] * T_weight(dx, dy, coef.t0, coef.t1, coef.t2))
-        val = mass + stiff
+    for d in OFFSETS:
+        val, ok, (kk, jj, ii) = _entry(prob, coef, pml, K, J, I, d)
         rows_all.append(n_idx[ok])
         cols_all.append(((kk * ny + jj) * nx + ii)[ok])
         vals_all.append(np.asarray(val)[ok])
@@ -175,6 +183,23 @@ def assemble(prob: Problem, coef: Optional[PointCoefficients] = None) -> sp.csr_
     A = sp.csr_matrix((vals, (rows.astype(idx_t), cols.astype(idx_t))), shape=(N, N))
     A.sort_indices()
     return A
+
+
+def apply_rows(prob: Problem, u: np.ndarray, nodes) -> np.ndarray:
+    """(Au)_n for selected nodes only (sampled parity at sizes where the full matrix is too big):
+    the same row entries as `assemble`, evaluated row by row.  u: [nz][ny][nx]; nodes: [m][3] as
+    (x, y, z).  Returns [m] complex128."""
+    nodes = np.asarray(nodes, dtype=np.int64).reshape(-1, 3)
+    I, J, K = nodes[:, 0], nodes[:, 1], nodes[:, 2]
+    coef = point_coefficients(prob.v[K, J, I], prob.freq, prob.h, prob.table)
+    pml = prob.pml()
+    nz, ny, nx = prob.v.shape
+    out = np.zeros(len(nodes), dtype=np.complex128)
+    for d in OFFSETS:
+        val, ok, (kk, jj, ii) = _entry(prob, coef, pml, K, J, I, d)
+        uu = u[np.clip(kk, 0, nz - 1), np.clip(jj, 0, ny - 1), np.clip(ii, 0, nx - 1)].astype(np.complex128)
+        out += np.where(ok, val * uu, 0.0)
+    return out
 
 
 def apply(A: sp.csr_matrix, u: np.ndarray) -> np.ndarray:

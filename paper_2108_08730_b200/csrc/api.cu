@@ -1,0 +1,955 @@
+// libhz C ABI (include/hz.h): contexts, tables, coefficient assembly, apply, batched BiCGSTAB,
+// point sources; z-slab halo exchange and dot-product allreduce over NCCL for nranks > 1.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "hz_internal.h"
+#include "kernels.h"
+
+// ---------------------------------------------------------------------------------------------
+// errors and counters
+// ---------------------------------------------------------------------------------------------
+namespace hz {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+static std::atomic<long long> g_launches{0};
+static inline void count_launch(long long n = 1) { g_launches += n; }
+}  // namespace hz
+
+using namespace hz;
+
+#define HZ_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      set_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call);     \
+      return e_ == cudaErrorMemoryAllocation ? HZ_ERR_OOM : HZ_ERR_CUDA;                    \
+    }                                                                                      \
+  } while (0)
+
+#define HZ_TRY(call)                   \
+  do {                                 \
+    hz_status s_ = (call);             \
+    if (s_ < 0) return s_;             \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------------
+// NCCL, loaded on demand (nranks > 1 only) so that libhz loads without NCCL on the path
+// ---------------------------------------------------------------------------------------------
+namespace {
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+#define SYM(f) f = reinterpret_cast<decltype(f)>(dlsym(h, "nccl" #f))
+    SYM(GetUniqueId); SYM(CommInitRank); SYM(CommDestroy); SYM(AllReduce); SYM(Broadcast);
+    SYM(Send); SYM(Recv); SYM(GroupStart); SYM(GroupEnd); SYM(GetErrorString);
+#undef SYM
+    return GetUniqueId && CommInitRank && AllReduce && Send && Recv && GroupStart && GroupEnd;
+  }
+};
+Nccl g_nccl;
+
+hz_status nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return HZ_OK;
+  set_error(std::string("NCCL error in ") + what + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+  return HZ_ERR_NCCL;
+}
+
+bool is_device_ptr(const void* p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// RAII device buffer
+struct DBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~DBuf() { if (p) cudaFree(p); }
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// objects
+// ---------------------------------------------------------------------------------------------
+struct hz_ctx {
+  int device = 0, nranks = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+};
+
+struct hz_table {
+  Table t;
+};
+
+struct SolverWork {
+  int nrhs = 0;
+  DBuf rhat, p, v, t, r;        // fields [nrhs][nzl+2][ny][nx]
+  DBuf dotA, dotB, dotR, dotN;  // fp64 dot buffers
+  DBuf state, active;
+  DBuf partials, tickets;
+  DBuf hb, hx;                  // staging for host b / x
+};
+
+struct hz_coeffs {
+  hz_ctx* ctx = nullptr;
+  hz_dtype dtype = HZ_C64;
+  hz_grid grid{};
+  hz_mass mass = HZ_MASS_EQ8;
+  double freq = 0, omega = 0, h = 0;
+  double v_pml = 0;
+  hz_pml pml{};
+  Table table;                 // host copy actually used (rank 0's on all ranks)
+  int n_g_dev = 0;             // rows uploaded (>= 2)
+  double g_min = 0, g_max = 0, dg = 0;
+  DBuf v;                      // [nzl+2][ny][nx] R
+  DBuf tab;                    // [n_g_dev][TAB_STRIDE] R
+  DBuf pml_d[6];               // dm x,y,z ; dp x,y,z (complex R)
+  int lo[3], hi[3];
+  std::vector<std::complex<double>> am_h[3], ap_h[3];  // host copies for export
+  DBuf partials, tickets;      // apply epilogue scratch
+  int zc = 1, nchunks = 1;
+  long long nlanes = 0;
+  std::unique_ptr<SolverWork> work;
+  size_t esz() const { return dtype == HZ_C64 ? 4 : 8; }   // real element size
+  long long plane() const { return (long long)grid.nx * grid.ny; }
+  long long fstride() const { return (long long)(grid.nz_local + 2) * plane(); }
+};
+
+extern "C" {
+
+const char* hz_last_error(void) { return g_err.c_str(); }
+const char* hz_version(void) { return "libhz 0.1 (sm_100a)"; }
+long long hz_kernel_launch_count(void) { return g_launches.load(); }
+
+hz_status hz_get_unique_id(unsigned char id[128]) {
+  if (!id) { set_error("hz_get_unique_id: id is NULL"); return HZ_ERR_INVALID_ARG; }
+  if (!g_nccl.load()) { set_error("hz_get_unique_id: cannot load libnccl.so.2"); return HZ_ERR_NCCL; }
+  ncclUniqueId u;
+  HZ_TRY(nccl_check(g_nccl.GetUniqueId(&u), "ncclGetUniqueId"));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(id, &u, 128);
+  return HZ_OK;
+}
+
+hz_status hz_ctx_create(int cuda_device, int nranks, int rank, const unsigned char* id, hz_ctx** out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) { set_error("hz_ctx_create: bad arguments"); return HZ_ERR_INVALID_ARG; }
+  int ndev = 0;
+  HZ_CUDA(cudaGetDeviceCount(&ndev));
+  if (cuda_device < 0 || cuda_device >= ndev) { set_error("hz_ctx_create: bad device"); return HZ_ERR_INVALID_ARG; }
+  HZ_CUDA(cudaSetDevice(cuda_device));
+  std::unique_ptr<hz_ctx> c(new hz_ctx);
+  c->device = cuda_device;
+  c->nranks = nranks;
+  c->rank = rank;
+  if (nranks > 1) {
+    if (!id) { set_error("hz_ctx_create: nranks > 1 needs a unique id"); return HZ_ERR_INVALID_ARG; }
+    if (!g_nccl.load()) { set_error("hz_ctx_create: cannot load libnccl.so.2"); return HZ_ERR_NCCL; }
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    HZ_TRY(nccl_check(g_nccl.CommInitRank(&c->comm, nranks, u, rank), "ncclCommInitRank"));
+  }
+  *out = c.release();
+  return HZ_OK;
+}
+
+void hz_ctx_destroy(hz_ctx* c) {
+  if (!c) return;
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  delete c;
+}
+
+// ---------------------------------------------------------------------------------------------
+// (1) weight table
+// ---------------------------------------------------------------------------------------------
+hz_status hz_build_weight_table(double g_min, double g_max, double dg, double lambda, const hz_angles* angles,
+                                hz_table** out) {
+  if (!out) { set_error("hz_build_weight_table: out is NULL"); return HZ_ERR_INVALID_ARG; }
+  std::vector<double> th, ph;
+  if (angles) {
+    if (angles->n_theta < 1 || angles->n_phi < 1 || !angles->theta_rad || !angles->phi_rad) {
+      set_error("hz_build_weight_table: bad angle grid");
+      return HZ_ERR_INVALID_ARG;
+    }
+    th.assign(angles->theta_rad, angles->theta_rad + angles->n_theta);
+    ph.assign(angles->phi_rad, angles->phi_rad + angles->n_phi);
+  } else {
+    for (int k = 0; k < 5; k++) {
+      th.push_back(k * 10.0 * M_PI / 180.0);   // reading A10
+      ph.push_back(k * 10.0 * M_PI / 180.0);
+    }
+  }
+  std::unique_ptr<hz_table> t(new hz_table);
+  HZ_TRY(build_table(g_min, g_max, dg, lambda, th, ph, &t->t));
+  *out = t.release();
+  return HZ_OK;
+}
+
+hz_status hz_table_import(double g_min, double dg, int n_g, const double* rows5, hz_table** out) {
+  if (!out || !rows5 || n_g < 1 || !(dg > 0) || !std::isfinite(g_min)) {
+    set_error("hz_table_import: bad arguments");
+    return HZ_ERR_INVALID_ARG;
+  }
+  for (long long i = 0; i < 5LL * n_g; i++)
+    if (!std::isfinite(rows5[i])) { set_error("hz_table_import: non-finite weight"); return HZ_ERR_DOMAIN; }
+  std::unique_ptr<hz_table> t(new hz_table);
+  t->t.g_min = g_min;
+  t->t.dg = dg;
+  t->t.n_g = n_g;
+  t->t.rows5.assign(rows5, rows5 + 5LL * n_g);
+  *out = t.release();
+  return HZ_OK;
+}
+
+hz_status hz_table_rows(const hz_table* t, int* n_g, double* rows5, double* rows7) {
+  if (!t) { set_error("hz_table_rows: NULL table"); return HZ_ERR_INVALID_ARG; }
+  if (n_g) *n_g = t->t.n_g;
+  for (int i = 0; i < t->t.n_g; i++) {
+    const double* w = &t->t.rows5[5 * i];
+    if (rows5) memcpy(rows5 + 5 * i, w, 5 * sizeof(double));
+    if (rows7) {
+      double* o = rows7 + 7 * i;
+      o[0] = w[0];
+      o[1] = w[1];
+      o[2] = 1.0 - w[0] - w[1];           // ws3
+      o[3] = w[2];                        // wm0 = mu0
+      o[4] = 6.0 * w[3];                  // wm1 = 6 mu1 (A2)
+      o[5] = 12.0 * w[4];                 // wm2 = 12 mu2
+      o[6] = 1.0 - o[3] - o[4] - o[5];    // wm3
+    }
+  }
+  return HZ_OK;
+}
+
+void hz_table_destroy(hz_table* t) { delete t; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// helpers on coeffs
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+// 1-D PML coefficients of one axis (A7, A8), in double on the host.
+void pml_axis(int n, int npml, double h, double omega, double v_pml, double R,
+              std::vector<std::complex<double>>& am, std::vector<std::complex<double>>& ap) {
+  am.resize(n);
+  ap.resize(n);
+  auto gamma = [&](double s) {
+    if (npml <= 0) return 0.0;
+    const double L = npml * h;
+    const double d = h * std::fmax(0.0, std::fmax(npml - s, s - (n - 1 - npml)));
+    return 1.5 * v_pml / L * std::log(1.0 / R) * (d / L) * (d / L);
+  };
+  auto xi = [&](double s) { return std::complex<double>(1.0, gamma(s) / omega); };
+  for (int i = 0; i < n; i++) {
+    am[i] = 1.0 / (h * h * xi(i) * xi(i - 0.5));
+    ap[i] = 1.0 / (h * h * xi(i) * xi(i + 0.5));
+  }
+}
+
+template <typename R>
+ApplyParams<R> make_params(const hz_coeffs* c) {
+  typedef typename Cx<R>::T C;
+  ApplyParams<R> p;
+  memset(&p, 0, sizeof(p));
+  p.nx = c->grid.nx;
+  p.ny = c->grid.ny;
+  p.nzl = c->grid.nz_local;
+  p.z0 = c->grid.z0;
+  p.nzg = c->grid.nz_global;
+  p.plane = c->plane();
+  p.fstride = c->fstride();
+  p.nlanes = c->nlanes;
+  p.zc = c->zc;
+  p.nchunks = c->nchunks;
+  p.v = c->v.as<R>();
+  p.tab = c->tab.as<R>();
+  p.n_g = c->n_g_dev;
+  p.g_min = (R)c->g_min;
+  p.g_max = (R)c->g_max;
+  p.inv_dg = (R)(1.0 / c->dg);
+  p.inv_fh = (R)(1.0 / (c->freq * c->h));
+  p.ih2 = (R)(1.0 / (c->h * c->h));
+  p.w2 = (R)(c->omega * c->omega);
+  for (int a = 0; a < 3; a++) {
+    p.dm[a] = c->pml_d[a].as<C>();
+    p.dp[a] = c->pml_d[3 + a].as<C>();
+    p.lo[a] = c->lo[a];
+    p.hi[a] = c->hi[a];
+  }
+  return p;
+}
+
+// Exchange the boundary planes of `field` ([nrhs][nzl+2][ny][nx] complex) with the z neighbours.
+hz_status halo_exchange(const hz_coeffs* c, void* field, int nrhs, size_t elem_bytes, cudaStream_t s) {
+  const hz_ctx* ctx = c->ctx;
+  if (ctx->nranks == 1) return HZ_OK;
+  const size_t pb = (size_t)c->plane() * elem_bytes;
+  const int nzl = c->grid.nz_local;
+  char* base = reinterpret_cast<char*>(field);
+  HZ_TRY(nccl_check(g_nccl.GroupStart(), "ncclGroupStart"));
+  for (int r = 0; r < nrhs; r++) {
+    char* f = base + (size_t)r * (size_t)c->fstride() * elem_bytes;
+    if (ctx->rank > 0) {
+      g_nccl.Send(f + 1 * pb, pb, ncclChar, ctx->rank - 1, ctx->comm, s);
+      g_nccl.Recv(f + 0 * pb, pb, ncclChar, ctx->rank - 1, ctx->comm, s);
+    }
+    if (ctx->rank < ctx->nranks - 1) {
+      g_nccl.Send(f + (size_t)nzl * pb, pb, ncclChar, ctx->rank + 1, ctx->comm, s);
+      g_nccl.Recv(f + (size_t)(nzl + 1) * pb, pb, ncclChar, ctx->rank + 1, ctx->comm, s);
+    }
+  }
+  HZ_TRY(nccl_check(g_nccl.GroupEnd(), "ncclGroupEnd"));
+  return HZ_OK;
+}
+
+hz_status allreduce_sum(const hz_coeffs* c, double* buf, size_t n, cudaStream_t s) {
+  if (c->ctx->nranks == 1) return HZ_OK;
+  return nccl_check(g_nccl.AllReduce(buf, buf, n, ncclDouble, ncclSum, c->ctx->comm, s), "ncclAllReduce");
+}
+
+template <typename R>
+hz_status apply_launch(const hz_coeffs* c, ApplyParams<R>& p, int nrhs, int epi, cudaStream_t s) {
+  const int K = epi_k(epi);
+  if (K > 0) {
+    auto* cc = const_cast<hz_coeffs*>(c);
+    const long long nb = ((c->nlanes + 32LL * apply_warps<R>() - 1) / (32LL * apply_warps<R>())) * c->nchunks;
+    HZ_CUDA(cc->partials.ensure(sizeof(double) * (size_t)nb * K * nrhs));
+    if (cc->tickets.n < sizeof(unsigned) * (size_t)nrhs) {
+      HZ_CUDA(cc->tickets.ensure(sizeof(unsigned) * (size_t)nrhs));
+      HZ_CUDA(cudaMemsetAsync(cc->tickets.p, 0, cc->tickets.n, s));
+    }
+    p.partials = cc->partials.as<double>();
+    p.tickets = cc->tickets.as<unsigned>();
+  }
+  HZ_CUDA(launch_apply<R>(p, nrhs, c->mass == HZ_MASS_COLLOC, epi, s));
+  count_launch();
+  return HZ_OK;
+}
+
+template <typename R>
+hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double freq, const hz_pml* pml,
+                     const hz_table* table, hz_mass mass, hz_coeffs** out, long long* n_clamped) {
+  typedef typename Cx<R>::T C;
+  std::unique_ptr<hz_coeffs> c(new hz_coeffs);
+  c->ctx = ctx;
+  c->dtype = sizeof(R) == 4 ? HZ_C64 : HZ_C128;
+  c->grid = *g;
+  c->mass = mass;
+  c->freq = freq;
+  c->omega = 2.0 * M_PI * freq;
+  c->h = g->h;
+  c->pml = pml ? *pml : hz_pml{0, 1e-3, 0.0};
+  if (c->pml.npml < 0 || !(c->pml.r_coeff > 0) || c->pml.r_coeff > 1.0) {
+    set_error("hz_assemble_coeffs: need npml >= 0 and 0 < r_coeff <= 1");
+    return HZ_ERR_INVALID_ARG;
+  }
+  cudaStream_t s = 0;
+  const long long plane = c->plane();
+  const long long nloc = plane * g->nz_local;
+  // ---- table: rank 0's rows broadcast to all ranks (bitwise-identical weights everywhere)
+  c->table = table->t;
+  if (ctx->nranks > 1) {
+    DBuf tb;
+    const size_t nb = 5 * (size_t)c->table.n_g * sizeof(double);
+    HZ_CUDA(tb.ensure(nb));
+    HZ_CUDA(cudaMemcpy(tb.p, c->table.rows5.data(), nb, cudaMemcpyHostToDevice));
+    HZ_TRY(nccl_check(g_nccl.Broadcast(tb.p, tb.p, 5 * (size_t)c->table.n_g, ncclDouble, 0, ctx->comm, s), "ncclBroadcast"));
+    HZ_CUDA(cudaMemcpy(c->table.rows5.data(), tb.p, nb, cudaMemcpyDeviceToHost));
+  }
+  // device table rows: (t1, t2, mu0, mu1, mu2 | forward differences), t1 = ws2/12, t2 = ws3/8 (A6)
+  {
+    const Table& T = c->table;
+    const int ng = T.n_g < 2 ? 2 : T.n_g;
+    std::vector<double> u(5 * (size_t)ng);
+    for (int i = 0; i < ng; i++) {
+      const double* w = &T.rows5[5 * (size_t)(T.n_g < 2 ? 0 : i)];
+      u[5 * i + 0] = w[1] / 12.0;
+      u[5 * i + 1] = (1.0 - w[0] - w[1]) / 8.0;
+      u[5 * i + 2] = w[2];
+      u[5 * i + 3] = w[3];
+      u[5 * i + 4] = w[4];
+    }
+    std::vector<R> rows((size_t)ng * TAB_STRIDE, R(0));
+    for (int i = 0; i < ng; i++)
+      for (int k = 0; k < 5; k++) {
+        rows[(size_t)i * TAB_STRIDE + k] = (R)u[5 * i + k];
+        rows[(size_t)i * TAB_STRIDE + 5 + k] = (i + 1 < ng) ? (R)(u[5 * (i + 1) + k] - u[5 * i + k]) : R(0);
+      }
+    c->n_g_dev = ng;
+    c->g_min = T.g_min;
+    c->dg = T.dg;
+    c->g_max = T.n_g < 2 ? T.g_min + T.dg : T.g_min + T.dg * (T.n_g - 1);
+    if ((size_t)ng * TAB_STRIDE * sizeof(R) > 60 * 1024) {
+      set_error("hz_assemble_coeffs: table too large for shared memory");
+      return HZ_ERR_INVALID_ARG;
+    }
+    HZ_CUDA(c->tab.ensure(rows.size() * sizeof(R)));
+    HZ_CUDA(cudaMemcpy(c->tab.p, rows.data(), rows.size() * sizeof(R), cudaMemcpyHostToDevice));
+  }
+  // ---- velocity with halo planes
+  HZ_CUDA(c->v.ensure((size_t)(g->nz_local + 2) * plane * sizeof(R)));
+  {
+    R one = R(1);
+    std::vector<R> ones((size_t)plane, one);
+    HZ_CUDA(cudaMemcpy(c->v.as<R>(), ones.data(), plane * sizeof(R), cudaMemcpyHostToDevice));
+    HZ_CUDA(cudaMemcpy(c->v.as<R>() + (g->nz_local + 1) * plane, ones.data(), plane * sizeof(R), cudaMemcpyHostToDevice));
+  }
+  {
+    const cudaMemcpyKind kind = is_device_ptr(v_in) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (g->v_halo) {
+      const R* vin = reinterpret_cast<const R*>(v_in);
+      HZ_CUDA(cudaMemcpy(c->v.as<R>() + plane, vin + plane, nloc * sizeof(R), kind));
+      if (g->z0 > 0) HZ_CUDA(cudaMemcpy(c->v.as<R>(), vin, plane * sizeof(R), kind));
+      if (g->z0 + g->nz_local < g->nz_global)
+        HZ_CUDA(cudaMemcpy(c->v.as<R>() + (g->nz_local + 1) * plane, vin + (g->nz_local + 1) * plane, plane * sizeof(R), kind));
+    } else {
+      HZ_CUDA(cudaMemcpy(c->v.as<R>() + plane, v_in, nloc * sizeof(R), kind));
+    }
+  }
+  // ---- statistics: domain check, v range, clamps
+  DBuf st;
+  HZ_CUDA(st.ensure(4 * sizeof(unsigned long long)));
+  unsigned long long init[4] = {~0ULL, 0ULL, 0ULL, 0ULL};
+  HZ_CUDA(cudaMemcpy(st.p, init, sizeof(init), cudaMemcpyHostToDevice));
+  HZ_CUDA(launch_vstats<R>(c->v.as<R>() + plane, nloc, (R)(1.0 / (freq * g->h)), (R)c->g_min, (R)c->g_max,
+                           st.as<unsigned long long>(), s));
+  count_launch();
+  unsigned long long res[4];
+  HZ_CUDA(cudaMemcpy(res, st.p, sizeof(res), cudaMemcpyDeviceToHost));
+  double vmin, vmax;
+  {
+    long long bmin = (long long)res[0], bmax = (long long)res[1];
+    memcpy(&vmin, &bmin, 8);
+    memcpy(&vmax, &bmax, 8);
+  }
+  double stats[3] = {(double)res[2], (double)res[3], 0.0};
+  if (ctx->nranks > 1) {
+    DBuf sb;
+    HZ_CUDA(sb.ensure(4 * sizeof(double)));
+    double sv[4] = {stats[0], stats[1], vmax, -vmin};
+    HZ_CUDA(cudaMemcpy(sb.p, sv, sizeof(sv), cudaMemcpyHostToDevice));
+    HZ_TRY(nccl_check(g_nccl.AllReduce(sb.p, sb.p, 2, ncclDouble, ncclSum, ctx->comm, s), "ncclAllReduce"));
+    HZ_TRY(nccl_check(g_nccl.AllReduce(sb.as<double>() + 2, sb.as<double>() + 2, 2, ncclDouble, ncclMax, ctx->comm, s),
+                      "ncclAllReduce"));
+    HZ_CUDA(cudaMemcpy(sv, sb.p, sizeof(sv), cudaMemcpyDeviceToHost));
+    stats[0] = sv[0];
+    stats[1] = sv[1];
+    vmax = sv[2];
+    vmin = -sv[3];
+  }
+  if (stats[0] > 0) {
+    set_error("hz_assemble_coeffs: velocity has " + std::to_string((long long)stats[0]) +
+              " non-positive or non-finite values (S:156, S:252)");
+    return HZ_ERR_DOMAIN;
+  }
+  // ---- v halo planes from the neighbours
+  if (!g->v_halo) HZ_TRY(halo_exchange(c.get(), c->v.p, 1, sizeof(R), s));
+  // ---- PML (host, double) → device deltas δ± = a± − 1/h²
+  c->v_pml = (c->pml.v_pml > 0) ? c->pml.v_pml : vmax;
+  const int ns[3] = {g->nx, g->ny, g->nz_global};
+  const double ih2 = 1.0 / (g->h * g->h);
+  for (int a = 0; a < 3; a++) {
+    pml_axis(ns[a], c->pml.npml, g->h, c->omega, c->v_pml, c->pml.r_coeff, c->am_h[a], c->ap_h[a]);
+    std::vector<C> dm(ns[a]), dp(ns[a]);
+    int lo = ns[a], hi = -1;
+    for (int i = 0; i < ns[a]; i++) {
+      std::complex<double> m = c->am_h[a][i] - ih2, q = c->ap_h[a][i] - ih2;
+      dm[i].x = (R)m.real(); dm[i].y = (R)m.imag();
+      dp[i].x = (R)q.real(); dp[i].y = (R)q.imag();
+    }
+    // interior range: the longest run of exactly-zero deltas (contiguous by construction)
+    for (int i = 0; i < ns[a]; i++) {
+      bool z = (c->am_h[a][i] - ih2) == std::complex<double>(0, 0) && (c->ap_h[a][i] - ih2) == std::complex<double>(0, 0);
+      if (z) { if (i < lo) lo = i; hi = i; }
+    }
+    if (hi < lo) { lo = 1; hi = 0; }   // every node needs the correction
+    c->lo[a] = lo;
+    c->hi[a] = hi;
+    HZ_CUDA(c->pml_d[a].ensure(ns[a] * sizeof(C)));
+    HZ_CUDA(c->pml_d[3 + a].ensure(ns[a] * sizeof(C)));
+    HZ_CUDA(cudaMemcpy(c->pml_d[a].p, dm.data(), ns[a] * sizeof(C), cudaMemcpyHostToDevice));
+    HZ_CUDA(cudaMemcpy(c->pml_d[3 + a].p, dp.data(), ns[a] * sizeof(C), cudaMemcpyHostToDevice));
+  }
+  // ---- launch geometry: strips of NY rows; z chunks sized to give >= ~4 waves
+  {
+    const int NY = apply_ny<R>(), W = apply_warps<R>();
+    const long long nstrips = (g->ny + NY - 1) / NY;
+    c->nlanes = nstrips * g->nx;
+    const long long bx = (c->nlanes + 32LL * W - 1) / (32LL * W);
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const long long target = 4LL * dev_sms * apply_occupancy<R>(mass == HZ_MASS_COLLOC);
+    long long nch = (target + bx - 1) / bx;
+    const long long maxch = std::max(1, g->nz_local / 8);
+    nch = std::max(1LL, std::min(nch, maxch));
+    c->zc = (int)((g->nz_local + nch - 1) / nch);
+    c->nchunks = (g->nz_local + c->zc - 1) / c->zc;
+  }
+  if (n_clamped) *n_clamped = (long long)stats[1];
+  *out = c.release();
+  return stats[1] > 0 ? HZ_WARN_CLAMPED : HZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, const void* v, double freq_hz,
+                             const hz_pml* pml, const hz_table* table, hz_mass mass, hz_coeffs** out,
+                             long long* n_clamped) {
+  if (!ctx || !grid || !v || !table || !out) { set_error("hz_assemble_coeffs: NULL argument"); return HZ_ERR_INVALID_ARG; }
+  const hz_grid& g = *grid;
+  if (g.nx < 3 || g.ny < 3 || g.nz_global < 3 || g.nz_local < 1 || g.z0 < 0 || g.z0 + g.nz_local > g.nz_global) {
+    set_error("hz_assemble_coeffs: bad grid (dims >= 3, slab inside the global grid; S:156)");
+    return HZ_ERR_INVALID_ARG;
+  }
+  if (!(g.h > 0) || !(freq_hz > 0)) { set_error("hz_assemble_coeffs: need h > 0 and f > 0 (S:172)"); return HZ_ERR_DOMAIN; }
+  if (table->t.n_g < 1) { set_error("hz_assemble_coeffs: empty table"); return HZ_ERR_INVALID_ARG; }
+  if (ctx->nranks > 1 && g.nz_local < 1) { set_error("hz_assemble_coeffs: empty slab"); return HZ_ERR_INVALID_ARG; }
+  if (cudaSetDevice(ctx->device) != cudaSuccess) { set_error("hz_assemble_coeffs: cudaSetDevice failed"); return HZ_ERR_CUDA; }
+  if (dtype == HZ_C64) return assemble_t<float>(ctx, grid, v, freq_hz, pml, table, mass, out, n_clamped);
+  if (dtype == HZ_C128) return assemble_t<double>(ctx, grid, v, freq_hz, pml, table, mass, out, n_clamped);
+  set_error("hz_assemble_coeffs: bad dtype");
+  return HZ_ERR_INVALID_ARG;
+}
+
+void hz_coeffs_destroy(hz_coeffs* c) { delete c; }
+
+hz_status hz_coeffs_export(const hz_coeffs* c, void* record, void* pml_host, int nmax) {
+  if (!c) { set_error("hz_coeffs_export: NULL coeffs"); return HZ_ERR_INVALID_ARG; }
+  cudaStream_t s = 0;
+  if (record) {
+    const size_t nb = 8 * (size_t)c->plane() * c->grid.nz_local * c->esz();
+    const bool dev = is_device_ptr(record);
+    DBuf tmp;
+    void* dst = record;
+    if (!dev) {
+      HZ_CUDA(tmp.ensure(nb));
+      dst = tmp.p;
+    }
+    if (c->dtype == HZ_C64) {
+      auto p = make_params<float>(c);
+      HZ_CUDA(launch_record<float>(p, reinterpret_cast<float*>(dst), s));
+    } else {
+      auto p = make_params<double>(c);
+      HZ_CUDA(launch_record<double>(p, reinterpret_cast<double*>(dst), s));
+    }
+    count_launch();
+    HZ_CUDA(cudaStreamSynchronize(s));
+    if (!dev) HZ_CUDA(cudaMemcpy(record, tmp.p, nb, cudaMemcpyDeviceToHost));
+  }
+  if (pml_host) {
+    const int ns[3] = {c->grid.nx, c->grid.ny, c->grid.nz_global};
+    if (nmax < std::max(ns[0], std::max(ns[1], ns[2]))) { set_error("hz_coeffs_export: nmax too small"); return HZ_ERR_INVALID_ARG; }
+    std::complex<double>* o = reinterpret_cast<std::complex<double>*>(pml_host);
+    for (int a = 0; a < 3; a++)
+      for (int i = 0; i < nmax; i++) {
+        o[(size_t)(2 * a + 0) * nmax + i] = i < ns[a] ? c->am_h[a][i] : 0.0;
+        o[(size_t)(2 * a + 1) * nmax + i] = i < ns[a] ? c->ap_h[a][i] : 0.0;
+      }
+  }
+  return HZ_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// (3) apply
+// ---------------------------------------------------------------------------------------------
+template <typename R>
+static hz_status apply_t(const hz_coeffs* c, void* u, void* au, int nrhs, cudaStream_t s) {
+  typedef typename Cx<R>::T C;
+  const size_t fb = (size_t)c->fstride() * nrhs * sizeof(C);
+  const bool du = is_device_ptr(u), da = is_device_ptr(au);
+  DBuf tu, ta;
+  void* ud = u;
+  void* ad = au;
+  if (!du) { HZ_CUDA(tu.ensure(fb)); HZ_CUDA(cudaMemcpyAsync(tu.p, u, fb, cudaMemcpyHostToDevice, s)); ud = tu.p; }
+  if (!da) { HZ_CUDA(ta.ensure(fb)); ad = ta.p; }
+  HZ_TRY(halo_exchange(c, ud, nrhs, sizeof(C), s));
+  ApplyParams<R> p = make_params<R>(c);
+  p.u = reinterpret_cast<const C*>(ud);
+  p.au = reinterpret_cast<C*>(ad);
+  HZ_TRY(apply_launch<R>(c, p, nrhs, EPI_PLAIN, s));
+  if (!da) {
+    HZ_CUDA(cudaMemcpyAsync(au, ad, fb, cudaMemcpyDeviceToHost, s));
+    HZ_CUDA(cudaStreamSynchronize(s));
+  } else if (!du) {
+    HZ_CUDA(cudaStreamSynchronize(s));
+  }
+  return HZ_OK;
+}
+
+extern "C" hz_status hz_apply_impedance(const hz_coeffs* c, void* u, void* au, int nrhs, void* stream) {
+  if (!c || !u || !au || nrhs < 1) { set_error("hz_apply_impedance: bad arguments"); return HZ_ERR_INVALID_ARG; }
+  if (u == au) { set_error("hz_apply_impedance: u and au must not alias"); return HZ_ERR_INVALID_ARG; }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return c->dtype == HZ_C64 ? apply_t<float>(c, u, au, nrhs, s) : apply_t<double>(c, u, au, nrhs, s);
+}
+
+// ---------------------------------------------------------------------------------------------
+// point sources
+// ---------------------------------------------------------------------------------------------
+template <typename R>
+static hz_status sources_t(const hz_coeffs* c, int nsrc, const long long* nodes, const double* amps, int consistent,
+                           void* b, cudaStream_t s) {
+  typedef typename Cx<R>::T C;
+  const int np = c->pml.npml;
+  for (int i = 0; i < nsrc; i++) {
+    const long long X = nodes[3 * i], Y = nodes[3 * i + 1], Z = nodes[3 * i + 2];
+    if (X < 0 || X >= c->grid.nx || Y < 0 || Y >= c->grid.ny || Z < 0 || Z >= c->grid.nz_global) {
+      set_error("hz_point_sources: source outside the grid");
+      return HZ_ERR_INVALID_ARG;
+    }
+    if (X < np || X >= c->grid.nx - np || Y < np || Y >= c->grid.ny - np || Z < np || Z >= c->grid.nz_global - np) {
+      set_error("hz_point_sources: source " + std::to_string(i) + " lies inside the PML (S:262-266)");
+      return HZ_ERR_SOURCE_IN_PML;
+    }
+  }
+  const size_t fb = (size_t)c->fstride() * nsrc * sizeof(C);
+  const bool db = is_device_ptr(b);
+  DBuf tb, dn, da;
+  void* bd = b;
+  if (!db) { HZ_CUDA(tb.ensure(fb)); bd = tb.p; }
+  HZ_CUDA(dn.ensure(3 * sizeof(long long) * nsrc));
+  HZ_CUDA(cudaMemcpyAsync(dn.p, nodes, 3 * sizeof(long long) * nsrc, cudaMemcpyHostToDevice, s));
+  if (amps) {
+    HZ_CUDA(da.ensure(2 * sizeof(double) * nsrc));
+    HZ_CUDA(cudaMemcpyAsync(da.p, amps, 2 * sizeof(double) * nsrc, cudaMemcpyHostToDevice, s));
+  }
+  HZ_CUDA(cudaMemsetAsync(bd, 0, fb, s));
+  ApplyParams<R> p = make_params<R>(c);
+  const R ih3 = (R)(1.0 / (c->h * c->h * c->h));
+  HZ_CUDA(launch_sources<R>(p, nsrc, dn.as<long long>(), amps ? da.as<double>() : nullptr, consistent, ih3,
+                            reinterpret_cast<C*>(bd), s));
+  count_launch();
+  if (!db) HZ_CUDA(cudaMemcpyAsync(b, bd, fb, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  return HZ_OK;
+}
+
+extern "C" hz_status hz_point_sources(const hz_coeffs* c, int nsrc, const long long* node_xyz,
+                                      const double* amp_re_im, int consistent, void* b, void* stream) {
+  if (!c || nsrc < 1 || !node_xyz || !b) { set_error("hz_point_sources: bad arguments"); return HZ_ERR_INVALID_ARG; }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return c->dtype == HZ_C64 ? sources_t<float>(c, nsrc, node_xyz, amp_re_im, consistent, b, s)
+                            : sources_t<double>(c, nsrc, node_xyz, amp_re_im, consistent, b, s);
+}
+
+
+
+// ---------------------------------------------------------------------------------------------
+// (4) batched BiCGSTAB (north star (3); reading A21)
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+struct EventTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  size_t used = 0;
+  ~EventTimer() { for (auto e : ev) cudaEventDestroy(e); }
+  void mark(cudaStream_t s) {
+    if (!on) return;
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    cudaEventRecord(ev[used++], s);
+  }
+  double total_ms() {
+    double t = 0;
+    for (size_t i = 0; i + 1 < used; i += 2) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      t += ms;
+    }
+    return t;
+  }
+};
+
+template <typename R>
+hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, const hz_solve_opts& o,
+                  double* relres_out, int* iters_out, hz_solve_stats* stats, cudaStream_t s) {
+  typedef typename Cx<R>::T C;
+  hz_coeffs* c = const_cast<hz_coeffs*>(cc);
+  const long long launches0 = g_launches.load();
+  if (!c->work || c->work->nrhs != nrhs) c->work.reset(new SolverWork);
+  SolverWork& w = *c->work;
+  w.nrhs = nrhs;
+  const size_t fb = (size_t)c->fstride() * nrhs * sizeof(C);
+  HZ_CUDA(w.rhat.ensure(fb));
+  HZ_CUDA(w.p.ensure(fb));
+  HZ_CUDA(w.v.ensure(fb));
+  HZ_CUDA(w.t.ensure(fb));
+  HZ_CUDA(w.r.ensure(fb));
+  HZ_CUDA(w.dotA.ensure(sizeof(double) * 2 * nrhs));
+  HZ_CUDA(w.dotB.ensure(sizeof(double) * 7 * nrhs));
+  HZ_CUDA(w.dotR.ensure(sizeof(double) * 3 * nrhs));
+  HZ_CUDA(w.dotN.ensure(sizeof(double) * nrhs));
+  HZ_CUDA(w.state.ensure(sizeof(SolverState) * nrhs));
+  HZ_CUDA(w.active.ensure(sizeof(int) * nrhs));
+  const long long n = c->plane() * c->grid.nz_local;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->ctx->device);
+  const int vblocks = (int)std::max(1LL, std::min((n + 1023) / 1024, (long long)(8 * sms + nrhs - 1) / nrhs));
+  HZ_CUDA(w.partials.ensure(sizeof(double) * (size_t)vblocks * nrhs));
+  HZ_CUDA(w.tickets.ensure(sizeof(unsigned) * nrhs));
+  HZ_CUDA(cudaMemsetAsync(w.tickets.p, 0, sizeof(unsigned) * nrhs, s));
+  HZ_CUDA(cudaMemsetAsync(w.state.p, 0, sizeof(SolverState) * nrhs, s));
+  // host / device placement of b and x
+  const bool db = is_device_ptr(b_in), dx = is_device_ptr(x_in);
+  const C* b = reinterpret_cast<const C*>(b_in);
+  C* x = reinterpret_cast<C*>(x_in);
+  if (!db) {
+    HZ_CUDA(w.hb.ensure(fb));
+    HZ_CUDA(cudaMemcpyAsync(w.hb.p, b_in, fb, cudaMemcpyHostToDevice, s));
+    b = w.hb.as<C>();
+  }
+  if (!dx) {
+    HZ_CUDA(w.hx.ensure(fb));
+    HZ_CUDA(cudaMemcpyAsync(w.hx.p, x_in, fb, cudaMemcpyHostToDevice, s));
+    x = w.hx.as<C>();
+  }
+  std::vector<int> active(nrhs, 1), iters(nrhs, 0);
+  HZ_CUDA(cudaMemcpyAsync(w.active.p, active.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
+
+  EventTimer timer;
+  timer.on = o.timing != 0;
+  long long apply_launches = 0;
+  ApplyParams<R> base = make_params<R>(c);
+  base.active = w.active.as<int>();
+  VecParams<R> q;
+  memset(&q, 0, sizeof(q));
+  q.n = n;
+  q.plane = c->plane();
+  q.fstride = c->fstride();
+  q.nblocks = vblocks;
+  q.x = x;
+  q.r = w.r.as<C>();
+  q.rhat = w.rhat.as<C>();
+  q.p = w.p.as<C>();
+  q.v = w.v.as<C>();
+  q.t = w.t.as<C>();
+  q.dotA = w.dotA.as<double>();
+  q.dotB = w.dotB.as<double>();
+  q.dotR = w.dotR.as<double>();
+  q.partials = w.partials.as<double>();
+  q.tickets = w.tickets.as<unsigned>();
+  q.state = w.state.as<SolverState>();
+  q.active = w.active.as<int>();
+
+  // r = b − A x (RESID epilogue; writes r, ‖r‖², (r̂0, r))
+  auto resid = [&](bool with_rhat) -> hz_status {
+    HZ_TRY(halo_exchange(c, x, nrhs, sizeof(C), s));
+    ApplyParams<R> p = base;
+    p.u = x;
+    p.au = w.r.as<C>();
+    p.bvec = b;
+    p.rhat = with_rhat ? w.rhat.as<C>() : nullptr;
+    p.dots = w.dotR.as<double>();
+    timer.mark(s);
+    HZ_TRY(apply_launch<R>(c, p, nrhs, EPI_RESID, s));
+    timer.mark(s);
+    apply_launches++;
+    HZ_TRY(allreduce_sum(c, w.dotR.as<double>(), 3 * (size_t)nrhs, s));
+    return HZ_OK;
+  };
+  auto vec = [&](int which) -> hz_status {
+    HZ_CUDA(launch_bicg<R>(which, q, nrhs, s));
+    count_launch();
+    return HZ_OK;
+  };
+
+  // ‖b‖²
+  HZ_CUDA(launch_norm2<R>(b, c->fstride(), c->plane(), n, nrhs, vblocks, w.partials.as<double>(), w.dotN.as<double>(),
+                          w.tickets.as<unsigned>(), s));
+  count_launch();
+  HZ_TRY(allreduce_sum(c, w.dotN.as<double>(), nrhs, s));
+  std::vector<double> bn2(nrhs);
+  HZ_CUDA(cudaMemcpyAsync(bn2.data(), w.dotN.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  // RHS with b = 0: x = 0, converged
+  for (int r = 0; r < nrhs; r++)
+    if (!(bn2[r] > 0)) {
+      active[r] = 0;
+      HZ_CUDA(cudaMemsetAsync(x + (size_t)r * c->fstride(), 0, sizeof(C) * c->fstride(), s));
+    }
+  HZ_CUDA(cudaMemcpyAsync(w.active.p, active.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
+  const double rtol2 = o.rtol * o.rtol;
+  HZ_TRY(resid(false));
+  HZ_TRY(vec(BICG_INIT));
+
+  int restarts = 0, replacements = 0;
+  int it = 0;
+  std::vector<double> hdot(3 * nrhs);
+  std::vector<SolverState> hst(nrhs);
+  auto any_active = [&]() {
+    for (int r = 0; r < nrhs; r++)
+      if (active[r]) return true;
+    return false;
+  };
+  // initial convergence check (x0 may already solve the system)
+  HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  for (int r = 0; r < nrhs; r++)
+    if (active[r] && hdot[3 * r] <= rtol2 * bn2[r]) active[r] = 0;
+  HZ_CUDA(cudaMemcpyAsync(w.active.p, active.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
+
+  while (any_active() && it < o.max_iter) {
+    // v = A p, (r̂0, v)
+    HZ_TRY(halo_exchange(c, w.p.p, nrhs, sizeof(C), s));
+    {
+      ApplyParams<R> p = base;
+      p.u = w.p.as<C>();
+      p.au = w.v.as<C>();
+      p.rhat = w.rhat.as<C>();
+      p.dots = w.dotA.as<double>();
+      timer.mark(s);
+      HZ_TRY(apply_launch<R>(c, p, nrhs, EPI_DOT1, s));
+      timer.mark(s);
+      apply_launches++;
+      HZ_TRY(allreduce_sum(c, w.dotA.as<double>(), 2 * (size_t)nrhs, s));
+    }
+    HZ_TRY(vec(BICG_S));  // s = r − α v (in r)
+    // t = A s, (t,s), (t,t), (r̂0,s), (r̂0,t)
+    HZ_TRY(halo_exchange(c, w.r.p, nrhs, sizeof(C), s));
+    {
+      ApplyParams<R> p = base;
+      p.u = w.r.as<C>();
+      p.au = w.t.as<C>();
+      p.rhat = w.rhat.as<C>();
+      p.dots = w.dotB.as<double>();
+      timer.mark(s);
+      HZ_TRY(apply_launch<R>(c, p, nrhs, EPI_DOT4, s));
+      timer.mark(s);
+      apply_launches++;
+      HZ_TRY(allreduce_sum(c, w.dotB.as<double>(), 7 * (size_t)nrhs, s));
+    }
+    HZ_TRY(vec(BICG_UPDATE));  // x, r, p; ‖r‖²
+    HZ_TRY(allreduce_sum(c, w.dotR.as<double>(), 3 * (size_t)nrhs, s));
+    ++it;
+    for (int r = 0; r < nrhs; r++)
+      if (active[r]) iters[r]++;
+    if (o.replace_every > 0 && it % o.replace_every == 0) {
+      HZ_TRY(resid(true));
+      HZ_TRY(vec(BICG_RHO_RESET));
+      replacements++;
+    }
+    if (it % std::max(1, o.check_every) == 0 || it >= o.max_iter) {
+      HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
+      HZ_CUDA(cudaMemcpyAsync(hst.data(), w.state.p, sizeof(SolverState) * nrhs, cudaMemcpyDeviceToHost, s));
+      HZ_CUDA(cudaStreamSynchronize(s));
+      bool cand = false, brk = false;
+      for (int r = 0; r < nrhs; r++) {
+        if (!active[r]) continue;
+        if (hst[r].flags & 1) brk = true;
+        else if (hdot[3 * r] <= rtol2 * bn2[r]) cand = true;
+      }
+      if (brk) {  // restart broken RHS with r̂0 = r = b − A x (all active RHS restart together)
+        HZ_TRY(resid(false));
+        HZ_TRY(vec(BICG_INIT));
+        restarts++;
+        if (restarts > 50) break;
+        continue;
+      }
+      if (cand) {  // verify on the recomputed TRUE residual (A21)
+        HZ_TRY(resid(true));
+        HZ_TRY(vec(BICG_RHO_RESET));
+        replacements++;
+        HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
+        HZ_CUDA(cudaStreamSynchronize(s));
+        bool changed = false;
+        for (int r = 0; r < nrhs; r++)
+          if (active[r] && hdot[3 * r] <= rtol2 * bn2[r]) {
+            active[r] = 0;
+            changed = true;
+          }
+        if (changed) HZ_CUDA(cudaMemcpyAsync(w.active.p, active.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
+      }
+    }
+  }
+  // final true residuals for every RHS
+  std::vector<int> all(nrhs, 1);
+  HZ_CUDA(cudaMemcpyAsync(w.active.p, all.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
+  HZ_TRY(resid(false));
+  HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  bool conv = true;
+  for (int r = 0; r < nrhs; r++) {
+    const double rel = bn2[r] > 0 ? std::sqrt(hdot[3 * r] / bn2[r]) : 0.0;
+    if (relres_out) relres_out[r] = rel;
+    if (iters_out) iters_out[r] = iters[r];
+    if (!(rel <= o.rtol)) conv = false;
+  }
+  if (!dx) {
+    HZ_CUDA(cudaMemcpyAsync(x_in, x, fb, cudaMemcpyDeviceToHost, s));
+    HZ_CUDA(cudaStreamSynchronize(s));
+  }
+  if (stats) {
+    stats->apply_ms_total = timer.on ? timer.total_ms() : 0.0;
+    stats->apply_launches = apply_launches;
+    stats->kernel_launches = g_launches.load() - launches0;
+    stats->bytes_per_apply = (double)n * (double)(sizeof(R) + 2 * sizeof(C));
+    stats->replacements = replacements;
+    stats->restarts = restarts;
+  }
+  if (conv) return HZ_OK;
+  return restarts > 50 ? HZ_BREAKDOWN : HZ_NOT_CONVERGED;
+}
+
+}  // namespace
+
+extern "C" hz_status hz_solve(const hz_coeffs* c, const void* b, void* x, int nrhs, const hz_solve_opts* opts,
+                              double* relres_out, int* iters_out, hz_solve_stats* stats, void* stream) {
+  if (!c || !b || !x || nrhs < 1) { set_error("hz_solve: bad arguments"); return HZ_ERR_INVALID_ARG; }
+  hz_solve_opts o = {1e-6, 20000, 50, 10, 0};
+  if (opts) o = *opts;
+  if (!(o.rtol > 0) || o.max_iter < 1) { set_error("hz_solve: need rtol > 0, max_iter >= 1"); return HZ_ERR_INVALID_ARG; }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return c->dtype == HZ_C64 ? solve_t<float>(c, b, x, nrhs, o, relres_out, iters_out, stats, s)
+                            : solve_t<double>(c, b, x, nrhs, o, relres_out, iters_out, stats, s);
+}

@@ -1,0 +1,80 @@
+// Complex helpers for the sm_100a kernels.  complex64 arithmetic uses the packed FP32x2 pipe of
+// Blackwell (add/mul/fma.rn.f32x2 → SASS FADD2/FMUL2/FFMA2): a complex value is one 64-bit register
+// pair, so real×complex and complex+complex cost ONE instruction instead of two.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace hz {
+
+template <typename R> struct Cx;
+template <> struct Cx<float> { typedef float2 T; };
+template <> struct Cx<double> { typedef double2 T; };
+
+__device__ __forceinline__ unsigned long long f2_as_u64(float2 a) {
+  return *reinterpret_cast<unsigned long long*>(&a);
+}
+__device__ __forceinline__ float2 u64_as_f2(unsigned long long a) {
+  return *reinterpret_cast<float2*>(&a);
+}
+
+// ---- float2 (complex64) ---------------------------------------------------------------------
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
+  return u64_as_f2(d);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
+  return u64_as_f2(d);
+}
+// s * a (s real)
+__device__ __forceinline__ float2 cscale(float s, float2 a) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(make_float2(s, s))), "l"(f2_as_u64(a)));
+  return u64_as_f2(d);
+}
+// acc + s * a (s real)
+__device__ __forceinline__ float2 cfma(float s, float2 a, float2 acc) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(f2_as_u64(make_float2(s, s))), "l"(f2_as_u64(a)), "l"(f2_as_u64(acc)));
+  return u64_as_f2(d);
+}
+// complex * complex (slow paths only)
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 czero(float) { return make_float2(0.f, 0.f); }
+
+// ---- double2 (complex128) -------------------------------------------------------------------
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+__device__ __forceinline__ double2 cfma(double s, double2 a, double2 acc) {
+  return make_double2(fma(s, a.x, acc.x), fma(s, a.y, acc.y));
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 czero(double) { return make_double2(0.0, 0.0); }
+
+// ---- loads ------------------------------------------------------------------------------------
+__device__ __forceinline__ float2 ldg_c(const float2* p) { return __ldg(p); }
+__device__ __forceinline__ double2 ldg_c(const double2* p) { return __ldg(p); }
+
+__device__ __forceinline__ float2 shfl_up_c(float2 a, int d) {
+  return u64_as_f2(__shfl_up_sync(0xffffffffu, f2_as_u64(a), d));
+}
+__device__ __forceinline__ float2 shfl_down_c(float2 a, int d) {
+  return u64_as_f2(__shfl_down_sync(0xffffffffu, f2_as_u64(a), d));
+}
+__device__ __forceinline__ double2 shfl_up_c(double2 a, int d) {
+  return make_double2(__shfl_up_sync(0xffffffffu, a.x, d), __shfl_up_sync(0xffffffffu, a.y, d));
+}
+__device__ __forceinline__ double2 shfl_down_c(double2 a, int d) {
+  return make_double2(__shfl_down_sync(0xffffffffu, a.x, d), __shfl_down_sync(0xffffffffu, a.y, d));
+}
+
+}  // namespace hz

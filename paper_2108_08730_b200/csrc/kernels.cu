@@ -1,0 +1,615 @@
+// sm_100a kernels of libhz: fused coefficient + 27-point apply (with optional BiCGSTAB dot
+// epilogues), coefficient-record export, point sources, BiCGSTAB vector updates.
+// See apply.cuh for the apply design; DESIGN.md §5 for rooflines.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "apply.cuh"
+#include "kernels.h"
+
+namespace hz {
+
+// =============================================================================================
+// K2: apply (a2–a6 fused), EPI selects the fused BiCGSTAB epilogue
+// =============================================================================================
+template <typename R, int NY, int WARPS, bool COLLOC, int EPI>
+__global__ void __launch_bounds__(32 * WARPS) apply27_kernel(ApplyParams<R> p) {
+  typedef typename Cx<R>::T C;
+  constexpr int K = epi_k(EPI);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* tab = reinterpret_cast<R*>(smem_raw);
+  const int rhs = blockIdx.z;
+  if (p.active != nullptr && p.active[rhs] == 0) return;   // uniform per CTA (converged RHS)
+  for (int i = threadIdx.x; i < p.n_g * TAB_STRIDE; i += blockDim.x) tab[i] = p.tab[i];
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long g = ((long long)blockIdx.x * WARPS + warp) * 32 + lane;
+  const bool lane_ok = g < p.nlanes;
+  const long long gg = lane_ok ? g : 0;
+  const int strip = (int)(gg / p.nx);
+  const int x = (int)(gg - (long long)strip * p.nx);
+  const int y0 = strip * NY;
+  const bool hasL = lane_ok && x > 0;
+  const bool hasR = lane_ok && x < p.nx - 1;
+  const bool edge_ld = (lane == 0 && hasL) || (lane == 31 && hasR);
+  const int xe = (lane == 0) ? x - 1 : x + 1;
+
+  const int zc0 = blockIdx.y * p.zc;
+  const int zc1 = min(zc0 + p.zc, p.nzl);
+  const C* __restrict__ ub = p.u + (long long)rhs * p.fstride;
+  C* __restrict__ aub = p.au + (long long)rhs * p.fstride;
+  const C czv = czero(R(0));
+
+  C accP[NY], accC[NY];
+  R cp1[NY], cp2[NY], cp3[NY], mp1[NY], mp2[NY], mp3[NY];
+  R cc0[NY], cc1[NY], cc2[NY], cc3[NY], mc0[NY], mc1[NY], mc2[NY], mc3[NY];
+  R vown[NY];
+  double part[K > 0 ? K : 1];
+#pragma unroll
+  for (int k = 0; k < (K > 0 ? K : 1); k++) part[k] = 0.0;
+#pragma unroll
+  for (int i = 0; i < NY; i++) {
+    accP[i] = czv; accC[i] = czv;
+    cp1[i] = cp2[i] = cp3[i] = mp1[i] = mp2[i] = mp3[i] = R(0);
+    cc0[i] = cc1[i] = cc2[i] = cc3[i] = mc0[i] = mc1[i] = mc2[i] = mc3[i] = R(0);
+  }
+  {  // v at own rows of plane zc0 - 1
+    const int pl = zc0 - 1, zg = p.z0 + pl;
+    const bool pin = zg >= 0 && zg < p.nzg;
+#pragma unroll
+    for (int i = 0; i < NY; i++) {
+      const int y = y0 + i;
+      vown[i] = (lane_ok && pin && y < p.ny) ? __ldg(p.v + (long long)(pl + 1) * p.plane + (long long)y * p.nx + x) : R(1);
+    }
+  }
+
+  for (int pl = zc0 - 1; pl <= zc1; ++pl) {
+    const int zg = p.z0 + pl;
+    const bool pin = zg >= 0 && zg < p.nzg;
+    const bool do_prev = (pl - 1 >= zc0);
+    const bool do_cur = (pl >= zc0 && pl < zc1);
+    const bool do_next = (pl + 1 < zc1);
+    const long long pbase = (long long)(pl + 1) * p.plane;
+
+    // ---------------- loads of plane pl (rows y0-1 .. y0+NY) ----------------
+    C uc[NY + 2], ue[NY + 2];
+    R vc[NY + 2], ve[NY + 2];
+#pragma unroll
+    for (int r = 0; r < NY + 2; r++) {
+      const int y = y0 - 1 + r;
+      const bool rv = lane_ok && pin && y >= 0 && y < p.ny;
+      const long long o = pbase + (long long)y * p.nx;
+      uc[r] = rv ? ldg_c(ub + o + x) : czv;
+      ue[r] = (rv && edge_ld) ? ldg_c(ub + o + xe) : czv;
+      if (!COLLOC) {
+        if (r == 0 || r == NY + 1) vc[r] = rv ? __ldg(p.v + o + x) : R(1);
+        else vc[r] = vown[r - 1];
+        ve[r] = (rv && edge_ld) ? __ldg(p.v + o + xe) : R(1);
+      }
+    }
+    // v of plane pl+1 at own rows (coefficients of the next plane; r of the next iteration)
+    R vnx[NY];
+    {
+      const bool pin1 = (zg + 1 >= 0) && (zg + 1 < p.nzg) && (pl + 1 <= zc1);
+#pragma unroll
+      for (int i = 0; i < NY; i++) {
+        const int y = y0 + i;
+        vnx[i] = (lane_ok && pin1 && y < p.ny) ? __ldg(p.v + pbase + p.plane + (long long)y * p.nx + x) : R(1);
+      }
+    }
+
+    // ---------------- row quantities: u, Rc_u (x-faces), q = u/v², Rc_q ----------------
+    C Rcu[NY + 2], qc[NY + 2], Rcq[NY + 2];
+#pragma unroll
+    for (int r = 0; r < NY + 2; r++) {
+      C uL = shfl_up_c(uc[r], 1);
+      C uR = shfl_down_c(uc[r], 1);
+      if (lane == 0) uL = ue[r];
+      if (lane == 31) uR = ue[r];
+      if (!hasL) uL = czv;
+      if (!hasR) uR = czv;
+      Rcu[r] = cadd(uL, uR);
+      if (!COLLOC) {
+        const R rc = R(1) / (vc[r] * vc[r]);
+        const R re = R(1) / (ve[r] * ve[r]);
+        qc[r] = cscale(rc, uc[r]);
+        const C qe = cscale(re, ue[r]);
+        C qL = shfl_up_c(qc[r], 1);
+        C qR = shfl_down_c(qc[r], 1);
+        if (lane == 0) qL = qe;
+        if (lane == 31) qR = qe;
+        if (!hasL) qL = czv;
+        if (!hasR) qR = czv;
+        Rcq[r] = cadd(qL, qR);
+      }
+    }
+
+    // ---------------- per output row: plane sums and z scatter-accumulation ----------------
+#pragma unroll
+    for (int i = 0; i < NY; i++) {
+      const C P0 = uc[i + 1];
+      const C P1 = cadd(Rcu[i + 1], cadd(uc[i], uc[i + 2]));
+      const C P2 = cadd(Rcu[i], Rcu[i + 2]);
+      C Q0 = czv, Q1 = czv, Q2 = czv;
+      if (!COLLOC) {
+        Q0 = qc[i + 1];
+        Q1 = cadd(Rcq[i + 1], cadd(qc[i], qc[i + 2]));
+        Q2 = cadd(Rcq[i], Rcq[i + 2]);
+      }
+      if (do_prev) {   // plane pl is the "+1" neighbour plane of output pl-1
+        C a = accP[i];
+        a = cfma(cp1[i], P0, a);
+        a = cfma(cp2[i], P1, a);
+        a = cfma(cp3[i], P2, a);
+        if (!COLLOC) {
+          a = cfma(mp1[i], Q0, a);
+          a = cfma(mp2[i], Q1, a);
+          a = cfma(mp3[i], Q2, a);
+        }
+        // ---- finalize output (x, y0+i, pl-1) ----
+        const int y = y0 + i;
+        const int zo = pl - 1;
+        if (lane_ok && y < p.ny) {
+          const int zgo = p.z0 + zo;
+          if (x < p.lo[0] || x > p.hi[0] || y < p.lo[1] || y > p.hi[1] || zgo < p.lo[2] || zgo > p.hi[2])
+            a = cadd(a, pml_correction<R>(p, tab, ub, x, y, zo));
+          const long long o = (long long)(zo + 1) * p.plane + (long long)y * p.nx + x;
+          if (EPI == EPI_RESID) {
+            const C bb = ldg_c(p.bvec + (long long)rhs * p.fstride + o);
+            const C rr = csub(bb, a);
+            aub[o] = rr;
+            part[0] += (double)rr.x * (double)rr.x + (double)rr.y * (double)rr.y;
+            if (p.rhat != nullptr) acc_cdot(part[1], part[2], ldg_c(p.rhat + (long long)rhs * p.fstride + o), rr);
+          } else {
+            aub[o] = a;
+            if (EPI == EPI_DOT1) {
+              acc_cdot(part[0], part[1], ldg_c(p.rhat + (long long)rhs * p.fstride + o), a);
+            } else if (EPI == EPI_DOT4) {
+              const C s = ldg_c(ub + o);
+              const C rh = ldg_c(p.rhat + (long long)rhs * p.fstride + o);
+              acc_cdot(part[0], part[1], a, s);
+              part[2] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+              acc_cdot(part[3], part[4], rh, s);
+              acc_cdot(part[5], part[6], rh, a);
+            }
+          }
+        }
+      }
+      C an = czv;
+      if (do_cur) {    // centre plane of output pl
+        C a = accC[i];
+        a = cfma(cc0[i], P0, a);
+        a = cfma(cc1[i], P1, a);
+        a = cfma(cc2[i], P2, a);
+        if (!COLLOC) {
+          a = cfma(mc0[i], Q0, a);
+          a = cfma(mc1[i], Q1, a);
+          a = cfma(mc2[i], Q2, a);
+        }
+        accC[i] = a;
+      }
+      RowCoef<R> cn;
+      if (do_next) {   // plane pl is the "-1" neighbour plane of output pl+1
+        cn = row_coef<R>(vnx[i], tab, p);
+        if (COLLOC) {  // Eq. "10": ω²/κ0 for all 27 points → fold m/v0² into the class coefficients
+          const R iv2 = R(1) / (vnx[i] * vnx[i]);
+          cn.c0 = fma(cn.m0, iv2, cn.c0);
+          cn.c1 = fma(cn.m1, iv2, cn.c1);
+          cn.c2 = fma(cn.m2, iv2, cn.c2);
+          cn.c3 = fma(cn.m3, iv2, cn.c3);
+        }
+        an = cscale(cn.c1, P0);
+        an = cfma(cn.c2, P1, an);
+        an = cfma(cn.c3, P2, an);
+        if (!COLLOC) {
+          an = cfma(cn.m1, Q0, an);
+          an = cfma(cn.m2, Q1, an);
+          an = cfma(cn.m3, Q2, an);
+        }
+      } else {
+        cn.c0 = cn.c1 = cn.c2 = cn.c3 = cn.m0 = cn.m1 = cn.m2 = cn.m3 = R(0);
+      }
+      // rotate state: (pl-1, pl, pl+1) -> (pl, pl+1)
+      accP[i] = accC[i];
+      accC[i] = an;
+      cp1[i] = cc1[i]; cp2[i] = cc2[i]; cp3[i] = cc3[i];
+      mp1[i] = mc1[i]; mp2[i] = mc2[i]; mp3[i] = mc3[i];
+      cc0[i] = cn.c0; cc1[i] = cn.c1; cc2[i] = cn.c2; cc3[i] = cn.c3;
+      mc0[i] = cn.m0; mc1[i] = cn.m1; mc2[i] = cn.m2; mc3[i] = cn.m3;
+      vown[i] = vnx[i];
+    }
+  }
+
+  if (K > 0) {
+    const int nblocks = gridDim.x * gridDim.y;
+    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
+    block_grid_reduce<K, 32 * WARPS>(part, p.partials + (long long)rhs * nblocks * K, p.dots + (long long)rhs * K,
+                                     p.tickets + rhs, nblocks, bid);
+  }
+}
+
+// =============================================================================================
+// K1 record export: (k², t0, t1, t2, μ0, μ1, μ2, μ3) per point
+// =============================================================================================
+template <typename R>
+__global__ void record_kernel(ApplyParams<R> p, R w2_over_1, R* __restrict__ rec) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* tab = reinterpret_cast<R*>(smem_raw);
+  for (int i = threadIdx.x; i < p.n_g * TAB_STRIDE; i += blockDim.x) tab[i] = p.tab[i];
+  __syncthreads();
+  const long long n = (long long)p.nzl * p.plane;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long long)gridDim.x * blockDim.x) {
+    const R v = p.v[p.plane + idx];
+    R t1, t2, mu0, mu1, mu2;
+    interp_weights<R>(v, tab, p.n_g, p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
+    rec[0 * n + idx] = w2_over_1 / (v * v);              // k² = ω²/v²
+    rec[1 * n + idx] = R(1) - R(4) * (t1 + t2);          // t0
+    rec[2 * n + idx] = t1;
+    rec[3 * n + idx] = t2;
+    rec[4 * n + idx] = mu0;
+    rec[5 * n + idx] = mu1;
+    rec[6 * n + idx] = mu2;
+    rec[7 * n + idx] = (R(1) - mu0 - R(6) * mu1 - R(12) * mu2) * R(0.125);
+  }
+}
+
+// =============================================================================================
+// K6 point sources (consistent: row n's own mass weights; nodal: 1/h³)
+// =============================================================================================
+template <typename R>
+__global__ void sources_kernel(ApplyParams<R> p, int nsrc, const long long* __restrict__ nodes,
+                               const double* __restrict__ amps, int consistent, R ih3,
+                               typename Cx<R>::T* __restrict__ b) {
+  typedef typename Cx<R>::T C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* tab = reinterpret_cast<R*>(smem_raw);
+  for (int i = threadIdx.x; i < p.n_g * TAB_STRIDE; i += blockDim.x) tab[i] = p.tab[i];
+  __syncthreads();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nsrc * 27) return;
+  const int s = t / 27, d = t % 27;
+  const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+  if (!consistent && (dx | dy | dz) != 0) return;
+  const long long X = nodes[3 * s] + dx, Y = nodes[3 * s + 1] + dy, Z = nodes[3 * s + 2] + dz;
+  if (X < 0 || X >= p.nx || Y < 0 || Y >= p.ny || Z < p.z0 || Z >= (long long)p.z0 + p.nzl) return;
+  const int zl = (int)(Z - p.z0);
+  const long long o = (long long)s * p.fstride + (long long)(zl + 1) * p.plane + Y * p.nx + X;
+  R w = ih3;
+  if (consistent) {
+    R t1, t2, mu0, mu1, mu2;
+    interp_weights<R>(p.v[(long long)(zl + 1) * p.plane + Y * p.nx + X], tab, p.n_g, p.g_min, p.g_max, p.inv_dg,
+                      p.inv_fh, t1, t2, mu0, mu1, mu2);
+    const int cls = (dx != 0) + (dy != 0) + (dz != 0);
+    const R mu3 = (R(1) - mu0 - R(6) * mu1 - R(12) * mu2) * R(0.125);
+    const R mu = cls == 0 ? mu0 : (cls == 1 ? mu1 : (cls == 2 ? mu2 : mu3));
+    w = mu * ih3;
+  }
+  const double ar = amps ? amps[2 * s] : 1.0, ai = amps ? amps[2 * s + 1] : 0.0;
+  C val;
+  val.x = (R)(ar * (double)w);
+  val.y = (R)(ai * (double)w);
+  b[o] = val;
+}
+
+// =============================================================================================
+// velocity validation / statistics: min, max, non-finite count, clamped count
+// =============================================================================================
+template <typename R>
+__global__ void vstats_kernel(const R* __restrict__ v, long long n, R inv_fh, R g_min, R g_max,
+                              unsigned long long* __restrict__ out /* [4]: minbits,maxbits,bad,clamped */) {
+  R lmin = R(3.0e38), lmax = R(0);
+  unsigned long long bad = 0, clamped = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const R x = v[i];
+    if (!(x > R(0)) || !isfinite((double)x)) { bad++; continue; }
+    lmin = x < lmin ? x : lmin;
+    lmax = x > lmax ? x : lmax;
+    const R G = x * inv_fh;
+    if (G < g_min || G > g_max) clamped++;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lmin = fmin(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+    lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    clamped += __shfl_xor_sync(0xffffffffu, clamped, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    const double dmin = (double)lmin, dmax = (double)lmax;   // positive doubles order like their bits
+    atomicMin(&out[0], (unsigned long long)__double_as_longlong(dmin));
+    atomicMax(&out[1], (unsigned long long)__double_as_longlong(dmax));
+    atomicAdd(&out[2], bad);
+    atomicAdd(&out[3], clamped);
+  }
+}
+
+// =============================================================================================
+// K3: BiCGSTAB vector kernels (per RHS in blockIdx.y).  Scalars come from the fp64 dot buffers
+// written by the previous kernels; every CTA recomputes them identically, CTA 0 records them.
+// =============================================================================================
+__device__ __forceinline__ double2 zdiv(double2 a, double2 b) {
+  const double d = b.x * b.x + b.y * b.y;
+  return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+__device__ __forceinline__ double2 zmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ bool tiny(double2 a, double scale) {
+  const double m = fabs(a.x) + fabs(a.y);
+  return !(m > 1e-300 * scale) || !isfinite(m);
+}
+
+template <typename R>
+__device__ __forceinline__ typename Cx<R>::T to_c(double2 a) {
+  typename Cx<R>::T r;
+  r.x = (R)a.x;
+  r.y = (R)a.y;
+  return r;
+}
+
+// p = r̂0 = r, rho = (r̂0, r) = ‖r‖²  (after the initial residual)
+template <typename R>
+__global__ void bicg_init_kernel(VecParams<R> q) {
+  typedef typename Cx<R>::T C;
+  const int rhs = blockIdx.y;
+  if (q.active[rhs] == 0) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    SolverState& st = q.state[rhs];
+    const double rr = q.dotR[3 * rhs + 0];
+    st.rho_next[0] = rr;
+    st.rho_next[1] = 0.0;
+    st.flags = 0;
+  }
+  const long long off = (long long)rhs * q.fstride + q.plane;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < q.n; i += (long long)gridDim.x * blockDim.x) {
+    const C r = q.r[off + i];
+    q.rhat[off + i] = r;
+    q.p[off + i] = r;
+  }
+}
+
+// after a residual replacement: rho = (r̂0, r)
+__global__ void bicg_rho_reset_kernel(const double* __restrict__ dotR, SolverState* state, const int* active, int nrhs) {
+  const int rhs = threadIdx.x + blockIdx.x * blockDim.x;
+  if (rhs >= nrhs || active[rhs] == 0) return;
+  state[rhs].rho_next[0] = dotR[3 * rhs + 1];
+  state[rhs].rho_next[1] = dotR[3 * rhs + 2];
+}
+
+// s = r − α v, α = ρ/(r̂0, v)   (s overwrites r)
+template <typename R>
+__global__ void bicg_s_kernel(VecParams<R> q) {
+  typedef typename Cx<R>::T C;
+  const int rhs = blockIdx.y;
+  if (q.active[rhs] == 0) return;
+  SolverState& st = q.state[rhs];
+  const double2 rho = make_double2(st.rho_next[0], st.rho_next[1]);
+  const double2 den = make_double2(q.dotA[2 * rhs], q.dotA[2 * rhs + 1]);
+  double2 alpha = make_double2(0.0, 0.0);
+  const bool brk = tiny(den, 1.0) || tiny(rho, 1.0);
+  if (!brk) alpha = zdiv(rho, den);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st.alpha[0] = alpha.x;
+    st.alpha[1] = alpha.y;
+    st.rho_used[0] = rho.x;
+    st.rho_used[1] = rho.y;
+    if (brk) st.flags |= 1;
+  }
+  const C a = to_c<R>(alpha);
+  const long long off = (long long)rhs * q.fstride + q.plane;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < q.n; i += (long long)gridDim.x * blockDim.x) {
+    const C r = q.r[off + i], v = q.v[off + i];
+    C s;
+    s.x = r.x - (a.x * v.x - a.y * v.y);
+    s.y = r.y - (a.x * v.y + a.y * v.x);
+    q.r[off + i] = s;
+  }
+}
+
+// ω = (t,s)/(t,t); ρ' = (r̂0,s) − ω (r̂0,t); β = (ρ'/ρ)(α/ω);
+// x += α p + ω s; r = s − ω t; p = r + β (p − ω v); partial ‖r‖²
+template <typename R, int NT>
+__global__ void __launch_bounds__(NT) bicg_update_kernel(VecParams<R> q) {
+  typedef typename Cx<R>::T C;
+  const int rhs = blockIdx.y;
+  if (q.active[rhs] == 0) return;
+  SolverState& st = q.state[rhs];
+  const double* dB = q.dotB + 7 * rhs;
+  const double2 ts = make_double2(dB[0], dB[1]);
+  const double tt = dB[2];
+  const double2 rs = make_double2(dB[3], dB[4]);
+  const double2 rt = make_double2(dB[5], dB[6]);
+  double2 alpha = make_double2(st.alpha[0], st.alpha[1]);
+  const double2 rho = make_double2(st.rho_used[0], st.rho_used[1]);
+  double2 omega = make_double2(0.0, 0.0), beta = make_double2(0.0, 0.0), rho_new = make_double2(0.0, 0.0);
+  bool brk = (st.flags & 1) != 0 || !(tt > 0.0) || !isfinite(tt);
+  if (!brk) {
+    omega = make_double2(ts.x / tt, ts.y / tt);
+    const double2 wrt = zmul(omega, rt);
+    rho_new = make_double2(rs.x - wrt.x, rs.y - wrt.y);
+    if (tiny(omega, 1.0) || tiny(rho, 1.0)) brk = true;
+    else beta = zmul(zdiv(rho_new, rho), zdiv(alpha, omega));
+  }
+  if (brk) { alpha.x = alpha.y = 0.0; omega.x = omega.y = 0.0; beta.x = beta.y = 0.0; }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st.omega[0] = omega.x;
+    st.omega[1] = omega.y;
+    st.rho_next[0] = rho_new.x;
+    st.rho_next[1] = rho_new.y;
+    if (brk) st.flags |= 1;
+  }
+  const C a = to_c<R>(alpha), w = to_c<R>(omega), bt = to_c<R>(beta);
+  const long long off = (long long)rhs * q.fstride + q.plane;
+  double part[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < q.n; i += (long long)gridDim.x * blockDim.x) {
+    const C s = q.r[off + i], t = q.t[off + i], pp = q.p[off + i], vv = q.v[off + i];
+    C xx = q.x[off + i];
+    // x += α p + ω s
+    xx.x += (a.x * pp.x - a.y * pp.y) + (w.x * s.x - w.y * s.y);
+    xx.y += (a.x * pp.y + a.y * pp.x) + (w.x * s.y + w.y * s.x);
+    // r = s − ω t
+    C r;
+    r.x = s.x - (w.x * t.x - w.y * t.y);
+    r.y = s.y - (w.x * t.y + w.y * t.x);
+    // p = r + β (p − ω v)
+    C d;
+    d.x = pp.x - (w.x * vv.x - w.y * vv.y);
+    d.y = pp.y - (w.x * vv.y + w.y * vv.x);
+    C pn;
+    pn.x = r.x + (bt.x * d.x - bt.y * d.y);
+    pn.y = r.y + (bt.x * d.y + bt.y * d.x);
+    q.x[off + i] = xx;
+    q.r[off + i] = r;
+    q.p[off + i] = pn;
+    part[0] += (double)r.x * (double)r.x + (double)r.y * (double)r.y;
+  }
+  const int nblocks = gridDim.x;
+  block_grid_reduce<1, NT>(part, q.partials + (long long)rhs * nblocks, q.dotR + 3 * rhs, q.tickets + rhs, nblocks,
+                           blockIdx.x);
+}
+
+// ‖f‖² per RHS (used for ‖b‖)
+template <typename R, int NT>
+__global__ void __launch_bounds__(NT) norm2_kernel(const typename Cx<R>::T* __restrict__ f, long long fstride,
+                                                   long long plane, long long n, double* partials, double* out,
+                                                   unsigned int* tickets) {
+  const int rhs = blockIdx.y;
+  const long long off = (long long)rhs * fstride + plane;
+  double part[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const typename Cx<R>::T a = f[off + i];
+    part[0] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+  }
+  block_grid_reduce<1, NT>(part, partials + (long long)rhs * gridDim.x, out + rhs, tickets + rhs, gridDim.x, blockIdx.x);
+}
+
+// =============================================================================================
+// host-side launchers (kernels.h)
+// =============================================================================================
+template <typename R, int NY, int WARPS, bool COLLOC, int EPI>
+static cudaError_t launch_apply_t(const ApplyParams<R>& p, int nrhs, cudaStream_t s) {
+  auto kern = apply27_kernel<R, NY, WARPS, COLLOC, EPI>;
+  const size_t smem = (size_t)p.n_g * TAB_STRIDE * sizeof(R);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr_set = true;
+  }
+  const long long nb = (p.nlanes + 32 * WARPS - 1) / (32 * WARPS);
+  dim3 grid((unsigned)nb, (unsigned)p.nchunks, (unsigned)nrhs);
+  kern<<<grid, 32 * WARPS, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename R> struct ApplyCfg;
+template <> struct ApplyCfg<float> { enum { NY = 4, WARPS = 4 }; };
+template <> struct ApplyCfg<double> { enum { NY = 2, WARPS = 4 }; };
+
+template <typename R>
+int apply_ny() { return ApplyCfg<R>::NY; }
+template int apply_ny<float>();
+template int apply_ny<double>();
+template <typename R>
+int apply_warps() { return ApplyCfg<R>::WARPS; }
+template int apply_warps<float>();
+template int apply_warps<double>();
+
+template <typename R>
+cudaError_t launch_apply(const ApplyParams<R>& p, int nrhs, bool colloc, int epi, cudaStream_t s) {
+  constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
+  if (!colloc) {
+    switch (epi) {
+      case EPI_PLAIN: return launch_apply_t<R, NY, W, false, EPI_PLAIN>(p, nrhs, s);
+      case EPI_DOT1: return launch_apply_t<R, NY, W, false, EPI_DOT1>(p, nrhs, s);
+      case EPI_DOT4: return launch_apply_t<R, NY, W, false, EPI_DOT4>(p, nrhs, s);
+      case EPI_RESID: return launch_apply_t<R, NY, W, false, EPI_RESID>(p, nrhs, s);
+    }
+  } else {
+    switch (epi) {
+      case EPI_PLAIN: return launch_apply_t<R, NY, W, true, EPI_PLAIN>(p, nrhs, s);
+      case EPI_DOT1: return launch_apply_t<R, NY, W, true, EPI_DOT1>(p, nrhs, s);
+      case EPI_DOT4: return launch_apply_t<R, NY, W, true, EPI_DOT4>(p, nrhs, s);
+      case EPI_RESID: return launch_apply_t<R, NY, W, true, EPI_RESID>(p, nrhs, s);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+template cudaError_t launch_apply<float>(const ApplyParams<float>&, int, bool, int, cudaStream_t);
+template cudaError_t launch_apply<double>(const ApplyParams<double>&, int, bool, int, cudaStream_t);
+
+template <typename R>
+int apply_occupancy(bool colloc) {
+  constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
+  int nb = 0;
+  if (colloc)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_kernel<R, NY, W, true, EPI_DOT4>, 32 * W, 16 * 1024);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_kernel<R, NY, W, false, EPI_DOT4>, 32 * W, 16 * 1024);
+  return nb > 0 ? nb : 1;
+}
+template int apply_occupancy<float>(bool);
+template int apply_occupancy<double>(bool);
+
+template <typename R>
+cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s) {
+  const size_t smem = (size_t)p.n_g * TAB_STRIDE * sizeof(R);
+  cudaFuncSetAttribute(record_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  record_kernel<R><<<1024, 256, smem, s>>>(p, p.w2, rec);
+  return cudaGetLastError();
+}
+template cudaError_t launch_record<float>(const ApplyParams<float>&, float*, cudaStream_t);
+template cudaError_t launch_record<double>(const ApplyParams<double>&, double*, cudaStream_t);
+
+template <typename R>
+cudaError_t launch_sources(const ApplyParams<R>& p, int nsrc, const long long* nodes, const double* amps,
+                           int consistent, R ih3, typename Cx<R>::T* b, cudaStream_t s) {
+  const size_t smem = (size_t)p.n_g * TAB_STRIDE * sizeof(R);
+  cudaFuncSetAttribute(sources_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  const int nt = nsrc * 27;
+  sources_kernel<R><<<(nt + 255) / 256, 256, smem, s>>>(p, nsrc, nodes, amps, consistent, ih3, b);
+  return cudaGetLastError();
+}
+template cudaError_t launch_sources<float>(const ApplyParams<float>&, int, const long long*, const double*, int, float,
+                                           float2*, cudaStream_t);
+template cudaError_t launch_sources<double>(const ApplyParams<double>&, int, const long long*, const double*, int,
+                                            double, double2*, cudaStream_t);
+
+template <typename R>
+cudaError_t launch_vstats(const R* v, long long n, R inv_fh, R g_min, R g_max, unsigned long long* out, cudaStream_t s) {
+  vstats_kernel<R><<<592, 256, 0, s>>>(v, n, inv_fh, g_min, g_max, out);
+  return cudaGetLastError();
+}
+template cudaError_t launch_vstats<float>(const float*, long long, float, float, float, unsigned long long*, cudaStream_t);
+template cudaError_t launch_vstats<double>(const double*, long long, double, double, double, unsigned long long*,
+                                           cudaStream_t);
+
+constexpr int VEC_NT = 256;
+
+template <typename R>
+cudaError_t launch_bicg(int which, const VecParams<R>& q, int nrhs, cudaStream_t s) {
+  dim3 grid((unsigned)q.nblocks, (unsigned)nrhs);
+  switch (which) {
+    case BICG_INIT: bicg_init_kernel<R><<<grid, VEC_NT, 0, s>>>(q); break;
+    case BICG_S: bicg_s_kernel<R><<<grid, VEC_NT, 0, s>>>(q); break;
+    case BICG_UPDATE: bicg_update_kernel<R, VEC_NT><<<grid, VEC_NT, 0, s>>>(q); break;
+    case BICG_RHO_RESET: bicg_rho_reset_kernel<<<(nrhs + 127) / 128, 128, 0, s>>>(q.dotR, q.state, q.active, nrhs); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+template cudaError_t launch_bicg<float>(int, const VecParams<float>&, int, cudaStream_t);
+template cudaError_t launch_bicg<double>(int, const VecParams<double>&, int, cudaStream_t);
+
+template <typename R>
+cudaError_t launch_norm2(const typename Cx<R>::T* f, long long fstride, long long plane, long long n, int nrhs,
+                         int nblocks, double* partials, double* out, unsigned int* tickets, cudaStream_t s) {
+  dim3 grid((unsigned)nblocks, (unsigned)nrhs);
+  norm2_kernel<R, VEC_NT><<<grid, VEC_NT, 0, s>>>(f, fstride, plane, n, partials, out, tickets);
+  return cudaGetLastError();
+}
+template cudaError_t launch_norm2<float>(const float2*, long long, long long, long long, int, int, double*, double*,
+                                         unsigned int*, cudaStream_t);
+template cudaError_t launch_norm2<double>(const double2*, long long, long long, long long, int, int, double*, double*,
+                                          unsigned int*, cudaStream_t);
+
+}  // namespace hz

@@ -1,0 +1,53 @@
+// Launch interface between the ABI layer (api.cu) and the kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "apply.cuh"
+
+namespace hz {
+
+// Per-RHS BiCGSTAB scalars on the device (see bicg_* kernels for who writes what).
+struct SolverState {
+  double rho_next[2];  // ρ for the next α (written by update / init / rho_reset)
+  double rho_used[2];  // ρ used by the last α (written by s-kernel, read by update)
+  double alpha[2];
+  double omega[2];
+  int flags;           // bit 0: breakdown detected
+  int pad;
+};
+
+template <typename R>
+struct VecParams {
+  typedef typename Cx<R>::T C;
+  long long n;        // owned points per RHS (nzl*plane)
+  long long plane;    // halo-plane offset
+  long long fstride;  // per-RHS stride
+  int nblocks;        // CTAs per RHS
+  C *x, *r, *rhat, *p, *v, *t;
+  const double* dotA;  // [nrhs][2]
+  const double* dotB;  // [nrhs][7]
+  double* dotR;        // [nrhs][3]
+  double* partials;
+  unsigned int* tickets;
+  SolverState* state;
+  const int* active;
+};
+
+enum { BICG_INIT = 0, BICG_S = 1, BICG_UPDATE = 2, BICG_RHO_RESET = 3 };
+
+template <typename R> int apply_ny();
+template <typename R> int apply_warps();
+template <typename R> int apply_occupancy(bool colloc);
+template <typename R> cudaError_t launch_apply(const ApplyParams<R>& p, int nrhs, bool colloc, int epi, cudaStream_t s);
+template <typename R> cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s);
+template <typename R>
+cudaError_t launch_sources(const ApplyParams<R>& p, int nsrc, const long long* nodes, const double* amps,
+                           int consistent, R ih3, typename Cx<R>::T* b, cudaStream_t s);
+template <typename R>
+cudaError_t launch_vstats(const R* v, long long n, R inv_fh, R g_min, R g_max, unsigned long long* out, cudaStream_t s);
+template <typename R> cudaError_t launch_bicg(int which, const VecParams<R>& q, int nrhs, cudaStream_t s);
+template <typename R>
+cudaError_t launch_norm2(const typename Cx<R>::T* f, long long fstride, long long plane, long long n, int nrhs,
+                         int nblocks, double* partials, double* out, unsigned int* tickets, cudaStream_t s);
+
+}  // namespace hz

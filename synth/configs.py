@@ -200,31 +200,40 @@ def velocity_slab(cfg: Config, z0: int = 0, nz_local: Optional[int] = None,
                 v[lo - z0:hi - z0, y0:y1, x0:x1] = vb
         return v
     if cfg.index == 4:
-        folds, zbar, vel, faults = _cfg4_draws(cfg)
-        x = (np.arange(nx) - npml) * h
-        y = (np.arange(ny) - npml) * h
-        z = (k - npml) * h
-        Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
-        X, Y, Z = X.copy(), Y.copy(), Z.copy()
-        for (xf, yf, zf, strike, dip, throw) in faults:
-            dh = np.array([-np.sin(strike), np.cos(strike)])
-            dist_h = (X - xf) * dh[0] + (Y - yf) * dh[1]
-            hanging = Z < zf + np.tan(dip) * dist_h
-            # hanging-wall nodes take the layer index of the point displaced by -throw along dip
-            X = np.where(hanging, X - throw * np.cos(dip) * dh[0], X)
-            Y = np.where(hanging, Y - throw * np.cos(dip) * dh[1], Y)
-            Z = np.where(hanging, Z - throw * np.sin(dip), Z)
-        fold = np.zeros_like(X)
-        for (A, Lam, beta, ph) in folds:
-            fold += A * np.sin(2 * np.pi * (X * np.cos(beta) + Y * np.sin(beta)) / Lam + ph)
-        layer = np.zeros(X.shape, dtype=np.int64)
-        for l, zb in enumerate(zbar):
-            taper = 1.0 - 0.5 * (l + 1) / 8.0
-            layer += (Z > zb + taper * fold).astype(np.int64)
-        return vel[layer]
+        draws = _cfg4_draws(cfg)
+        out = np.empty((nz_local, ny, nx))
+        for a in range(0, nz_local, 8):       # z-chunks bound the temporary memory
+            b = min(nz_local, a + 8)
+            out[a:b] = _cfg4_eval(cfg, draws, k[a:b])
+        return out
     if cfg.index == 5:
         return _cfg5_slab(cfg, z0, nz_local, device)
     raise ValueError(cfg.index)
+
+
+def _cfg4_eval(cfg: Config, draws, k) -> np.ndarray:
+    folds, zbar, vel, faults = draws
+    nx, ny, h, npml = cfg.nx, cfg.ny, cfg.h, cfg.npml
+    x = (np.arange(nx) - npml) * h
+    y = (np.arange(ny) - npml) * h
+    z = (np.asarray(k, dtype=np.float64) - npml) * h
+    Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
+    for (xf, yf, zf, strike, dip, throw) in faults:
+        dh = np.array([-np.sin(strike), np.cos(strike)])
+        dist_h = (X - xf) * dh[0] + (Y - yf) * dh[1]
+        hanging = Z < zf + np.tan(dip) * dist_h
+        # hanging-wall nodes take the layer index of the point displaced by -throw along dip
+        X = np.where(hanging, X - throw * np.cos(dip) * dh[0], X)
+        Y = np.where(hanging, Y - throw * np.cos(dip) * dh[1], Y)
+        Z = np.where(hanging, Z - throw * np.sin(dip), Z)
+    fold = np.zeros_like(X)
+    for (A, Lam, beta, ph) in folds:
+        fold += A * np.sin(2 * np.pi * (X * np.cos(beta) + Y * np.sin(beta)) / Lam + ph)
+    layer = np.zeros(X.shape, dtype=np.int64)
+    for l, zb in enumerate(zbar):
+        taper = 1.0 - 0.5 * (l + 1) / 8.0
+        layer += (Z > zb + taper * fold).astype(np.int64)
+    return vel[layer]
 
 
 def _cfg5_slab(cfg: Config, z0: int, nz_local: int, device=None) -> np.ndarray:

@@ -1,0 +1,224 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs:
+coefficient record, PML arrays, operator apply (several tiles + ragged tails, both precisions, both
+mass formulations, batched RHS), decomposition invariance, point sources, and sampled rows at the
+full BASELINE sizes in the launch configuration bench.py times."""
+import zlib
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import operator as op
+from oracle import weights
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {"c64": 1e-5, "c128": 1e-12}     # north star: apply / coefficients rel. L2
+
+
+@pytest.fixture(scope="module")
+def hz():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2108_08730_b200 import hz as _hz
+    return _hz
+
+
+@pytest.fixture(scope="module")
+def ctx(hz):
+    return hz.hz_ctx_create(0)
+
+
+@pytest.fixture(scope="module")
+def table(hz, ga_table):
+    """Shared table: the ORACLE's rows imported into libhz (the table builders are compared
+    separately in test_abi.py; cond ~1e10 makes independent builders agree only to ~1e-10)."""
+    return hz.hz_table_import(ga_table.g_min, ga_table.dg, ga_table.u5)
+
+
+def rdt(dtype):
+    return np.float32 if dtype == "c64" else np.float64
+
+
+def cdt(dtype):
+    return np.complex64 if dtype == "c64" else np.complex128
+
+
+def assemble(hz, ctx, table, v, h, f, npml, dtype, mass="eq8", **kw):
+    vt = torch.from_numpy(np.ascontiguousarray(v.astype(rdt(dtype)))).cuda()
+    nz, ny, nx = v.shape
+    return hz.hz_assemble_coeffs(ctx, nx, ny, nz, h, vt, f, table, npml=npml,
+                                 dtype=hz.HZ_C64 if dtype == "c64" else hz.HZ_C128,
+                                 mass=hz.HZ_MASS_EQ8 if mass == "eq8" else hz.HZ_MASS_COLLOC, **kw)
+
+
+def gpu_apply(hz, C, u):
+    ud = C.alloc_field(u.shape[0])
+    ud[:, 1:-1] = torch.from_numpy(u).cuda()
+    aud = C.alloc_field(u.shape[0])
+    hz.hz_apply_impedance(C, ud, aud)
+    torch.cuda.synchronize()
+    return aud[:, 1:-1].cpu().numpy()
+
+
+def oracle_problem(v, h, f, npml, ga_table, dtype, mass="eq8"):
+    # the oracle receives exactly the values the GPU received (float32-rounded for c64)
+    return op.Problem(v.astype(rdt(dtype)).astype(np.float64), h, f, npml, ga_table, mass=mass)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+# ------------------------------------------------------------------------------------------------
+CASES = [
+    # (name, nx, ny, nz, h, f, npml, vmin, vmax, nrhs)
+    ("tiny", 5, 4, 3, 20.0, 9.0, 1, 1500.0, 4000.0, 1),
+    ("ragged", 37, 29, 23, 25.0, 7.0, 4, 1200.0, 6000.0, 2),     # G 6.9..34 + clamps below 4
+    ("wide", 70, 9, 6, 30.0, 3.0, 2, 1400.0, 5000.0, 3),
+    ("clamped", 33, 34, 11, 10.0, 30.0, 3, 500.0, 20000.0, 1),    # G 1.7..67: clamping both ends
+]
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_apply_random_models(hz, ctx, table, ga_table, dtype, case):
+    name, nx, ny, nz, h, f, npml, vmin, vmax, nrhs = case
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    v = rng.uniform(vmin, vmax, (nz, ny, nx))
+    u = synth.random_field((nrhs, nz, ny, nx), seed=3).astype(cdt(dtype))
+    C = assemble(hz, ctx, table, v, h, f, npml, dtype)
+    got = gpu_apply(hz, C, u)
+    P = oracle_problem(v, h, f, npml, ga_table, dtype)
+    ref = op.apply(op.assemble(P), u)
+    assert rel(got, ref) <= TOL[dtype], rel(got, ref)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_apply_colloc_mass(hz, ctx, table, ga_table, dtype):
+    """Eq. "10" collocation-κ mass, NEXT-1 variant on the same kernel."""
+    rng = np.random.default_rng(11)
+    v = rng.uniform(1500.0, 4500.0, (13, 17, 35))
+    u = synth.random_field((1, 13, 17, 35), seed=4).astype(cdt(dtype))
+    C = assemble(hz, ctx, table, v, 25.0, 7.0, 3, dtype, mass="colloc")
+    got = gpu_apply(hz, C, u)
+    ref = op.apply(op.assemble(oracle_problem(v, 25.0, 7.0, 3, ga_table, dtype, mass="colloc")), u)
+    assert rel(got, ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("cfg_i", [1, 2])
+def test_apply_baseline_configs(hz, ctx, table, ga_table, dtype, cfg_i):
+    cfg = synth.get_config(cfg_i)
+    v = synth.velocity_model(cfg)
+    u = synth.random_field((1,) + cfg.shape, seed=cfg_i).astype(cdt(dtype))
+    C = assemble(hz, ctx, table, v, cfg.h, cfg.freq, cfg.npml, dtype)
+    got = gpu_apply(hz, C, u)
+    ref = op.apply(op.assemble(oracle_problem(v, cfg.h, cfg.freq, cfg.npml, ga_table, dtype)), u)
+    assert rel(got, ref) <= TOL[dtype]
+
+
+def sample_nodes(cfg, n, seed):
+    rng = np.random.default_rng(seed)
+    pts = np.stack([rng.integers(0, cfg.nx, n), rng.integers(0, cfg.ny, n), rng.integers(0, cfg.nz, n)], 1)
+    corners = np.array([[x, y, z] for x in (0, 1, cfg.nx - 2, cfg.nx - 1) for y in (0, cfg.ny - 1)
+                        for z in (0, cfg.npml, cfg.nz - 1)])
+    return np.concatenate([pts, corners])
+
+
+@pytest.mark.parametrize("cfg_i", [3, 4])
+def test_apply_full_size_sampled(hz, ctx, table, ga_table, cfg_i):
+    """Full BASELINE sizes (configs 3 and 4, c64) in the bench launch configuration: the oracle
+    evaluates sampled rows one by one."""
+    cfg = synth.get_config(cfg_i)
+    v = synth.velocity_model(cfg).astype(np.float32)
+    u = synth.random_field((1,) + cfg.shape, seed=10 + cfg_i)
+    C = assemble(hz, ctx, table, v, cfg.h, cfg.freqs[-1], cfg.npml, "c64")
+    got = gpu_apply(hz, C, u)[0]
+    nodes = sample_nodes(cfg, 4000, cfg_i)
+    P = op.Problem(v.astype(np.float64), cfg.h, cfg.freqs[-1], cfg.npml, ga_table)
+    ref = op.apply_rows(P, u[0], nodes)
+    g = got[nodes[:, 2], nodes[:, 1], nodes[:, 0]]
+    assert rel(g, ref) <= TOL["c64"]
+    assert np.all(np.isfinite(got))
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_record_and_pml_export(hz, ctx, table, ga_table, dtype):
+    rng = np.random.default_rng(21)
+    nz, ny, nx, h, f, npml = 9, 14, 40, 20.0, 10.0, 3
+    v = rng.uniform(700.0, 9000.0, (nz, ny, nx))        # G 3.5 .. 45: clamps on both ends
+    C = assemble(hz, ctx, table, v, h, f, npml, dtype)
+    rec = np.zeros((8, nz, ny, nx), dtype=rdt(dtype))
+    nmax = max(nx, ny, nz)
+    pml = np.zeros((3, 2, nmax), dtype=np.complex128)
+    hz.hz_coeffs_export(C, rec, pml)
+    P = oracle_problem(v, h, f, npml, ga_table, dtype)
+    c = P.coefficients()
+    ref = np.stack([c.k2, c.t0, c.t1, c.t2, c.mu[..., 0], c.mu[..., 1], c.mu[..., 2], c.mu[..., 3]])
+    for k in range(8):
+        assert rel(rec[k].astype(np.float64), ref[k]) <= TOL[dtype], k
+    assert C.n_clamped == int(c.clamped.sum()) and C.status == hz.HZ_WARN_CLAMPED
+    for a, n in enumerate((nx, ny, nz)):
+        am, ap = P.pml()[a]
+        assert rel(pml[a, 0, :n], am) <= 1e-13 and rel(pml[a, 1, :n], ap) <= 1e-13
+
+
+def test_decomposition_invariance(hz, ctx, table):
+    """Apply on emulated z-slabs (halo planes supplied by the caller) is BITWISE equal to the
+    single-domain apply (per-point arithmetic is identical; halos are copies) — SURVEY §4.4."""
+    rng = np.random.default_rng(31)
+    nz, ny, nx, h, f, npml = 23, 21, 45, 25.0, 7.0, 4
+    v = rng.uniform(1500.0, 4500.0, (nz, ny, nx)).astype(np.float32)
+    u = synth.random_field((2, nz, ny, nx), seed=6)
+    full = gpu_apply(hz, assemble(hz, ctx, table, v, h, f, npml, "c64"), u)
+    vmax = float(v.max())
+    for cuts in ([0, 11, 23], [0, 1, 9, 16, 23]):
+        out = np.zeros_like(full)
+        for z0, z1 in zip(cuts[:-1], cuts[1:]):
+            nzl = z1 - z0
+            vs = np.ones((nzl + 2, ny, nx), np.float32)
+            lo, hi = max(z0 - 1, 0), min(z1 + 1, nz)
+            vs[lo - (z0 - 1):hi - (z0 - 1)] = v[lo:hi]
+            vt = torch.from_numpy(vs).cuda()
+            C = hz.hz_assemble_coeffs(ctx, nx, ny, nz, h, vt, f, table, npml=npml, z0=z0, nz_local=nzl,
+                                      v_pml=vmax, v_halo=True)
+            ud = C.alloc_field(2)
+            for k in range(nzl + 2):
+                zg = z0 - 1 + k
+                if 0 <= zg < nz:
+                    ud[:, k] = torch.from_numpy(u[:, zg]).cuda()
+            aud = C.alloc_field(2)
+            hz.hz_apply_impedance(C, ud, aud)
+            torch.cuda.synchronize()
+            out[:, z0:z1] = aud[:, 1:-1].cpu().numpy()
+        assert np.array_equal(out, full)
+
+
+@pytest.mark.parametrize("consistent", [True, False])
+def test_point_sources(hz, ctx, table, ga_table, consistent):
+    cfg = synth.get_config(2)
+    v = synth.velocity_model(cfg)
+    C = assemble(hz, ctx, table, v, cfg.h, cfg.freq, cfg.npml, "c128")
+    nodes = synth.source_nodes(cfg)
+    b = C.alloc_field(len(nodes))
+    amps = np.array([1.0, 2.0 - 1.0j, 0.5j, -1.0])
+    hz.hz_point_sources(C, nodes, b, amps=amps, consistent=consistent)
+    ref = op.point_sources(oracle_problem(v, cfg.h, cfg.freq, cfg.npml, ga_table, "c128"), nodes, amps,
+                           consistent=consistent)
+    got = b[:, 1:-1].cpu().numpy()
+    assert rel(got, ref) <= 1e-12
+    with pytest.raises(hz.HzError) as e:
+        hz.hz_point_sources(C, [[3, 50, 50]], C.alloc_field(1))
+    assert e.value.status == -7
+
+
+def test_domain_errors(hz, ctx, table):
+    v = np.full((5, 5, 5), 2000.0, np.float32)
+    v[2, 2, 2] = -1.0
+    with pytest.raises(hz.HzError) as e:
+        assemble(hz, ctx, table, v, 10.0, 5.0, 1, "c64")
+    assert e.value.status == -2
+    with pytest.raises(hz.HzError):
+        assemble(hz, ctx, table, np.full((5, 2, 5), 2000.0), 10.0, 5.0, 1, "c64")
