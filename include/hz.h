@@ -170,12 +170,18 @@ typedef struct {
 } hz_solve_opts;
 
 typedef struct {
-  double apply_ms_total;   /* sum of operator-apply kernel durations (timing = 1)        */
-  long long apply_launches;/* number of operator-apply kernel launches                    */
-  long long kernel_launches;/* all libhz kernel launches during the call                  */
-  double bytes_per_apply;  /* algorithmic bytes of one apply launch (all active RHS)       */
-  int replacements;        /* residual replacements performed                             */
-  int restarts;            /* breakdown restarts                                          */
+  double apply_ms_total;    /* sum of operator-apply kernel durations (timing = 1)               */
+  long long apply_launches; /* number of operator-apply kernel launches                          */
+  long long kernel_launches;/* all libhz kernel launches during the call                         */
+  double apply_bytes_total; /* algorithmic HBM bytes of all apply launches: per launch
+                               n_points * (sizeof(real) + n_active_rhs * k * sizeof(complex)),
+                               k = fields read/written per RHS by the launch's epilogue          */
+  double apply_points_total;/* grid points x active RHS processed by all apply launches          */
+  int replacements;         /* residual replacements performed                                   */
+  int restarts;             /* breakdown restarts                                                */
+  int iterations;           /* BiCGSTAB iterations of the batch (max over RHS)                   */
+  int stagnated;            /* 1 if some RHS was retired because its true residual stagnated
+                               (no 10% reduction in max(20*replace_every, 1000) iterations)      */
 } hz_solve_stats;
 
 hz_status hz_solve(const hz_coeffs* c, const void* b, void* x, int nrhs, const hz_solve_opts* opts,

@@ -28,18 +28,18 @@ static inline void count_launch(long long n = 1) { g_launches += n; }
 
 using namespace hz;
 
-#define HZ_CUDA(call)                                                                      \
+#define HZ_CUDA(...)                                                                       \
   do {                                                                                     \
-    cudaError_t e_ = (call);                                                               \
+    cudaError_t e_ = (__VA_ARGS__);                                                        \
     if (e_ != cudaSuccess) {                                                               \
-      set_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call);     \
+      set_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #__VA_ARGS__); \
       return e_ == cudaErrorMemoryAllocation ? HZ_ERR_OOM : HZ_ERR_CUDA;                    \
     }                                                                                      \
   } while (0)
 
-#define HZ_TRY(call)                   \
+#define HZ_TRY(...)                    \
   do {                                 \
-    hz_status s_ = (call);             \
+    hz_status s_ = (__VA_ARGS__);      \
     if (s_ < 0) return s_;             \
   } while (0)
 
@@ -126,6 +126,7 @@ struct hz_table {
 struct SolverWork {
   int nrhs = 0;
   DBuf rhat, p, v, t, r;        // fields [nrhs][nzl+2][ny][nx]
+  DBuf xlo;                     // compensation term of the c64 iterate (double-float x)
   DBuf dotA, dotB, dotR, dotN;  // fp64 dot buffers
   DBuf state, active;
   DBuf partials, tickets;
@@ -144,13 +145,12 @@ struct hz_coeffs {
   int n_g_dev = 0;             // rows uploaded (>= 2)
   double g_min = 0, g_max = 0, dg = 0;
   DBuf v;                      // [nzl+2][ny][nx] R
-  DBuf tab;                    // [n_g_dev][TAB_STRIDE] R
-  DBuf pml_d[6];               // dm x,y,z ; dp x,y,z (complex R)
+  DBuf tab_f, tab_d;           // [n_g_dev][TAB_STRIDE] float / double rows (float only for C64)
+  DBuf pml_f[6], pml_d[6];     // dm x,y,z ; dp x,y,z (complex float / complex double)
   int lo[3], hi[3];
   std::vector<std::complex<double>> am_h[3], ap_h[3];  // host copies for export
   DBuf partials, tickets;      // apply epilogue scratch
   int zc = 1, nchunks = 1;
-  long long nlanes = 0;
   std::unique_ptr<SolverWork> work;
   size_t esz() const { return dtype == HZ_C64 ? 4 : 8; }   // real element size
   long long plane() const { return (long long)grid.nx * grid.ny; }
@@ -289,10 +289,11 @@ void pml_axis(int n, int npml, double h, double omega, double v_pml, double R,
   }
 }
 
-template <typename R>
-ApplyParams<R> make_params(const hz_coeffs* c) {
+// R: arithmetic type, S: storage type (= the coeffs' dtype)
+template <typename R, typename S = R>
+ApplyParams<R, S> make_params(const hz_coeffs* c) {
   typedef typename Cx<R>::T C;
-  ApplyParams<R> p;
+  ApplyParams<R, S> p;
   memset(&p, 0, sizeof(p));
   p.nx = c->grid.nx;
   p.ny = c->grid.ny;
@@ -301,11 +302,10 @@ ApplyParams<R> make_params(const hz_coeffs* c) {
   p.nzg = c->grid.nz_global;
   p.plane = c->plane();
   p.fstride = c->fstride();
-  p.nlanes = c->nlanes;
   p.zc = c->zc;
   p.nchunks = c->nchunks;
-  p.v = c->v.as<R>();
-  p.tab = c->tab.as<R>();
+  p.v = c->v.as<S>();
+  p.tab = sizeof(R) == 4 ? c->tab_f.as<R>() : c->tab_d.as<R>();
   p.n_g = c->n_g_dev;
   p.g_min = (R)c->g_min;
   p.g_max = (R)c->g_max;
@@ -314,8 +314,8 @@ ApplyParams<R> make_params(const hz_coeffs* c) {
   p.ih2 = (R)(1.0 / (c->h * c->h));
   p.w2 = (R)(c->omega * c->omega);
   for (int a = 0; a < 3; a++) {
-    p.dm[a] = c->pml_d[a].as<C>();
-    p.dp[a] = c->pml_d[3 + a].as<C>();
+    p.dm[a] = sizeof(R) == 4 ? c->pml_f[a].as<C>() : c->pml_d[a].as<C>();
+    p.dp[a] = sizeof(R) == 4 ? c->pml_f[3 + a].as<C>() : c->pml_d[3 + a].as<C>();
     p.lo[a] = c->lo[a];
     p.hi[a] = c->hi[a];
   }
@@ -350,12 +350,12 @@ hz_status allreduce_sum(const hz_coeffs* c, double* buf, size_t n, cudaStream_t 
   return nccl_check(g_nccl.AllReduce(buf, buf, n, ncclDouble, ncclSum, c->ctx->comm, s), "ncclAllReduce");
 }
 
-template <typename R>
-hz_status apply_launch(const hz_coeffs* c, ApplyParams<R>& p, int nrhs, int epi, cudaStream_t s) {
+template <typename R, typename S>
+hz_status apply_launch(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs, int epi, cudaStream_t s) {
   const int K = epi_k(epi);
   if (K > 0) {
     auto* cc = const_cast<hz_coeffs*>(c);
-    const long long nb = ((c->nlanes + 32LL * apply_warps<R>() - 1) / (32LL * apply_warps<R>())) * c->nchunks;
+    const long long nb = apply_nblocks_x<R>(c->grid.nx, c->grid.ny) * c->nchunks;
     HZ_CUDA(cc->partials.ensure(sizeof(double) * (size_t)nb * K * nrhs));
     if (cc->tickets.n < sizeof(unsigned) * (size_t)nrhs) {
       HZ_CUDA(cc->tickets.ensure(sizeof(unsigned) * (size_t)nrhs));
@@ -364,7 +364,7 @@ hz_status apply_launch(const hz_coeffs* c, ApplyParams<R>& p, int nrhs, int epi,
     p.partials = cc->partials.as<double>();
     p.tickets = cc->tickets.as<unsigned>();
   }
-  HZ_CUDA(launch_apply<R>(p, nrhs, c->mass == HZ_MASS_COLLOC, epi, s));
+  HZ_CUDA(launch_apply<R, S>(p, nrhs, c->mass == HZ_MASS_COLLOC, epi, s));
   count_launch();
   return HZ_OK;
 }
@@ -412,12 +412,14 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
       u[5 * i + 3] = w[3];
       u[5 * i + 4] = w[4];
     }
-    std::vector<R> rows((size_t)ng * TAB_STRIDE, R(0));
+    std::vector<double> rows((size_t)ng * TAB_STRIDE, 0.0);
     for (int i = 0; i < ng; i++)
       for (int k = 0; k < 5; k++) {
-        rows[(size_t)i * TAB_STRIDE + k] = (R)u[5 * i + k];
-        rows[(size_t)i * TAB_STRIDE + 5 + k] = (i + 1 < ng) ? (R)(u[5 * (i + 1) + k] - u[5 * i + k]) : R(0);
+        rows[(size_t)i * TAB_STRIDE + k] = u[5 * i + k];
+        rows[(size_t)i * TAB_STRIDE + 5 + k] = (i + 1 < ng) ? (u[5 * (i + 1) + k] - u[5 * i + k]) : 0.0;
       }
+    std::vector<float> rows_f(rows.size());
+    for (size_t i = 0; i < rows.size(); i++) rows_f[i] = (float)rows[i];
     c->n_g_dev = ng;
     c->g_min = T.g_min;
     c->dg = T.dg;
@@ -426,8 +428,12 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
       set_error("hz_assemble_coeffs: table too large for shared memory");
       return HZ_ERR_INVALID_ARG;
     }
-    HZ_CUDA(c->tab.ensure(rows.size() * sizeof(R)));
-    HZ_CUDA(cudaMemcpy(c->tab.p, rows.data(), rows.size() * sizeof(R), cudaMemcpyHostToDevice));
+    HZ_CUDA(c->tab_d.ensure(rows.size() * sizeof(double)));
+    HZ_CUDA(cudaMemcpy(c->tab_d.p, rows.data(), rows.size() * sizeof(double), cudaMemcpyHostToDevice));
+    if (sizeof(R) == 4) {
+      HZ_CUDA(c->tab_f.ensure(rows_f.size() * sizeof(float)));
+      HZ_CUDA(cudaMemcpy(c->tab_f.p, rows_f.data(), rows_f.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
   }
   // ---- velocity with halo planes
   HZ_CUDA(c->v.ensure((size_t)(g->nz_local + 2) * plane * sizeof(R)));
@@ -493,12 +499,15 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
   const double ih2 = 1.0 / (g->h * g->h);
   for (int a = 0; a < 3; a++) {
     pml_axis(ns[a], c->pml.npml, g->h, c->omega, c->v_pml, c->pml.r_coeff, c->am_h[a], c->ap_h[a]);
-    std::vector<C> dm(ns[a]), dp(ns[a]);
+    std::vector<float2> dm(ns[a]), dp(ns[a]);
+    std::vector<double2> dmd(ns[a]), dpd(ns[a]);
     int lo = ns[a], hi = -1;
     for (int i = 0; i < ns[a]; i++) {
       std::complex<double> m = c->am_h[a][i] - ih2, q = c->ap_h[a][i] - ih2;
-      dm[i].x = (R)m.real(); dm[i].y = (R)m.imag();
-      dp[i].x = (R)q.real(); dp[i].y = (R)q.imag();
+      dm[i].x = (float)m.real(); dm[i].y = (float)m.imag();
+      dp[i].x = (float)q.real(); dp[i].y = (float)q.imag();
+      dmd[i].x = m.real(); dmd[i].y = m.imag();
+      dpd[i].x = q.real(); dpd[i].y = q.imag();
     }
     // interior range: the longest run of exactly-zero deltas (contiguous by construction)
     for (int i = 0; i < ns[a]; i++) {
@@ -508,17 +517,20 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
     if (hi < lo) { lo = 1; hi = 0; }   // every node needs the correction
     c->lo[a] = lo;
     c->hi[a] = hi;
-    HZ_CUDA(c->pml_d[a].ensure(ns[a] * sizeof(C)));
-    HZ_CUDA(c->pml_d[3 + a].ensure(ns[a] * sizeof(C)));
-    HZ_CUDA(cudaMemcpy(c->pml_d[a].p, dm.data(), ns[a] * sizeof(C), cudaMemcpyHostToDevice));
-    HZ_CUDA(cudaMemcpy(c->pml_d[3 + a].p, dp.data(), ns[a] * sizeof(C), cudaMemcpyHostToDevice));
+    HZ_CUDA(c->pml_d[a].ensure(ns[a] * sizeof(double2)));
+    HZ_CUDA(c->pml_d[3 + a].ensure(ns[a] * sizeof(double2)));
+    HZ_CUDA(cudaMemcpy(c->pml_d[a].p, dmd.data(), ns[a] * sizeof(double2), cudaMemcpyHostToDevice));
+    HZ_CUDA(cudaMemcpy(c->pml_d[3 + a].p, dpd.data(), ns[a] * sizeof(double2), cudaMemcpyHostToDevice));
+    if (sizeof(R) == 4) {
+      HZ_CUDA(c->pml_f[a].ensure(ns[a] * sizeof(float2)));
+      HZ_CUDA(c->pml_f[3 + a].ensure(ns[a] * sizeof(float2)));
+      HZ_CUDA(cudaMemcpy(c->pml_f[a].p, dm.data(), ns[a] * sizeof(float2), cudaMemcpyHostToDevice));
+      HZ_CUDA(cudaMemcpy(c->pml_f[3 + a].p, dp.data(), ns[a] * sizeof(float2), cudaMemcpyHostToDevice));
+    }
   }
   // ---- launch geometry: strips of NY rows; z chunks sized to give >= ~4 waves
   {
-    const int NY = apply_ny<R>(), W = apply_warps<R>();
-    const long long nstrips = (g->ny + NY - 1) / NY;
-    c->nlanes = nstrips * g->nx;
-    const long long bx = (c->nlanes + 32LL * W - 1) / (32LL * W);
+    const long long bx = apply_nblocks_x<R>(g->nx, g->ny);
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device);
     const long long target = 4LL * dev_sms * apply_occupancy<R>(mass == HZ_MASS_COLLOC);
@@ -726,6 +738,10 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   HZ_CUDA(w.v.ensure(fb));
   HZ_CUDA(w.t.ensure(fb));
   HZ_CUDA(w.r.ensure(fb));
+  if (sizeof(R) == 4) {
+    HZ_CUDA(w.xlo.ensure(fb));
+    HZ_CUDA(cudaMemsetAsync(w.xlo.p, 0, fb, s));
+  }
   HZ_CUDA(w.dotA.ensure(sizeof(double) * 2 * nrhs));
   HZ_CUDA(w.dotB.ensure(sizeof(double) * 7 * nrhs));
   HZ_CUDA(w.dotR.ensure(sizeof(double) * 3 * nrhs));
@@ -756,10 +772,23 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   }
   std::vector<int> active(nrhs, 1), iters(nrhs, 0);
   HZ_CUDA(cudaMemcpyAsync(w.active.p, active.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
+  auto n_active = [&]() {
+    int k = 0;
+    for (int r = 0; r < nrhs; r++) k += active[r] != 0;
+    return k;
+  };
 
   EventTimer timer;
   timer.on = o.timing != 0;
   long long apply_launches = 0;
+  double apply_bytes = 0.0, apply_points = 0.0;
+  // algorithmic bytes of one apply launch: v (shared by the RHS) + per active RHS the fields
+  // the epilogue touches (u in, out, plus r̂0 / b reads)
+  auto account = [&](int nfields_per_rhs) {
+    apply_bytes += (double)n * ((double)sizeof(R) + (double)n_active() * nfields_per_rhs * (double)sizeof(C));
+    apply_points += (double)n * (double)n_active();
+    apply_launches++;
+  };
   ApplyParams<R> base = make_params<R>(c);
   base.active = w.active.as<int>();
   VecParams<R> q;
@@ -774,6 +803,7 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   q.p = w.p.as<C>();
   q.v = w.v.as<C>();
   q.t = w.t.as<C>();
+  q.xlo = sizeof(R) == 4 ? w.xlo.as<C>() : nullptr;
   q.dotA = w.dotA.as<double>();
   q.dotB = w.dotB.as<double>();
   q.dotR = w.dotR.as<double>();
@@ -782,19 +812,34 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   q.state = w.state.as<SolverState>();
   q.active = w.active.as<int>();
 
-  // r = b − A x (RESID epilogue; writes r, ‖r‖², (r̂0, r))
+  // r = b − A x (RESID epilogue; writes r, ‖r‖², (r̂0, r)).  For complex64 the residual is
+  // computed in fp64 arithmetic on the c64 storage (reading A21): the fp32 apply's rounding
+  // (~eps32·‖|A||x|‖/‖b‖ ≈ 1e-6 on config 1) would otherwise set the attainable true residual.
+  bool use_lo = sizeof(R) == 4;   // false for the final residual of the rounded output x
   auto resid = [&](bool with_rhat) -> hz_status {
     HZ_TRY(halo_exchange(c, x, nrhs, sizeof(C), s));
-    ApplyParams<R> p = base;
-    p.u = x;
-    p.au = w.r.as<C>();
-    p.bvec = b;
-    p.rhat = with_rhat ? w.rhat.as<C>() : nullptr;
-    p.dots = w.dotR.as<double>();
     timer.mark(s);
-    HZ_TRY(apply_launch<R>(c, p, nrhs, EPI_RESID, s));
+    if constexpr (sizeof(R) == 4) {
+      ApplyParams<double, float> p = make_params<double, float>(c);
+      p.active = w.active.as<int>();
+      p.u = x;
+      p.ulo = use_lo ? w.xlo.as<C>() : nullptr;
+      p.au = w.r.as<C>();
+      p.bvec = b;
+      p.rhat = with_rhat ? w.rhat.as<C>() : nullptr;
+      p.dots = w.dotR.as<double>();
+      HZ_TRY(apply_launch<double, float>(c, p, nrhs, EPI_RESID, s));
+    } else {
+      ApplyParams<R> p = base;
+      p.u = x;
+      p.au = w.r.as<C>();
+      p.bvec = b;
+      p.rhat = with_rhat ? w.rhat.as<C>() : nullptr;
+      p.dots = w.dotR.as<double>();
+      HZ_TRY(apply_launch<R, R>(c, p, nrhs, EPI_RESID, s));
+    }
     timer.mark(s);
-    apply_launches++;
+    account((with_rhat ? 4 : 3) + (use_lo ? 1 : 0));
     HZ_TRY(allreduce_sum(c, w.dotR.as<double>(), 3 * (size_t)nrhs, s));
     return HZ_OK;
   };
@@ -827,11 +872,11 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   int it = 0;
   std::vector<double> hdot(3 * nrhs);
   std::vector<SolverState> hst(nrhs);
-  auto any_active = [&]() {
-    for (int r = 0; r < nrhs; r++)
-      if (active[r]) return true;
-    return false;
-  };
+  // stagnation guard: best true residual per RHS and the iteration it was reached
+  std::vector<double> best(nrhs, HUGE_VAL);
+  std::vector<int> best_it(nrhs, 0);
+  bool stagnated_any = false;
+  const int stall_iters = std::max(20 * std::max(1, o.replace_every), 1000);
   // initial convergence check (x0 may already solve the system)
   HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
   HZ_CUDA(cudaStreamSynchronize(s));
@@ -839,7 +884,30 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
     if (active[r] && hdot[3 * r] <= rtol2 * bn2[r]) active[r] = 0;
   HZ_CUDA(cudaMemcpyAsync(w.active.p, active.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
 
-  while (any_active() && it < o.max_iter) {
+  // deactivate RHS whose TRUE residual (in hdot after a resid) meets rtol or has stagnated
+  auto retire = [&](bool true_resid) -> hz_status {
+    bool changed = false;
+    for (int r = 0; r < nrhs; r++) {
+      if (!active[r]) continue;
+      if (hdot[3 * r] <= rtol2 * bn2[r]) {
+        active[r] = 0;
+        changed = true;
+      } else if (true_resid) {
+        if (hdot[3 * r] < 0.81 * best[r]) {   // ≥ 10% reduction of the norm
+          best[r] = hdot[3 * r];
+          best_it[r] = it;
+        } else if (it - best_it[r] >= stall_iters) {
+          active[r] = 0;
+          changed = true;
+          stagnated_any = true;
+        }
+      }
+    }
+    if (changed) HZ_CUDA(cudaMemcpyAsync(w.active.p, active.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
+    return HZ_OK;
+  };
+
+  while (n_active() > 0 && it < o.max_iter) {
     // v = A p, (r̂0, v)
     HZ_TRY(halo_exchange(c, w.p.p, nrhs, sizeof(C), s));
     {
@@ -849,9 +917,9 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
       p.rhat = w.rhat.as<C>();
       p.dots = w.dotA.as<double>();
       timer.mark(s);
-      HZ_TRY(apply_launch<R>(c, p, nrhs, EPI_DOT1, s));
+      HZ_TRY(apply_launch<R, R>(c, p, nrhs, EPI_DOT1, s));
       timer.mark(s);
-      apply_launches++;
+      account(3);
       HZ_TRY(allreduce_sum(c, w.dotA.as<double>(), 2 * (size_t)nrhs, s));
     }
     HZ_TRY(vec(BICG_S));  // s = r − α v (in r)
@@ -864,9 +932,9 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
       p.rhat = w.rhat.as<C>();
       p.dots = w.dotB.as<double>();
       timer.mark(s);
-      HZ_TRY(apply_launch<R>(c, p, nrhs, EPI_DOT4, s));
+      HZ_TRY(apply_launch<R, R>(c, p, nrhs, EPI_DOT4, s));
       timer.mark(s);
-      apply_launches++;
+      account(3);
       HZ_TRY(allreduce_sum(c, w.dotB.as<double>(), 7 * (size_t)nrhs, s));
     }
     HZ_TRY(vec(BICG_UPDATE));  // x, r, p; ‖r‖²
@@ -874,12 +942,13 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
     ++it;
     for (int r = 0; r < nrhs; r++)
       if (active[r]) iters[r]++;
-    if (o.replace_every > 0 && it % o.replace_every == 0) {
+    const bool replaced = o.replace_every > 0 && it % o.replace_every == 0;
+    if (replaced) {
       HZ_TRY(resid(true));
       HZ_TRY(vec(BICG_RHO_RESET));
       replacements++;
     }
-    if (it % std::max(1, o.check_every) == 0 || it >= o.max_iter) {
+    if (replaced || it % std::max(1, o.check_every) == 0 || it >= o.max_iter) {
       HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
       HZ_CUDA(cudaMemcpyAsync(hst.data(), w.state.p, sizeof(SolverState) * nrhs, cudaMemcpyDeviceToHost, s));
       HZ_CUDA(cudaStreamSynchronize(s));
@@ -896,24 +965,22 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
         if (restarts > 50) break;
         continue;
       }
-      if (cand) {  // verify on the recomputed TRUE residual (A21)
+      if (replaced) {
+        HZ_TRY(retire(true));           // hdot holds the recomputed true residuals
+      } else if (cand) {                // verify on the recomputed TRUE residual (A21)
         HZ_TRY(resid(true));
         HZ_TRY(vec(BICG_RHO_RESET));
         replacements++;
         HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
         HZ_CUDA(cudaStreamSynchronize(s));
-        bool changed = false;
-        for (int r = 0; r < nrhs; r++)
-          if (active[r] && hdot[3 * r] <= rtol2 * bn2[r]) {
-            active[r] = 0;
-            changed = true;
-          }
-        if (changed) HZ_CUDA(cudaMemcpyAsync(w.active.p, active.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
+        HZ_TRY(retire(true));
       }
     }
   }
-  // final true residuals for every RHS
+  // final true residuals for every RHS, of the output x itself (the rounded double-word iterate)
+  use_lo = false;
   std::vector<int> all(nrhs, 1);
+  active = all;
   HZ_CUDA(cudaMemcpyAsync(w.active.p, all.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
   HZ_TRY(resid(false));
   HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
@@ -933,9 +1000,12 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
     stats->apply_ms_total = timer.on ? timer.total_ms() : 0.0;
     stats->apply_launches = apply_launches;
     stats->kernel_launches = g_launches.load() - launches0;
-    stats->bytes_per_apply = (double)n * (double)(sizeof(R) + 2 * sizeof(C));
+    stats->apply_bytes_total = apply_bytes;
+    stats->apply_points_total = apply_points;
     stats->replacements = replacements;
     stats->restarts = restarts;
+    stats->iterations = it;
+    stats->stagnated = stagnated_any ? 1 : 0;
   }
   if (conv) return HZ_OK;
   return restarts > 50 ? HZ_BREAKDOWN : HZ_NOT_CONVERGED;

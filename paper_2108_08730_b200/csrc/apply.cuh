@@ -43,18 +43,23 @@ __host__ __device__ constexpr int epi_k(int epi) { return epi == 1 ? 2 : (epi ==
 
 constexpr int TAB_STRIDE = 12;   // table row: t1 t2 mu0 mu1 mu2 | dt1 dt2 dmu0 dmu1 dmu2 | pad pad
 
-template <typename R>
+// R: arithmetic type; S: storage type of the fields and the velocity (S = R except the
+// mixed-precision residual of the complex64 solver, which reads c64 storage and computes in fp64).
+template <typename R, typename S = R>
 struct ApplyParams {
   typedef typename Cx<R>::T C;
+  typedef typename Cx<S>::T CS;
   int nx, ny, nzl;            // local slab dims
   int z0, nzg;                // global index of local plane 0, global nz
   long long plane;            // nx*ny
   long long fstride;          // (nzl+2)*plane: per-RHS field stride (elements)
-  long long nlanes;           // nstrips*nx
+  long long nlanes;           // nstrips*nx (set by the launcher)
   int zc, nchunks;            // z planes per CTA chunk, number of chunks
-  const R* v;                 // [nzl+2][ny][nx] velocity incl. halo planes
-  const C* u;                 // [nrhs][nzl+2][ny][nx]
-  C* au;                      // output
+  const S* v;                 // [nzl+2][ny][nx] velocity incl. halo planes
+  const CS* u;                // [nrhs][nzl+2][ny][nx]
+  const CS* ulo;              // optional low part of u (mixed-precision residual of the c64 solver:
+                              // u = u + ulo in fp64; only read when R != S), else null
+  CS* au;                     // output
   const R* tab;               // [n_g][TAB_STRIDE]
   int n_g;                    // >= 2
   R g_min, g_max, inv_dg, inv_fh, ih2, w2;
@@ -62,8 +67,8 @@ struct ApplyParams {
   const C* dp[3];             // PML δ⁺
   int lo[3], hi[3];           // per-axis index range where δ± == 0 (inclusive)
   // epilogue inputs / outputs
-  const C* rhat;              // r̂0 (DOT1, DOT4, RESID) — may be null for RESID
-  const C* bvec;              // b (RESID)
+  const CS* rhat;             // r̂0 (DOT1, DOT4, RESID) — may be null for RESID
+  const CS* bvec;             // b (RESID)
   double* partials;           // [nrhs][gridDim.x*gridDim.y][K]
   double* dots;               // [nrhs][K]
   unsigned int* tickets;      // [nrhs]
@@ -94,8 +99,8 @@ __device__ __forceinline__ void interp_weights(R v, const R* __restrict__ tab, i
   mu2 = fma(tau, row[9], row[4]);
 }
 
-template <typename R>
-__device__ __forceinline__ RowCoef<R> row_coef(R v, const R* __restrict__ tab, const ApplyParams<R>& p) {
+template <typename R, typename S>
+__device__ __forceinline__ RowCoef<R> row_coef(R v, const R* __restrict__ tab, const ApplyParams<R, S>& p) {
   R t1, t2, mu0, mu1, mu2;
   interp_weights<R>(v, tab, p.n_g, p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
   RowCoef<R> c;
@@ -116,9 +121,22 @@ __device__ __forceinline__ RowCoef<R> row_coef(R v, const R* __restrict__ tab, c
 // ---------------------------------------------------------------------------------------------
 // PML correction for one row (slow path).  zl: local plane index of the output.
 // ---------------------------------------------------------------------------------------------
-template <typename R>
-__device__ __noinline__ typename Cx<R>::T pml_correction(const ApplyParams<R>& p, const R* __restrict__ tab,
-                                                         const typename Cx<R>::T* __restrict__ ub,
+// field value at element idx of this RHS: storage → arithmetic type, plus the compensation term
+// of the double-float iterate in the mixed-precision residual (R = double, S = float)
+template <typename R, typename S>
+__device__ __forceinline__ typename Cx<R>::T load_u(const typename Cx<S>::T* __restrict__ ub,
+                                                    const typename Cx<S>::T* __restrict__ ulb, long long idx) {
+  typename Cx<R>::T u = to_cx(ldg_c(ub + idx), R(0));
+  if constexpr (sizeof(R) != sizeof(S)) {
+    if (ulb != nullptr) u = cadd(u, to_cx(ldg_c(ulb + idx), R(0)));
+  }
+  return u;
+}
+
+template <typename R, typename S>
+__device__ __noinline__ typename Cx<R>::T pml_correction(const ApplyParams<R, S>& p, const R* __restrict__ tab,
+                                                         const typename Cx<S>::T* __restrict__ ub,
+                                                         const typename Cx<S>::T* __restrict__ ulb,
                                                          int x, int y, int zl) {
   typedef typename Cx<R>::T C;
   const int zg = p.z0 + zl;
@@ -131,10 +149,10 @@ __device__ __noinline__ typename Cx<R>::T pml_correction(const ApplyParams<R>& p
       for (int dx = 0; dx < 3; dx++) {
         int xx = x + dx - 1, yy = y + dy - 1, zz = zg + dz - 1;
         bool in = xx >= 0 && xx < p.nx && yy >= 0 && yy < p.ny && zz >= 0 && zz < p.nzg;
-        n[dz][dy][dx] = in ? ldg_c(ub + (long long)(zl + dz) * p.plane + (long long)yy * p.nx + xx) : czero(R(0));
+        n[dz][dy][dx] = in ? load_u<R, S>(ub, ulb, (long long)(zl + dz) * p.plane + (long long)yy * p.nx + xx) : czero(R(0));
       }
   R t1, t2, mu0, mu1, mu2;
-  const R vv = p.v[(long long)(zl + 1) * p.plane + (long long)y * p.nx + x];
+  const R vv = (R)p.v[(long long)(zl + 1) * p.plane + (long long)y * p.nx + x];
   interp_weights<R>(vv, tab, p.n_g, p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
   const R t0 = (R)1 - (R)4 * (t1 + t2);
   C corr = czero(R(0));

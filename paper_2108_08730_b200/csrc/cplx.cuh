@@ -77,4 +77,12 @@ __device__ __forceinline__ double2 shfl_down_c(double2 a, int d) {
   return make_double2(__shfl_down_sync(0xffffffffu, a.x, d), __shfl_down_sync(0xffffffffu, a.y, d));
 }
 
+// ---- storage <-> compute conversion (mixed-precision residual: c64 storage, fp64 arithmetic) ----
+__device__ __forceinline__ float2 to_cx(float2 a, float) { return a; }
+__device__ __forceinline__ double2 to_cx(double2 a, double) { return a; }
+__device__ __forceinline__ double2 to_cx(float2 a, double) { return make_double2((double)a.x, (double)a.y); }
+__device__ __forceinline__ float2 from_cx(float2 a, float) { return a; }
+__device__ __forceinline__ double2 from_cx(double2 a, double) { return a; }
+__device__ __forceinline__ float2 from_cx(double2 a, float) { return make_float2((float)a.x, (float)a.y); }
+
 }  // namespace hz

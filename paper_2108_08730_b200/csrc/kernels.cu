@@ -12,9 +12,10 @@ namespace hz {
 // =============================================================================================
 // K2: apply (a2–a6 fused), EPI selects the fused BiCGSTAB epilogue
 // =============================================================================================
-template <typename R, int NY, int WARPS, bool COLLOC, int EPI>
-__global__ void __launch_bounds__(32 * WARPS) apply27_kernel(ApplyParams<R> p) {
+template <typename R, typename S, int NY, int WARPS, bool COLLOC, int EPI>
+__global__ void __launch_bounds__(32 * WARPS) apply27_kernel(ApplyParams<R, S> p) {
   typedef typename Cx<R>::T C;
+  typedef typename Cx<S>::T CS;
   constexpr int K = epi_k(EPI);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* tab = reinterpret_cast<R*>(smem_raw);
@@ -37,8 +38,9 @@ __global__ void __launch_bounds__(32 * WARPS) apply27_kernel(ApplyParams<R> p) {
 
   const int zc0 = blockIdx.y * p.zc;
   const int zc1 = min(zc0 + p.zc, p.nzl);
-  const C* __restrict__ ub = p.u + (long long)rhs * p.fstride;
-  C* __restrict__ aub = p.au + (long long)rhs * p.fstride;
+  const CS* __restrict__ ub = p.u + (long long)rhs * p.fstride;
+  CS* __restrict__ aub = p.au + (long long)rhs * p.fstride;
+  const CS* __restrict__ ulb = p.ulo ? p.ulo + (long long)rhs * p.fstride : nullptr;
   const C czv = czero(R(0));
 
   C accP[NY], accC[NY];
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(32 * WARPS) apply27_kernel(ApplyParams<R> p) {
 #pragma unroll
     for (int i = 0; i < NY; i++) {
       const int y = y0 + i;
-      vown[i] = (lane_ok && pin && y < p.ny) ? __ldg(p.v + (long long)(pl + 1) * p.plane + (long long)y * p.nx + x) : R(1);
+      vown[i] = (lane_ok && pin && y < p.ny) ? (R)__ldg(p.v + (long long)(pl + 1) * p.plane + (long long)y * p.nx + x) : R(1);
     }
   }
 
@@ -80,12 +82,12 @@ __global__ void __launch_bounds__(32 * WARPS) apply27_kernel(ApplyParams<R> p) {
       const int y = y0 - 1 + r;
       const bool rv = lane_ok && pin && y >= 0 && y < p.ny;
       const long long o = pbase + (long long)y * p.nx;
-      uc[r] = rv ? ldg_c(ub + o + x) : czv;
-      ue[r] = (rv && edge_ld) ? ldg_c(ub + o + xe) : czv;
+      uc[r] = rv ? load_u<R, S>(ub, ulb, o + x) : czv;
+      ue[r] = (rv && edge_ld) ? load_u<R, S>(ub, ulb, o + xe) : czv;
       if (!COLLOC) {
-        if (r == 0 || r == NY + 1) vc[r] = rv ? __ldg(p.v + o + x) : R(1);
+        if (r == 0 || r == NY + 1) vc[r] = rv ? (R)__ldg(p.v + o + x) : R(1);
         else vc[r] = vown[r - 1];
-        ve[r] = (rv && edge_ld) ? __ldg(p.v + o + xe) : R(1);
+        ve[r] = (rv && edge_ld) ? (R)__ldg(p.v + o + xe) : R(1);
       }
     }
     // v of plane pl+1 at own rows (coefficients of the next plane; r of the next iteration)
@@ -95,7 +97,7 @@ __global__ void __launch_bounds__(32 * WARPS) apply27_kernel(ApplyParams<R> p) {
 #pragma unroll
       for (int i = 0; i < NY; i++) {
         const int y = y0 + i;
-        vnx[i] = (lane_ok && pin1 && y < p.ny) ? __ldg(p.v + pbase + p.plane + (long long)y * p.nx + x) : R(1);
+        vnx[i] = (lane_ok && pin1 && y < p.ny) ? (R)__ldg(p.v + pbase + p.plane + (long long)y * p.nx + x) : R(1);
       }
     }
 
@@ -153,21 +155,22 @@ __global__ void __launch_bounds__(32 * WARPS) apply27_kernel(ApplyParams<R> p) {
         if (lane_ok && y < p.ny) {
           const int zgo = p.z0 + zo;
           if (x < p.lo[0] || x > p.hi[0] || y < p.lo[1] || y > p.hi[1] || zgo < p.lo[2] || zgo > p.hi[2])
-            a = cadd(a, pml_correction<R>(p, tab, ub, x, y, zo));
+            a = cadd(a, pml_correction<R, S>(p, tab, ub, ulb, x, y, zo));
           const long long o = (long long)(zo + 1) * p.plane + (long long)y * p.nx + x;
           if (EPI == EPI_RESID) {
-            const C bb = ldg_c(p.bvec + (long long)rhs * p.fstride + o);
+            const C bb = to_cx(ldg_c(p.bvec + (long long)rhs * p.fstride + o), R(0));
             const C rr = csub(bb, a);
-            aub[o] = rr;
+            aub[o] = from_cx(rr, S(0));
             part[0] += (double)rr.x * (double)rr.x + (double)rr.y * (double)rr.y;
-            if (p.rhat != nullptr) acc_cdot(part[1], part[2], ldg_c(p.rhat + (long long)rhs * p.fstride + o), rr);
+            if (p.rhat != nullptr)
+              acc_cdot(part[1], part[2], to_cx(ldg_c(p.rhat + (long long)rhs * p.fstride + o), R(0)), rr);
           } else {
-            aub[o] = a;
+            aub[o] = from_cx(a, S(0));
             if (EPI == EPI_DOT1) {
-              acc_cdot(part[0], part[1], ldg_c(p.rhat + (long long)rhs * p.fstride + o), a);
+              acc_cdot(part[0], part[1], to_cx(ldg_c(p.rhat + (long long)rhs * p.fstride + o), R(0)), a);
             } else if (EPI == EPI_DOT4) {
-              const C s = ldg_c(ub + o);
-              const C rh = ldg_c(p.rhat + (long long)rhs * p.fstride + o);
+              const C s = to_cx(ldg_c(ub + o), R(0));
+              const C rh = to_cx(ldg_c(p.rhat + (long long)rhs * p.fstride + o), R(0));
               acc_cdot(part[0], part[1], a, s);
               part[2] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
               acc_cdot(part[3], part[4], rh, s);
@@ -331,6 +334,17 @@ __device__ __forceinline__ double2 zdiv(double2 a, double2 b) {
   const double d = b.x * b.x + b.y * b.y;
   return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
 }
+// error-free sum (Knuth TwoSum): s = fl(a + b), e = (a + b) − s exactly
+__device__ __forceinline__ void two_sum(float a, float b, float& s, float& e) {
+  s = __fadd_rn(a, b);
+  const float bp = __fsub_rn(s, a);
+  e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bp)), __fsub_rn(b, bp));
+}
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bp = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bp)), __dsub_rn(b, bp));
+}
 __device__ __forceinline__ double2 zmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -444,9 +458,19 @@ __global__ void __launch_bounds__(NT) bicg_update_kernel(VecParams<R> q) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < q.n; i += (long long)gridDim.x * blockDim.x) {
     const C s = q.r[off + i], t = q.t[off + i], pp = q.p[off + i], vv = q.v[off + i];
     C xx = q.x[off + i];
-    // x += α p + ω s
-    xx.x += (a.x * pp.x - a.y * pp.y) + (w.x * s.x - w.y * s.y);
-    xx.y += (a.x * pp.y + a.y * pp.x) + (w.x * s.y + w.y * s.x);
+    // x += α p + ω s; with q.xlo the iterate is the double-word x + xlo (compensated update)
+    C dx;
+    dx.x = (a.x * pp.x - a.y * pp.y) + (w.x * s.x - w.y * s.y);
+    dx.y = (a.x * pp.y + a.y * pp.x) + (w.x * s.y + w.y * s.x);
+    if (q.xlo != nullptr) {
+      C lo = q.xlo[off + i];
+      two_sum(xx.x, dx.x + lo.x, xx.x, lo.x);
+      two_sum(xx.y, dx.y + lo.y, xx.y, lo.y);
+      q.xlo[off + i] = lo;
+    } else {
+      xx.x += dx.x;
+      xx.y += dx.y;
+    }
     // r = s − ω t
     C r;
     r.x = s.x - (w.x * t.x - w.y * t.y);
@@ -486,24 +510,35 @@ __global__ void __launch_bounds__(NT) norm2_kernel(const typename Cx<R>::T* __re
 // =============================================================================================
 // host-side launchers (kernels.h)
 // =============================================================================================
-template <typename R, int NY, int WARPS, bool COLLOC, int EPI>
-static cudaError_t launch_apply_t(const ApplyParams<R>& p, int nrhs, cudaStream_t s) {
-  auto kern = apply27_kernel<R, NY, WARPS, COLLOC, EPI>;
+template <typename R> struct ApplyCfg;
+template <> struct ApplyCfg<float> { enum { NY = 4, WARPS = 4 }; };
+template <> struct ApplyCfg<double> { enum { NY = 2, WARPS = 4 }; };
+
+template <typename R>
+long long apply_nblocks_x(int nx, int ny) {
+  constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
+  const long long nlanes = (long long)((ny + NY - 1) / NY) * nx;
+  return (nlanes + 32LL * W - 1) / (32LL * W);
+}
+template long long apply_nblocks_x<float>(int, int);
+template long long apply_nblocks_x<double>(int, int);
+
+template <typename R, typename S, bool COLLOC, int EPI>
+static cudaError_t launch_apply_t(ApplyParams<R, S> p, int nrhs, cudaStream_t s) {
+  constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
+  auto kern = apply27_kernel<R, S, NY, W, COLLOC, EPI>;
   const size_t smem = (size_t)p.n_g * TAB_STRIDE * sizeof(R);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr_set = true;
   }
-  const long long nb = (p.nlanes + 32 * WARPS - 1) / (32 * WARPS);
+  p.nlanes = (long long)((p.ny + NY - 1) / NY) * p.nx;
+  const long long nb = apply_nblocks_x<R>(p.nx, p.ny);
   dim3 grid((unsigned)nb, (unsigned)p.nchunks, (unsigned)nrhs);
-  kern<<<grid, 32 * WARPS, smem, s>>>(p);
+  kern<<<grid, 32 * W, smem, s>>>(p);
   return cudaGetLastError();
 }
-
-template <typename R> struct ApplyCfg;
-template <> struct ApplyCfg<float> { enum { NY = 4, WARPS = 4 }; };
-template <> struct ApplyCfg<double> { enum { NY = 2, WARPS = 4 }; };
 
 template <typename R>
 int apply_ny() { return ApplyCfg<R>::NY; }
@@ -514,37 +549,47 @@ int apply_warps() { return ApplyCfg<R>::WARPS; }
 template int apply_warps<float>();
 template int apply_warps<double>();
 
-template <typename R>
-cudaError_t launch_apply(const ApplyParams<R>& p, int nrhs, bool colloc, int epi, cudaStream_t s) {
-  constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
+template <typename R, typename S>
+cudaError_t launch_apply(const ApplyParams<R, S>& p, int nrhs, bool colloc, int epi, cudaStream_t s) {
   if (!colloc) {
     switch (epi) {
-      case EPI_PLAIN: return launch_apply_t<R, NY, W, false, EPI_PLAIN>(p, nrhs, s);
-      case EPI_DOT1: return launch_apply_t<R, NY, W, false, EPI_DOT1>(p, nrhs, s);
-      case EPI_DOT4: return launch_apply_t<R, NY, W, false, EPI_DOT4>(p, nrhs, s);
-      case EPI_RESID: return launch_apply_t<R, NY, W, false, EPI_RESID>(p, nrhs, s);
+      case EPI_PLAIN: return launch_apply_t<R, S, false, EPI_PLAIN>(p, nrhs, s);
+      case EPI_DOT1: return launch_apply_t<R, S, false, EPI_DOT1>(p, nrhs, s);
+      case EPI_DOT4: return launch_apply_t<R, S, false, EPI_DOT4>(p, nrhs, s);
+      case EPI_RESID: return launch_apply_t<R, S, false, EPI_RESID>(p, nrhs, s);
     }
   } else {
     switch (epi) {
-      case EPI_PLAIN: return launch_apply_t<R, NY, W, true, EPI_PLAIN>(p, nrhs, s);
-      case EPI_DOT1: return launch_apply_t<R, NY, W, true, EPI_DOT1>(p, nrhs, s);
-      case EPI_DOT4: return launch_apply_t<R, NY, W, true, EPI_DOT4>(p, nrhs, s);
-      case EPI_RESID: return launch_apply_t<R, NY, W, true, EPI_RESID>(p, nrhs, s);
+      case EPI_PLAIN: return launch_apply_t<R, S, true, EPI_PLAIN>(p, nrhs, s);
+      case EPI_DOT1: return launch_apply_t<R, S, true, EPI_DOT1>(p, nrhs, s);
+      case EPI_DOT4: return launch_apply_t<R, S, true, EPI_DOT4>(p, nrhs, s);
+      case EPI_RESID: return launch_apply_t<R, S, true, EPI_RESID>(p, nrhs, s);
     }
   }
   return cudaErrorInvalidValue;
 }
-template cudaError_t launch_apply<float>(const ApplyParams<float>&, int, bool, int, cudaStream_t);
-template cudaError_t launch_apply<double>(const ApplyParams<double>&, int, bool, int, cudaStream_t);
+template cudaError_t launch_apply<float, float>(const ApplyParams<float, float>&, int, bool, int, cudaStream_t);
+template cudaError_t launch_apply<double, double>(const ApplyParams<double, double>&, int, bool, int, cudaStream_t);
+
+// mixed precision (c64 storage, fp64 arithmetic): residual and plain apply only
+template <>
+cudaError_t launch_apply<double, float>(const ApplyParams<double, float>& p, int nrhs, bool colloc, int epi,
+                                        cudaStream_t s) {
+  if (epi == EPI_RESID) return colloc ? launch_apply_t<double, float, true, EPI_RESID>(p, nrhs, s)
+                                      : launch_apply_t<double, float, false, EPI_RESID>(p, nrhs, s);
+  if (epi == EPI_PLAIN) return colloc ? launch_apply_t<double, float, true, EPI_PLAIN>(p, nrhs, s)
+                                      : launch_apply_t<double, float, false, EPI_PLAIN>(p, nrhs, s);
+  return cudaErrorInvalidValue;
+}
 
 template <typename R>
 int apply_occupancy(bool colloc) {
   constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
   int nb = 0;
   if (colloc)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_kernel<R, NY, W, true, EPI_DOT4>, 32 * W, 16 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_kernel<R, R, NY, W, true, EPI_DOT4>, 32 * W, 16 * 1024);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_kernel<R, NY, W, false, EPI_DOT4>, 32 * W, 16 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_kernel<R, R, NY, W, false, EPI_DOT4>, 32 * W, 16 * 1024);
   return nb > 0 ? nb : 1;
 }
 template int apply_occupancy<float>(bool);

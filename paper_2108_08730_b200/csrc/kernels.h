@@ -24,6 +24,7 @@ struct VecParams {
   long long fstride;  // per-RHS stride
   int nblocks;        // CTAs per RHS
   C *x, *r, *rhat, *p, *v, *t;
+  C* xlo;              // compensation term of the iterate (complex64 solver) or null
   const double* dotA;  // [nrhs][2]
   const double* dotB;  // [nrhs][7]
   double* dotR;        // [nrhs][3]
@@ -38,7 +39,12 @@ enum { BICG_INIT = 0, BICG_S = 1, BICG_UPDATE = 2, BICG_RHO_RESET = 3 };
 template <typename R> int apply_ny();
 template <typename R> int apply_warps();
 template <typename R> int apply_occupancy(bool colloc);
-template <typename R> cudaError_t launch_apply(const ApplyParams<R>& p, int nrhs, bool colloc, int epi, cudaStream_t s);
+template <typename R> long long apply_nblocks_x(int nx, int ny);   // CTAs along x of one z-chunk
+template <typename R, typename S>
+cudaError_t launch_apply(const ApplyParams<R, S>& p, int nrhs, bool colloc, int epi, cudaStream_t s);
+template <>
+cudaError_t launch_apply<double, float>(const ApplyParams<double, float>& p, int nrhs, bool colloc, int epi,
+                                        cudaStream_t s);
 template <typename R> cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s);
 template <typename R>
 cudaError_t launch_sources(const ApplyParams<R>& p, int nsrc, const long long* nodes, const double* amps,

@@ -56,8 +56,10 @@ class hz_solve_opts(ct.Structure):
 
 class hz_solve_stats(ct.Structure):
     _fields_ = [("apply_ms_total", ct.c_double), ("apply_launches", ct.c_longlong),
-                ("kernel_launches", ct.c_longlong), ("bytes_per_apply", ct.c_double),
-                ("replacements", ct.c_int), ("restarts", ct.c_int)]
+                ("kernel_launches", ct.c_longlong), ("apply_bytes_total", ct.c_double),
+                ("apply_points_total", ct.c_double),
+                ("replacements", ct.c_int), ("restarts", ct.c_int), ("iterations", ct.c_int),
+                ("stagnated", ct.c_int)]
 
 
 _vp = ct.c_void_p
@@ -132,8 +134,11 @@ class Ctx:
         self._h = handle
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.hz_ctx_destroy(self._h)
+        if getattr(self, "_h", None) and _lib is not None:
+            try:
+                _lib.hz_ctx_destroy(self._h)
+            except Exception:   # interpreter shutdown
+                pass
             self._h = None
 
 
@@ -155,8 +160,11 @@ class Table:
         self._h = handle
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.hz_table_destroy(self._h)
+        if getattr(self, "_h", None) and _lib is not None:
+            try:
+                _lib.hz_table_destroy(self._h)
+            except Exception:   # interpreter shutdown
+                pass
             self._h = None
 
     @property
@@ -210,8 +218,11 @@ class Coeffs:
         self._ctx = ctx   # keep the context alive
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.hz_coeffs_destroy(self._h)
+        if getattr(self, "_h", None) and _lib is not None:
+            try:
+                _lib.hz_coeffs_destroy(self._h)
+            except Exception:   # interpreter shutdown
+                pass
             self._h = None
 
     @property
