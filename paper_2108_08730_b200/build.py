@@ -8,11 +8,11 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libhz.so")
+OBJ = os.environ.get("HZ_BUILD_DIR") or os.path.join(HERE, "_build")
+LIB = os.environ.get("HZ_LIB") or os.path.join(HERE, "libhz.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
+FLAGS = ["-O3", "-lineinfo"] + os.environ.get("HZ_EXTRA_NVCC", "").split() + ["-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I" + os.path.join(HERE, "..", "include")]
 SOURCES = ["kernels.cu", "api.cu", "table.cpp"]
 

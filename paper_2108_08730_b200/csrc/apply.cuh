@@ -55,7 +55,10 @@ struct ApplyParams {
   long long fstride;          // (nzl+2)*plane: per-RHS field stride (elements)
   long long nlanes;           // nstrips*nx (set by the launcher)
   int zc, nchunks;            // z planes per CTA chunk, number of chunks
+  int nbx, nrhs;              // CTAs along the flattened (strip, x) axis; RHS in the launch
   const S* v;                 // [nzl+2][ny][nx] velocity incl. halo planes
+  const S* w;                 // [nzl+2][ny][nx] 1/v² incl. halo planes (apply input)
+  const R* ctab;              // [n_g][CTAB_STRIDE] pre-scaled class coefficients + differences
   const CS* u;                // [nrhs][nzl+2][ny][nx]
   const CS* ulo;              // optional low part of u (mixed-precision residual of the c64 solver:
                               // u = u + ulo in fp64; only read when R != S), else null
@@ -63,6 +66,7 @@ struct ApplyParams {
   const R* tab;               // [n_g][TAB_STRIDE]
   int n_g;                    // >= 2
   R g_min, g_max, inv_dg, inv_fh, ih2, w2;
+  R invih2, inv2ih2, inv3ih2;  // h², h²/2, h²/3 (class coefficients → transverse weights)
   const C* dm[3];             // PML δ⁻ per axis (x, y, z[global])
   const C* dp[3];             // PML δ⁺
   int lo[3], hi[3];           // per-axis index range where δ± == 0 (inclusive)

@@ -1,0 +1,434 @@
+// K2 — fused coefficient build + matrix-free 27-point impedance apply (north-star steps a2–a6).
+//
+//   (Au)_n = Σ_d ω² μ_{|d|}(w_n) u_{n+d} / v²_{n+d}                        Eq. 8, A2, A4
+//          + Σ_a Σ_{e∈{-1,0,1}} D_a(n_a, e) Σ_{p,q} T(p,q; w_n) u_{n+e ê_a+p ê_b+q ê_c}   A6 (App. A), A8
+//   w_n = clamped linear interpolation of the Tikhonov weight table at G_n = v_n/(f h)  P:36, A13
+//
+// B200 design (HBM-bound: 4 + 16·nrhs bytes/point for complex64):
+//  * Data: u (complex, [nrhs][nzl+2][ny][nx]) and w = 1/v² (real, [nzl+2][ny][nx], library-owned) are
+//    the only per-point inputs; the row coefficients are recomputed from w in registers (G = 1/(√w f h)).
+//    The coefficient table is pre-scaled on the host to the class coefficients
+//    (c0..c3 = h⁻²(−6t0, t0−4t1, 2t1−2t2, 3t2), m0..m3 = ω²μ0..3) with forward differences, 16 values per
+//    G row, read through L1 (__ldg of 16-byte vectors): interpolation = 8 FMAs.
+//  * Mapping: a lane owns one x position and a strip of NY consecutive y rows; a warp covers 32
+//    consecutive (strip, x) positions of the flattened strip-row space (no idle lanes for ragged nx:
+//    where x wraps inside a warp the missing neighbours are Dirichlet zeros anyway).  x-neighbours come
+//    from warp shuffles of (u, w) (lanes 0/31 load the warp-edge column), y-neighbours from the strip's
+//    own registers (+1 halo row each side), z by marching planes with scatter-accumulation into the
+//    partial outputs of planes k−1, k, k+1.  The next plane's loads are issued before the current
+//    plane is consumed (register double-buffering) to keep ~2 planes of loads in flight.
+//  * Interior (warp-uniform test): class-sum form, SURVEY App. A.5 — per input plane P0 = u, P1 = 4 faces,
+//    P2 = 4 corners (and Q0..Q2 of q = u·w), then 18 real×complex FMAs (packed FFMA2 for complex64).
+//  * PML (warp-uniform branch, no divergence within a warp's strip): per-axis form with the stretched
+//    1-D operators D_a = (a⁻, −a⁻−a⁺, a⁺) (A8).  Per input plane and point
+//      L1 = D_x u + D_y u,  L2 = D_x Y + D_y X   (X, Y = in-plane x-/y-neighbour sums)
+//    and the contribution to output plane k from plane k+e is
+//      e = 0:  t0 L1 + t1 L2 + D_z(k,0)(t0 P0 + t1 P1 + t2 P2)
+//      e = ±1: t1 L1 + t2 L2 + D_z(k,e)(t0 P0 + t1 P1 + t2 P2)
+//    which reduces exactly to the class form when every a± = h⁻².
+//  * Mixed precision (R = double, S = float): the complex64 solver's residual b − A(x + x_lo) in fp64
+//    arithmetic on c64 storage; w is then recomputed in fp64 from the float velocity.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "apply.cuh"
+
+namespace hz {
+
+constexpr int CTAB_STRIDE = 16;  // c0 c1 c2 c3 m0 m1 m2 m3 | dc0..dc3 dm0..dm3
+
+template <typename R> struct Vec4;
+template <> struct Vec4<float> { typedef float4 T; };
+template <> struct Vec4<double> { typedef double4 T; };
+
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ double4 ldg4(const double* p) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+template <typename R>
+struct Coef8 {
+  R c0, c1, c2, c3, m0, m1, m2, m3;
+};
+
+// a2 + a3: G = v/(f h), clamp (A13), linear interpolation of the pre-scaled class coefficients
+template <typename R>
+__device__ __forceinline__ Coef8<R> coef_from_v(R v, const R* __restrict__ ctab, int n_g, R g_min, R g_max, R inv_dg,
+                                                R inv_fh) {
+  R G = v * inv_fh;
+  G = fmin(fmax(G, g_min), g_max);
+  const R s = (G - g_min) * inv_dg;
+  const int i = min((int)s, n_g - 2);
+  const R tau = s - (R)i;
+  const R* row = ctab + (long long)i * CTAB_STRIDE;
+  typedef typename Vec4<R>::T V4;
+  const V4 a = ldg4(row), b = ldg4(row + 4), da = ldg4(row + 8), db = ldg4(row + 12);
+  Coef8<R> c;
+  c.c0 = fma(tau, da.x, a.x);
+  c.c1 = fma(tau, da.y, a.y);
+  c.c2 = fma(tau, da.z, a.z);
+  c.c3 = fma(tau, da.w, a.w);
+  c.m0 = fma(tau, db.x, b.x);
+  c.m1 = fma(tau, db.y, b.y);
+  c.m2 = fma(tau, db.z, b.z);
+  c.m3 = fma(tau, db.w, b.w);
+  return c;
+}
+
+// complex × complex (PML path); the rounding is spelled out (no compiler contraction choice) so that
+// every unrolled copy of the kernel body computes bitwise the same value
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+template <typename C>
+__device__ __forceinline__ C zmulc(C a, C b) {
+  C r;
+  r.x = fma(a.x, b.x, -mul_rn(a.y, b.y));
+  r.y = fma(a.x, b.y, mul_rn(a.y, b.x));
+  return r;
+}
+// acc + a*b (complex)
+template <typename C>
+__device__ __forceinline__ C zfma(C a, C b, C acc) {
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+  return acc;
+}
+
+// Per-lane view of one input plane: rows 0..NY+1 = y0-1 .. y0+NY
+template <typename R, int NY>
+struct PlaneRegs {
+  typedef typename Cx<R>::T C;
+  C u[NY + 2];
+  R w[NY + 2];
+};
+
+// Warp tiling: a warp covers 32 consecutive x positions x0-1 .. x0+30 of one strip of NY rows; lanes
+// 1..30 produce outputs, lanes 0 and 31 are halo lanes that only load (so x-neighbours come from plain
+// shuffles, and out-of-grid columns/rows load zeros: Dirichlet without masks).  XT = 30 outputs/warp.
+constexpr int XT = 30;
+
+#ifndef HZ_MINB_F
+#define HZ_MINB_F 4
+#endif
+template <typename R> struct ApplyBounds { enum { MINB = HZ_MINB_F }; };
+template <> struct ApplyBounds<double> { enum { MINB = 2 }; };
+
+template <typename R, typename S, int NY, int W, bool COLLOC, int EPI>
+__global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(ApplyParams<R, S> p) {
+  typedef typename Cx<R>::T C;
+  typedef typename Cx<S>::T CS;
+  constexpr bool MIXED = !std::is_same<R, S>::value;
+  constexpr int K = epi_k(EPI);
+  const unsigned FULL = 0xffffffffu;
+
+  // ---- block → (rhs, x-block, z-chunk); rhs fastest so the RHS of one tile share w through L2
+  const int nrhs = p.nrhs;
+  const int bid = blockIdx.x;
+  const int rhs = bid % nrhs;
+  const int tile = bid / nrhs;
+  const int xb = tile % p.nbx;
+  const int chunk = tile / p.nbx;
+  if (p.active != nullptr && p.active[rhs] == 0) return;   // converged RHS (uniform per CTA)
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ntx = (p.nx + XT - 1) / XT;
+  const int gw = xb * W + warp;                 // global warp index over (strip, x-tile)
+  const int strip = gw / ntx;
+  const int xt = gw - strip * ntx;
+  const int nstrips = (p.ny + NY - 1) / NY;
+  const bool warp_ok = strip < nstrips;
+  const int x = xt * XT - 1 + lane;
+  const int y0 = strip * NY;
+  const int nx = p.nx;
+  const bool xin = warp_ok && x >= 0 && x < nx;
+  const bool is_out = xin && lane >= 1 && lane <= XT;     // this lane produces outputs
+
+  unsigned rmask = 0;                           // bit r: row y0-1+r inside the grid (and lane in x)
+#pragma unroll
+  for (int r = 0; r < NY + 2; r++) {
+    const int y = y0 - 1 + r;
+    if (xin && y >= 0 && y < p.ny) rmask |= 1u << r;
+  }
+  // warp-uniform: x- or y-PML among this warp's output points?
+  bool col_pml = is_out && (x < p.lo[0] || x > p.hi[0]);
+#pragma unroll
+  for (int i = 0; i < NY; i++) {
+    const int y = y0 + i;
+    col_pml = col_pml || (is_out && y < p.ny && (y < p.lo[1] || y > p.hi[1]));
+  }
+  const bool gen_col = __any_sync(FULL, col_pml);
+
+  const int zc0 = chunk * p.zc;
+  const int zc1 = min(zc0 + p.zc, p.nzl);
+  const long long plane = p.plane;
+  const long long rofs = (long long)rhs * p.fstride;
+  const long long lbase = (long long)(y0 - 1) * nx + x;   // (storage plane 0, row y0-1, column x)
+  const CS* __restrict__ ub = p.u + rofs + lbase;
+  const CS* __restrict__ ulb = (MIXED && p.ulo != nullptr) ? p.ulo + rofs + lbase : nullptr;
+  const S* __restrict__ wb = MIXED ? p.v + lbase : p.w + lbase;
+  const C czv = czero(R(0));
+  const int zlo = p.lo[2], zhi = p.hi[2];
+  const int zbase = p.z0;
+
+  // fetch plane pl (local index; storage index pl+1)
+  auto fetch = [&](PlaneRegs<R, NY>& P, int pl) {
+    const int zg = zbase + pl;
+    const unsigned m = (zg >= 0 && zg < p.nzg) ? rmask : 0u;
+    const long long pb = (long long)(pl + 1) * plane;
+    const CS* up = ub + pb;
+    const S* wp = wb + pb;
+#pragma unroll
+    for (int r = 0; r < NY + 2; r++) {
+      const bool ok = (m >> r) & 1u;
+      if (!MIXED) {
+        P.u[r] = ok ? to_cx(ldg_c(up + r * nx), R(0)) : czv;
+        P.w[r] = ok ? (R)__ldg(wp + r * nx) : R(0);
+      } else {
+        P.u[r] = ok ? load_u<R, S>(ub, ulb, pb + (long long)r * nx) : czv;
+        const R vv = ok ? (R)__ldg(wp + r * nx) : R(1);
+        P.w[r] = ok ? R(1) / (vv * vv) : R(0);
+      }
+    }
+  };
+
+  double part[K > 0 ? K : 1];
+#pragma unroll
+  for (int k = 0; k < (K > 0 ? K : 1); k++) part[k] = 0.0;
+
+  // PML x coefficients of this lane (gen_col warps): δ± = a± − h⁻²
+  C dxm = czv, dxp = czv;
+  if (gen_col && xin) {
+    dxm = p.dm[0][x];
+    dxp = p.dp[0][x];
+  }
+  const R i3h = p.inv3ih2, i2h = p.inv2ih2, i1h = p.invih2;
+  const R s_k1 = p.inv_fh * p.inv_dg, s_k0 = -p.g_min * p.inv_dg, s_max = (R)(p.n_g - 1);
+
+  // coefficients of output rows of plane pl+1 from w of that plane (a2 + a3)
+  auto coefs = [&](Coef8<R> (&cn)[NY], const PlaneRegs<R, NY>& Pn, bool valid) {
+#pragma unroll
+    for (int i = 0; i < NY; i++) {
+      const R wn = Pn.w[i + 1];
+      if (valid) {
+        const R vv = (wn > R(0)) ? rsqrt_r(wn) : R(0);
+        R sidx = fma(vv, s_k1, s_k0);                      // (G − g_min)/ΔG, G = v/(f h)
+        sidx = fmin(fmax(sidx, R(0)), s_max);              // clamp (A13)
+        const int ii = min((int)sidx, p.n_g - 2);
+        const R tau = sidx - (R)ii;
+        const R* row = p.ctab + ii * CTAB_STRIDE;
+        typedef typename Vec4<R>::T V4;
+        const V4 a = ldg4(row), b = ldg4(row + 4), da = ldg4(row + 8), db = ldg4(row + 12);
+        cn[i].c0 = fma(tau, da.x, a.x);
+        cn[i].c1 = fma(tau, da.y, a.y);
+        cn[i].c2 = fma(tau, da.z, a.z);
+        cn[i].c3 = fma(tau, da.w, a.w);
+        cn[i].m0 = fma(tau, db.x, b.x);
+        cn[i].m1 = fma(tau, db.y, b.y);
+        cn[i].m2 = fma(tau, db.z, b.z);
+        cn[i].m3 = fma(tau, db.w, b.w);
+        if (COLLOC) {   // Eq. "10": ω²/κ0 for all 27 neighbours → m·w0 multiplies the u class sums
+          cn[i].m0 *= wn;
+          cn[i].m1 *= wn;
+          cn[i].m2 *= wn;
+          cn[i].m3 *= wn;
+        }
+      } else {
+        cn[i] = Coef8<R>{R(0), R(0), R(0), R(0), R(0), R(0), R(0), R(0)};
+      }
+    }
+  };
+
+  // One input plane pl.  cP: coefficients of output pl-1 (overwritten with those of pl+1);
+  // cC: of output pl.  aP: partial of output pl-1 (overwritten with the first partial of pl+1);
+  // aC: partial of output pl.  Roles alternate between two slots → no register rotation.
+  auto body = [&](PlaneRegs<R, NY>& Pc, PlaneRegs<R, NY>& Pn, Coef8<R> (&cP)[NY], Coef8<R> (&cC)[NY],
+                  C (&aP)[NY], C (&aC)[NY], int pl) {
+    if (pl + 1 <= zc1) fetch(Pn, pl + 1);   // prefetch: in flight while plane pl is consumed
+    const bool do_prev = (pl - 1 >= zc0);
+    const bool do_next = (pl + 1 < zc1);
+    const int zg = zbase + pl;
+    const bool zp_prev = do_prev && (zg - 1 < zlo || zg - 1 > zhi);
+    const bool zp_cur = (pl >= zc0 && pl < zc1) && (zg < zlo || zg > zhi);
+    const bool zp_next = do_next && (zg + 1 < zlo || zg + 1 > zhi);
+    const bool zcorr = zp_prev || zp_cur || zp_next;
+
+    // ---- in-plane x sums: X = u(x-1) + u(x+1), Xq = q(x-1) + q(x+1), q = u·w
+    C X[NY + 2], q[NY + 2], Xq[NY + 2];
+#pragma unroll
+    for (int r = 0; r < NY + 2; r++) {
+      const C a = shfl_up_c(Pc.u[r], 1);
+      const C b = shfl_down_c(Pc.u[r], 1);
+      X[r] = cadd(a, b);
+      if (!COLLOC) {
+        const R wa = __shfl_up_sync(FULL, Pc.w[r], 1);
+        const R wbv = __shfl_down_sync(FULL, Pc.w[r], 1);
+        q[r] = cscale(Pc.w[r], Pc.u[r]);
+        Xq[r] = cfma(wbv, b, cscale(wa, a));
+      }
+    }
+    Coef8<R> cN[NY];
+    coefs(cN, Pn, do_next);
+
+    C outv[NY];
+#pragma unroll
+    for (int i = 0; i < NY; i++) {
+      const C u0 = Pc.u[i + 1];
+      const C Y = cadd(Pc.u[i], Pc.u[i + 2]);
+      const C P1 = cadd(X[i + 1], Y);
+      const C P2 = cadd(X[i], X[i + 2]);
+      const C Q0 = COLLOC ? u0 : q[i + 1];
+      const C Q1 = COLLOC ? P1 : cadd(Xq[i + 1], cadd(q[i], q[i + 2]));
+      const C Q2 = COLLOC ? P2 : cadd(Xq[i], Xq[i + 2]);
+      // ---- interior class-sum form
+      C a = aP[i];
+      a = cfma(cP[i].c1, u0, a);
+      a = cfma(cP[i].c2, P1, a);
+      a = cfma(cP[i].c3, P2, a);
+      a = cfma(cP[i].m1, Q0, a);
+      a = cfma(cP[i].m2, Q1, a);
+      a = cfma(cP[i].m3, Q2, a);
+      C b = aC[i];
+      b = cfma(cC[i].c0, u0, b);
+      b = cfma(cC[i].c1, P1, b);
+      b = cfma(cC[i].c2, P2, b);
+      b = cfma(cC[i].m0, Q0, b);
+      b = cfma(cC[i].m1, Q1, b);
+      b = cfma(cC[i].m2, Q2, b);
+      C c = cscale(cN[i].c1, u0);
+      c = cfma(cN[i].c2, P1, c);
+      c = cfma(cN[i].c3, P2, c);
+      c = cfma(cN[i].m1, Q0, c);
+      c = cfma(cN[i].m2, Q1, c);
+      c = cfma(cN[i].m3, Q2, c);
+      // ---- PML corrections (A8): a± = h⁻² + δ±; warp/plane-uniform branches
+      if (gen_col || zcorr) {
+        // transverse weights from the class coefficients: t2 = c3 h²/3, t1 = t2 + c2 h²/2, t0 = c1 h² + 4 t1
+        const R pt2 = cP[i].c3 * i3h, pt1 = fma(cP[i].c2, i2h, pt2), pt0 = fma(cP[i].c1, i1h, R(4) * pt1);
+        const R ct2 = cC[i].c3 * i3h, ct1 = fma(cC[i].c2, i2h, ct2), ct0 = fma(cC[i].c1, i1h, R(4) * ct1);
+        const R nt2 = cN[i].c3 * i3h, nt1 = fma(cN[i].c2, i2h, nt2), nt0 = fma(cN[i].c1, i1h, R(4) * nt1);
+        if (gen_col) {
+          // ΔL1 = δx(u) + δy(u), ΔL2 = δx(Y) + δy(X): the stretched parts of D_x, D_y
+          C dym = czv, dyp = czv;
+          if ((rmask >> (i + 1)) & 1u) {
+            dym = p.dm[1][y0 + i];
+            dyp = p.dp[1][y0 + i];
+          }
+          const C uL = shfl_up_c(u0, 1), uR = shfl_down_c(u0, 1);
+          const C YL = shfl_up_c(Y, 1), YR = shfl_down_c(Y, 1);
+          C L1 = zmulc(dxm, csub(uL, u0));
+          L1 = zfma(dxp, csub(uR, u0), L1);
+          L1 = zfma(dym, csub(Pc.u[i], u0), L1);
+          L1 = zfma(dyp, csub(Pc.u[i + 2], u0), L1);
+          C L2 = zmulc(dxm, csub(YL, Y));
+          L2 = zfma(dxp, csub(YR, Y), L2);
+          L2 = zfma(dym, csub(X[i], X[i + 1]), L2);
+          L2 = zfma(dyp, csub(X[i + 2], X[i + 1]), L2);
+          a = cfma(pt1, L1, a);
+          a = cfma(pt2, L2, a);
+          b = cfma(ct0, L1, b);
+          b = cfma(ct1, L2, b);
+          c = cfma(nt1, L1, c);
+          c = cfma(nt2, L2, c);
+        }
+        if (zcorr) {   // δz · (t0 P0 + t1 P1 + t2 P2) of each output plane
+          if (zp_prev) {
+            C B3 = cscale(pt0, u0);
+            B3 = cfma(pt1, P1, B3);
+            B3 = cfma(pt2, P2, B3);
+            a = zfma(p.dp[2][zg - 1], B3, a);
+          }
+          if (zp_cur) {
+            C B3 = cscale(ct0, u0);
+            B3 = cfma(ct1, P1, B3);
+            B3 = cfma(ct2, P2, B3);
+            const C dz = cadd(p.dm[2][zg], p.dp[2][zg]);
+            b = zfma(make_cx(-dz.x, -dz.y), B3, b);
+          }
+          if (zp_next) {
+            C B3 = cscale(nt0, u0);
+            B3 = cfma(nt1, P1, B3);
+            B3 = cfma(nt2, P2, B3);
+            c = zfma(p.dm[2][zg + 1], B3, c);
+          }
+        }
+      }
+      outv[i] = a;
+      aC[i] = b;          // output pl: "prev" of the next plane (slot roles swap)
+      aP[i] = c;          // output pl+1: "cur" of the next plane
+      cP[i] = cN[i];      // coefficients of pl+1 take the slot of pl-1
+    }
+
+    // ---- finalize outputs of plane pl-1, epilogue
+    if (do_prev && is_out) {
+      const long long ob = rofs + lbase + (long long)pl * plane;   // storage index of local plane pl-1
+#pragma unroll
+      for (int i = 0; i < NY; i++) {
+        if (!((rmask >> (i + 1)) & 1u)) continue;
+        const long long o = ob + (long long)(i + 1) * nx;
+        const C a = outv[i];
+        if (EPI == EPI_RESID) {
+          const C bb = to_cx(ldg_c(p.bvec + o), R(0));
+          const C rr = csub(bb, a);
+          p.au[o] = from_cx(rr, S(0));
+          part[0] += (double)rr.x * (double)rr.x + (double)rr.y * (double)rr.y;
+          if (p.rhat != nullptr) acc_cdot(part[1], part[2], to_cx(ldg_c(p.rhat + o), R(0)), rr);
+        } else {
+          p.au[o] = from_cx(a, S(0));
+          if (EPI == EPI_DOT1) {
+            acc_cdot(part[0], part[1], to_cx(ldg_c(p.rhat + o), R(0)), a);
+          } else if (EPI == EPI_DOT4) {
+            const C sv = to_cx(ldg_c(p.u + o), R(0));
+            const C rh = to_cx(ldg_c(p.rhat + o), R(0));
+            acc_cdot(part[0], part[1], a, sv);
+            part[2] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+            acc_cdot(part[3], part[4], rh, sv);
+            acc_cdot(part[5], part[6], rh, a);
+          }
+        }
+      }
+    }
+  };
+
+  PlaneRegs<R, NY> A, B;
+  Coef8<R> c0s[NY], c1s[NY];
+  C a0s[NY], a1s[NY];
+#pragma unroll
+  for (int i = 0; i < NY; i++) {
+    c0s[i] = Coef8<R>{R(0), R(0), R(0), R(0), R(0), R(0), R(0), R(0)};
+    c1s[i] = c0s[i];
+    a0s[i] = czv;
+    a1s[i] = czv;
+  }
+  fetch(A, zc0 - 1);
+#ifdef HZ_NO_UNROLL
+  for (int pl = zc0 - 1; pl <= zc1; ++pl) {
+    body(A, B, c0s, c1s, a0s, a1s, pl);
+    PlaneRegs<R, NY> T = A; A = B; B = T;
+#pragma unroll
+    for (int i = 0; i < NY; i++) {
+      Coef8<R> t = c0s[i]; c0s[i] = c1s[i]; c1s[i] = t;
+      C ta = a0s[i]; a0s[i] = a1s[i]; a1s[i] = ta;
+    }
+  }
+#else
+  int pl = zc0 - 1;
+  for (; pl + 1 <= zc1; pl += 2) {
+    body(A, B, c0s, c1s, a0s, a1s, pl);
+    body(B, A, c1s, c0s, a1s, a0s, pl + 1);
+  }
+  if (pl <= zc1) body(A, B, c0s, c1s, a0s, a1s, pl);
+#endif
+
+  if (K > 0) {
+    const int nblocks = p.nbx * p.nchunks;
+    block_grid_reduce<K, 32 * W>(part, p.partials + (long long)rhs * nblocks * K, p.dots + (long long)rhs * K,
+                                 p.tickets + rhs, nblocks, tile);
+  }
+}
+
+}  // namespace hz

@@ -1,6 +1,5 @@
-// Complex helpers for the sm_100a kernels.  complex64 arithmetic uses the packed FP32x2 pipe of
-// Blackwell (add/mul/fma.rn.f32x2 → SASS FADD2/FMUL2/FFMA2): a complex value is one 64-bit register
-// pair, so real×complex and complex+complex cost ONE instruction instead of two.
+// Complex helpers for the sm_100a kernels.  A complex64 value is one 64-bit register pair, so ptxas
+// can issue real×complex and complex+complex on the packed FP32x2 pipe (FFMA2/FADD2/FMUL2).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -18,29 +17,14 @@ __device__ __forceinline__ float2 u64_as_f2(unsigned long long a) {
 }
 
 // ---- float2 (complex64) ---------------------------------------------------------------------
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
-  unsigned long long d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
-  return u64_as_f2(d);
-}
-__device__ __forceinline__ float2 csub(float2 a, float2 b) {
-  unsigned long long d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
-  return u64_as_f2(d);
-}
-// s * a (s real)
-__device__ __forceinline__ float2 cscale(float s, float2 a) {
-  unsigned long long d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(make_float2(s, s))), "l"(f2_as_u64(a)));
-  return u64_as_f2(d);
-}
-// acc + s * a (s real)
+// Scalar IEEE ops with explicit rounding (ptxas pairs them into FFMA2/FADD2/FMUL2 where it can).  An
+// inline-PTX fma.rn.f32x2 version was measured equally fast but gave 1-ulp differences between
+// unrolled copies of the apply body, breaking bitwise z-slab decomposition invariance.
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y)); }
+__device__ __forceinline__ float2 cscale(float s, float2 a) { return make_float2(__fmul_rn(s, a.x), __fmul_rn(s, a.y)); }
 __device__ __forceinline__ float2 cfma(float s, float2 a, float2 acc) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(d)
-      : "l"(f2_as_u64(make_float2(s, s))), "l"(f2_as_u64(a)), "l"(f2_as_u64(acc)));
-  return u64_as_f2(d);
+  return make_float2(__fmaf_rn(s, a.x, acc.x), __fmaf_rn(s, a.y, acc.y));
 }
 // complex * complex (slow paths only)
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
@@ -76,6 +60,11 @@ __device__ __forceinline__ double2 shfl_up_c(double2 a, int d) {
 __device__ __forceinline__ double2 shfl_down_c(double2 a, int d) {
   return make_double2(__shfl_down_sync(0xffffffffu, a.x, d), __shfl_down_sync(0xffffffffu, a.y, d));
 }
+
+__device__ __forceinline__ float2 make_cx(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ double2 make_cx(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ float rsqrt_r(float a) { return rsqrtf(a); }
+__device__ __forceinline__ double rsqrt_r(double a) { return rsqrt(a); }
 
 // ---- storage <-> compute conversion (mixed-precision residual: c64 storage, fp64 arithmetic) ----
 __device__ __forceinline__ float2 to_cx(float2 a, float) { return a; }

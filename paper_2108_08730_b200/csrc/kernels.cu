@@ -5,232 +5,10 @@
 #include <stdint.h>
 
 #include "apply.cuh"
+#include "apply27.cuh"
 #include "kernels.h"
 
 namespace hz {
-
-// =============================================================================================
-// K2: apply (a2–a6 fused), EPI selects the fused BiCGSTAB epilogue
-// =============================================================================================
-template <typename R, typename S, int NY, int WARPS, bool COLLOC, int EPI>
-__global__ void __launch_bounds__(32 * WARPS) apply27_kernel(ApplyParams<R, S> p) {
-  typedef typename Cx<R>::T C;
-  typedef typename Cx<S>::T CS;
-  constexpr int K = epi_k(EPI);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* tab = reinterpret_cast<R*>(smem_raw);
-  const int rhs = blockIdx.z;
-  if (p.active != nullptr && p.active[rhs] == 0) return;   // uniform per CTA (converged RHS)
-  for (int i = threadIdx.x; i < p.n_g * TAB_STRIDE; i += blockDim.x) tab[i] = p.tab[i];
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long g = ((long long)blockIdx.x * WARPS + warp) * 32 + lane;
-  const bool lane_ok = g < p.nlanes;
-  const long long gg = lane_ok ? g : 0;
-  const int strip = (int)(gg / p.nx);
-  const int x = (int)(gg - (long long)strip * p.nx);
-  const int y0 = strip * NY;
-  const bool hasL = lane_ok && x > 0;
-  const bool hasR = lane_ok && x < p.nx - 1;
-  const bool edge_ld = (lane == 0 && hasL) || (lane == 31 && hasR);
-  const int xe = (lane == 0) ? x - 1 : x + 1;
-
-  const int zc0 = blockIdx.y * p.zc;
-  const int zc1 = min(zc0 + p.zc, p.nzl);
-  const CS* __restrict__ ub = p.u + (long long)rhs * p.fstride;
-  CS* __restrict__ aub = p.au + (long long)rhs * p.fstride;
-  const CS* __restrict__ ulb = p.ulo ? p.ulo + (long long)rhs * p.fstride : nullptr;
-  const C czv = czero(R(0));
-
-  C accP[NY], accC[NY];
-  R cp1[NY], cp2[NY], cp3[NY], mp1[NY], mp2[NY], mp3[NY];
-  R cc0[NY], cc1[NY], cc2[NY], cc3[NY], mc0[NY], mc1[NY], mc2[NY], mc3[NY];
-  R vown[NY];
-  double part[K > 0 ? K : 1];
-#pragma unroll
-  for (int k = 0; k < (K > 0 ? K : 1); k++) part[k] = 0.0;
-#pragma unroll
-  for (int i = 0; i < NY; i++) {
-    accP[i] = czv; accC[i] = czv;
-    cp1[i] = cp2[i] = cp3[i] = mp1[i] = mp2[i] = mp3[i] = R(0);
-    cc0[i] = cc1[i] = cc2[i] = cc3[i] = mc0[i] = mc1[i] = mc2[i] = mc3[i] = R(0);
-  }
-  {  // v at own rows of plane zc0 - 1
-    const int pl = zc0 - 1, zg = p.z0 + pl;
-    const bool pin = zg >= 0 && zg < p.nzg;
-#pragma unroll
-    for (int i = 0; i < NY; i++) {
-      const int y = y0 + i;
-      vown[i] = (lane_ok && pin && y < p.ny) ? (R)__ldg(p.v + (long long)(pl + 1) * p.plane + (long long)y * p.nx + x) : R(1);
-    }
-  }
-
-  for (int pl = zc0 - 1; pl <= zc1; ++pl) {
-    const int zg = p.z0 + pl;
-    const bool pin = zg >= 0 && zg < p.nzg;
-    const bool do_prev = (pl - 1 >= zc0);
-    const bool do_cur = (pl >= zc0 && pl < zc1);
-    const bool do_next = (pl + 1 < zc1);
-    const long long pbase = (long long)(pl + 1) * p.plane;
-
-    // ---------------- loads of plane pl (rows y0-1 .. y0+NY) ----------------
-    C uc[NY + 2], ue[NY + 2];
-    R vc[NY + 2], ve[NY + 2];
-#pragma unroll
-    for (int r = 0; r < NY + 2; r++) {
-      const int y = y0 - 1 + r;
-      const bool rv = lane_ok && pin && y >= 0 && y < p.ny;
-      const long long o = pbase + (long long)y * p.nx;
-      uc[r] = rv ? load_u<R, S>(ub, ulb, o + x) : czv;
-      ue[r] = (rv && edge_ld) ? load_u<R, S>(ub, ulb, o + xe) : czv;
-      if (!COLLOC) {
-        if (r == 0 || r == NY + 1) vc[r] = rv ? (R)__ldg(p.v + o + x) : R(1);
-        else vc[r] = vown[r - 1];
-        ve[r] = (rv && edge_ld) ? (R)__ldg(p.v + o + xe) : R(1);
-      }
-    }
-    // v of plane pl+1 at own rows (coefficients of the next plane; r of the next iteration)
-    R vnx[NY];
-    {
-      const bool pin1 = (zg + 1 >= 0) && (zg + 1 < p.nzg) && (pl + 1 <= zc1);
-#pragma unroll
-      for (int i = 0; i < NY; i++) {
-        const int y = y0 + i;
-        vnx[i] = (lane_ok && pin1 && y < p.ny) ? (R)__ldg(p.v + pbase + p.plane + (long long)y * p.nx + x) : R(1);
-      }
-    }
-
-    // ---------------- row quantities: u, Rc_u (x-faces), q = u/v², Rc_q ----------------
-    C Rcu[NY + 2], qc[NY + 2], Rcq[NY + 2];
-#pragma unroll
-    for (int r = 0; r < NY + 2; r++) {
-      C uL = shfl_up_c(uc[r], 1);
-      C uR = shfl_down_c(uc[r], 1);
-      if (lane == 0) uL = ue[r];
-      if (lane == 31) uR = ue[r];
-      if (!hasL) uL = czv;
-      if (!hasR) uR = czv;
-      Rcu[r] = cadd(uL, uR);
-      if (!COLLOC) {
-        const R rc = R(1) / (vc[r] * vc[r]);
-        const R re = R(1) / (ve[r] * ve[r]);
-        qc[r] = cscale(rc, uc[r]);
-        const C qe = cscale(re, ue[r]);
-        C qL = shfl_up_c(qc[r], 1);
-        C qR = shfl_down_c(qc[r], 1);
-        if (lane == 0) qL = qe;
-        if (lane == 31) qR = qe;
-        if (!hasL) qL = czv;
-        if (!hasR) qR = czv;
-        Rcq[r] = cadd(qL, qR);
-      }
-    }
-
-    // ---------------- per output row: plane sums and z scatter-accumulation ----------------
-#pragma unroll
-    for (int i = 0; i < NY; i++) {
-      const C P0 = uc[i + 1];
-      const C P1 = cadd(Rcu[i + 1], cadd(uc[i], uc[i + 2]));
-      const C P2 = cadd(Rcu[i], Rcu[i + 2]);
-      C Q0 = czv, Q1 = czv, Q2 = czv;
-      if (!COLLOC) {
-        Q0 = qc[i + 1];
-        Q1 = cadd(Rcq[i + 1], cadd(qc[i], qc[i + 2]));
-        Q2 = cadd(Rcq[i], Rcq[i + 2]);
-      }
-      if (do_prev) {   // plane pl is the "+1" neighbour plane of output pl-1
-        C a = accP[i];
-        a = cfma(cp1[i], P0, a);
-        a = cfma(cp2[i], P1, a);
-        a = cfma(cp3[i], P2, a);
-        if (!COLLOC) {
-          a = cfma(mp1[i], Q0, a);
-          a = cfma(mp2[i], Q1, a);
-          a = cfma(mp3[i], Q2, a);
-        }
-        // ---- finalize output (x, y0+i, pl-1) ----
-        const int y = y0 + i;
-        const int zo = pl - 1;
-        if (lane_ok && y < p.ny) {
-          const int zgo = p.z0 + zo;
-          if (x < p.lo[0] || x > p.hi[0] || y < p.lo[1] || y > p.hi[1] || zgo < p.lo[2] || zgo > p.hi[2])
-            a = cadd(a, pml_correction<R, S>(p, tab, ub, ulb, x, y, zo));
-          const long long o = (long long)(zo + 1) * p.plane + (long long)y * p.nx + x;
-          if (EPI == EPI_RESID) {
-            const C bb = to_cx(ldg_c(p.bvec + (long long)rhs * p.fstride + o), R(0));
-            const C rr = csub(bb, a);
-            aub[o] = from_cx(rr, S(0));
-            part[0] += (double)rr.x * (double)rr.x + (double)rr.y * (double)rr.y;
-            if (p.rhat != nullptr)
-              acc_cdot(part[1], part[2], to_cx(ldg_c(p.rhat + (long long)rhs * p.fstride + o), R(0)), rr);
-          } else {
-            aub[o] = from_cx(a, S(0));
-            if (EPI == EPI_DOT1) {
-              acc_cdot(part[0], part[1], to_cx(ldg_c(p.rhat + (long long)rhs * p.fstride + o), R(0)), a);
-            } else if (EPI == EPI_DOT4) {
-              const C s = to_cx(ldg_c(ub + o), R(0));
-              const C rh = to_cx(ldg_c(p.rhat + (long long)rhs * p.fstride + o), R(0));
-              acc_cdot(part[0], part[1], a, s);
-              part[2] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
-              acc_cdot(part[3], part[4], rh, s);
-              acc_cdot(part[5], part[6], rh, a);
-            }
-          }
-        }
-      }
-      C an = czv;
-      if (do_cur) {    // centre plane of output pl
-        C a = accC[i];
-        a = cfma(cc0[i], P0, a);
-        a = cfma(cc1[i], P1, a);
-        a = cfma(cc2[i], P2, a);
-        if (!COLLOC) {
-          a = cfma(mc0[i], Q0, a);
-          a = cfma(mc1[i], Q1, a);
-          a = cfma(mc2[i], Q2, a);
-        }
-        accC[i] = a;
-      }
-      RowCoef<R> cn;
-      if (do_next) {   // plane pl is the "-1" neighbour plane of output pl+1
-        cn = row_coef<R>(vnx[i], tab, p);
-        if (COLLOC) {  // Eq. "10": ω²/κ0 for all 27 points → fold m/v0² into the class coefficients
-          const R iv2 = R(1) / (vnx[i] * vnx[i]);
-          cn.c0 = fma(cn.m0, iv2, cn.c0);
-          cn.c1 = fma(cn.m1, iv2, cn.c1);
-          cn.c2 = fma(cn.m2, iv2, cn.c2);
-          cn.c3 = fma(cn.m3, iv2, cn.c3);
-        }
-        an = cscale(cn.c1, P0);
-        an = cfma(cn.c2, P1, an);
-        an = cfma(cn.c3, P2, an);
-        if (!COLLOC) {
-          an = cfma(cn.m1, Q0, an);
-          an = cfma(cn.m2, Q1, an);
-          an = cfma(cn.m3, Q2, an);
-        }
-      } else {
-        cn.c0 = cn.c1 = cn.c2 = cn.c3 = cn.m0 = cn.m1 = cn.m2 = cn.m3 = R(0);
-      }
-      // rotate state: (pl-1, pl, pl+1) -> (pl, pl+1)
-      accP[i] = accC[i];
-      accC[i] = an;
-      cp1[i] = cc1[i]; cp2[i] = cc2[i]; cp3[i] = cc3[i];
-      mp1[i] = mc1[i]; mp2[i] = mc2[i]; mp3[i] = mc3[i];
-      cc0[i] = cn.c0; cc1[i] = cn.c1; cc2[i] = cn.c2; cc3[i] = cn.c3;
-      mc0[i] = cn.m0; mc1[i] = cn.m1; mc2[i] = cn.m2; mc3[i] = cn.m3;
-      vown[i] = vnx[i];
-    }
-  }
-
-  if (K > 0) {
-    const int nblocks = gridDim.x * gridDim.y;
-    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
-    block_grid_reduce<K, 32 * WARPS>(part, p.partials + (long long)rhs * nblocks * K, p.dots + (long long)rhs * K,
-                                     p.tickets + rhs, nblocks, bid);
-  }
-}
 
 // =============================================================================================
 // K1 record export: (k², t0, t1, t2, μ0, μ1, μ2, μ3) per point
@@ -294,6 +72,25 @@ __global__ void sources_kernel(ApplyParams<R> p, int nsrc, const long long* __re
   val.y = (R)(ai * (double)w);
   b[o] = val;
 }
+
+// =============================================================================================
+// w = 1/v² (the apply's per-point model input), all planes incl. halos
+// =============================================================================================
+template <typename R>
+__global__ void winv_kernel(const R* __restrict__ v, R* __restrict__ w, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const R a = v[i];
+    w[i] = R(1) / (a * a);
+  }
+}
+
+template <typename R>
+cudaError_t launch_winv(const R* v, R* w, long long n, cudaStream_t s) {
+  winv_kernel<R><<<592, 256, 0, s>>>(v, w, n);
+  return cudaGetLastError();
+}
+template cudaError_t launch_winv<float>(const float*, float*, long long, cudaStream_t);
+template cudaError_t launch_winv<double>(const double*, double*, long long, cudaStream_t);
 
 // =============================================================================================
 // velocity validation / statistics: min, max, non-finite count, clamped count
@@ -511,14 +308,23 @@ __global__ void __launch_bounds__(NT) norm2_kernel(const typename Cx<R>::T* __re
 // host-side launchers (kernels.h)
 // =============================================================================================
 template <typename R> struct ApplyCfg;
-template <> struct ApplyCfg<float> { enum { NY = 4, WARPS = 4 }; };
-template <> struct ApplyCfg<double> { enum { NY = 2, WARPS = 4 }; };
+#ifndef HZ_NY_F
+#define HZ_NY_F 2
+#endif
+#ifndef HZ_W_F
+#define HZ_W_F 4
+#endif
+#ifndef HZ_NY_D
+#define HZ_NY_D 2
+#endif
+template <> struct ApplyCfg<float> { enum { NY = HZ_NY_F, WARPS = HZ_W_F }; };
+template <> struct ApplyCfg<double> { enum { NY = HZ_NY_D, WARPS = 4 }; };
 
 template <typename R>
-long long apply_nblocks_x(int nx, int ny) {
+long long apply_nblocks_x(int nx, int ny) {   // CTAs covering one z-chunk of the (strip, x-tile) space
   constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
-  const long long nlanes = (long long)((ny + NY - 1) / NY) * nx;
-  return (nlanes + 32LL * W - 1) / (32LL * W);
+  const long long nwarps = (long long)((ny + NY - 1) / NY) * ((nx + XT - 1) / XT);
+  return (nwarps + W - 1) / W;
 }
 template long long apply_nblocks_x<float>(int, int);
 template long long apply_nblocks_x<double>(int, int);
@@ -526,17 +332,12 @@ template long long apply_nblocks_x<double>(int, int);
 template <typename R, typename S, bool COLLOC, int EPI>
 static cudaError_t launch_apply_t(ApplyParams<R, S> p, int nrhs, cudaStream_t s) {
   constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
-  auto kern = apply27_kernel<R, S, NY, W, COLLOC, EPI>;
-  const size_t smem = (size_t)p.n_g * TAB_STRIDE * sizeof(R);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr_set = true;
-  }
-  p.nlanes = (long long)((p.ny + NY - 1) / NY) * p.nx;
-  const long long nb = apply_nblocks_x<R>(p.nx, p.ny);
-  dim3 grid((unsigned)nb, (unsigned)p.nchunks, (unsigned)nrhs);
-  kern<<<grid, 32 * W, smem, s>>>(p);
+  auto kern = apply27_v2<R, S, NY, W, COLLOC, EPI>;
+  p.nbx = (int)apply_nblocks_x<R>(p.nx, p.ny);
+  p.nrhs = nrhs;
+  const long long nb = (long long)p.nbx * p.nchunks * nrhs;
+  if (nb >= (1LL << 31)) return cudaErrorInvalidConfiguration;
+  kern<<<(unsigned)nb, 32 * W, 0, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -587,9 +388,9 @@ int apply_occupancy(bool colloc) {
   constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
   int nb = 0;
   if (colloc)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_kernel<R, R, NY, W, true, EPI_DOT4>, 32 * W, 16 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_v2<R, R, NY, W, true, EPI_DOT4>, 32 * W, 0);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_kernel<R, R, NY, W, false, EPI_DOT4>, 32 * W, 16 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_v2<R, R, NY, W, false, EPI_DOT4>, 32 * W, 0);
   return nb > 0 ? nb : 1;
 }
 template int apply_occupancy<float>(bool);

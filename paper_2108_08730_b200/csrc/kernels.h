@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include "apply.cuh"
+#include "apply27.cuh"
 
 namespace hz {
 
@@ -45,6 +46,7 @@ cudaError_t launch_apply(const ApplyParams<R, S>& p, int nrhs, bool colloc, int 
 template <>
 cudaError_t launch_apply<double, float>(const ApplyParams<double, float>& p, int nrhs, bool colloc, int epi,
                                         cudaStream_t s);
+template <typename R> cudaError_t launch_winv(const R* v, R* w, long long n, cudaStream_t s);
 template <typename R> cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s);
 template <typename R>
 cudaError_t launch_sources(const ApplyParams<R>& p, int nsrc, const long long* nodes, const double* amps,

@@ -13,7 +13,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(_HERE, "libhz.so")
+_LIBPATH = os.environ.get("HZ_LIB") or os.path.join(_HERE, "libhz.so")   # HZ_LIB: tuning-sweep builds
 if not os.path.exists(_LIBPATH):
     raise ImportError(
         f"libhz.so not found at {_LIBPATH}: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -1,8 +1,18 @@
-"""GPU batched BiCGSTAB (through the C ABI) against the oracle's solves and the analytic field."""
+"""GPU batched BiCGSTAB (through the C ABI) against the oracle's solves and the analytic field.
+
+North-star bar: solved wavefields within 1e-4 (relative L2) of the oracle's at a fixed residual
+tolerance of 1e-6.  Config 1 is solved by the oracle live; configs 2-3 compare against oracle
+wavefields stored by tools/make_golden_solutions.py (oracle complex128 BiCGSTAB to 1e-10, sampled at
+20000 seeded nodes), and every GPU wavefield is also checked by its residual with the ORACLE's
+explicit matrix.
+"""
+import os
+
 import numpy as np
 import pytest
 
 import synth
+from conftest import GOLDEN
 from oracle import analytic, metrics, operator as op, solvers
 
 torch = pytest.importorskip("torch")
@@ -45,20 +55,34 @@ def gpu_solve(hz, C, nodes, rtol=1e-6):
     return st, rel, its, x[:, 1:-1].cpu().numpy().astype(np.complex128)
 
 
+def golden(ci):
+    path = os.path.join(GOLDEN, f"solve_cfg{ci}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} missing (run tools/make_golden_solutions.py)")
+    return np.load(path)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 def test_config1_solve_vs_oracle_and_analytic(hz, ctx, table, ga_table, dtype):
     cfg = synth.get_config(1)
     v, C = setup(hz, ctx, table, cfg, dtype)
     nodes = synth.source_nodes(cfg)
-    st, rel, its, x = gpu_solve(hz, C, nodes)
-    assert st == hz.HZ_OK and rel[0] <= 1e-6, (st, rel)
+    st, relres, its, x = gpu_solve(hz, C, nodes)
+    assert st == hz.HZ_OK and relres[0] <= 1e-6, (st, relres)
     P = op.Problem(v, cfg.h, cfg.freq, cfg.npml, ga_table)
     A = op.assemble(P)
     b = op.point_sources(P, nodes)[0].ravel()
     xo, rr, _ = solvers.bicgstab(A, b, rtol=1e-10)
-    assert np.linalg.norm(x[0].ravel() - xo) / np.linalg.norm(xo) <= 1e-4       # north star: 1e-4
-    assert np.linalg.norm(b - A @ x[0].ravel()) / np.linalg.norm(b) <= 2e-6
-    # end to end against the analytic Green's function (check 1)
+    assert rel(x[0].ravel(), xo) <= 1e-4                      # north star: 1e-4
+    assert np.linalg.norm(b - A @ x[0].ravel()) / np.linalg.norm(b) <= 1.5e-6
+    # against the stored oracle wavefield as well (same model: v = 3000 is exact in float32)
+    G = golden(1)
+    assert rel(x[0].ravel()[G["idx"]], G["values"][0]) <= 1e-4
+    # end to end against the analytic Green's function (north-star check 1)
     src = nodes[0]
     D = metrics.distance(v.shape, src, cfg.h)
     m = metrics.interior_mask(v.shape, cfg.npml, src)
@@ -68,36 +92,41 @@ def test_config1_solve_vs_oracle_and_analytic(hz, ctx, table, ga_table, dtype):
 
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 def test_config2_batched_solve(hz, ctx, table, ga_table, dtype):
-    """4 RHS solved together; RHS 0 against the oracle's own solve at 1e-10, all RHS by the
-    oracle matrix residual of the GPU solution."""
+    """4 RHS solved together: every wavefield against the stored oracle wavefield (1e-4) and by its
+    residual with the oracle matrix."""
     cfg = synth.get_config(2)
     v, C = setup(hz, ctx, table, cfg, dtype)
     nodes = synth.source_nodes(cfg)
-    st, rel, its, x = gpu_solve(hz, C, nodes)
-    assert st == hz.HZ_OK and np.all(rel <= 1e-6), (st, rel, its)
+    st, relres, its, x = gpu_solve(hz, C, nodes)
+    assert st == hz.HZ_OK and np.all(relres <= 1e-6), (st, relres, its)
+    G = golden(2)
+    for k, r in enumerate(G["rhs"]):
+        assert rel(x[r].ravel()[G["idx"]], G["values"][k]) <= 1e-4, r
     P = op.Problem(v, cfg.h, cfg.freq, cfg.npml, ga_table)
     A = op.assemble(P)
     B = op.point_sources(P, nodes)
     for r in range(len(nodes)):
         br = B[r].ravel()
-        assert np.linalg.norm(br - A @ x[r].ravel()) / np.linalg.norm(br) <= 2e-6
-    xo, rr, _ = solvers.bicgstab(A, B[0].ravel(), rtol=1e-10)
-    assert np.linalg.norm(x[0].ravel() - xo) / np.linalg.norm(xo) <= 1e-4
+        assert np.linalg.norm(br - A @ x[r].ravel()) / np.linalg.norm(br) <= 1.5e-6
 
 
-def test_config3_residual_property(hz, ctx, table, ga_table):
-    """Config 3 (16 RHS, c64): each GPU wavefield solves the oracle's matrix to the tolerance."""
+def test_config3_batched_solve(hz, ctx, table, ga_table):
+    """Config 3 (16 RHS, c64, sharp contrasts): stored oracle wavefields for RHS 0 and 15, and the
+    oracle-matrix residual of 4 RHS."""
     cfg = synth.get_config(3)
     v, C = setup(hz, ctx, table, cfg, "c64")
     nodes = synth.source_nodes(cfg)
-    st, rel, its, x = gpu_solve(hz, C, nodes)
-    assert st == hz.HZ_OK and np.all(rel <= 1e-6), (st, rel, its)
+    st, relres, its, x = gpu_solve(hz, C, nodes)
+    assert st == hz.HZ_OK and np.all(relres <= 1e-6), (st, relres, its)
+    G = golden(3)
+    for k, r in enumerate(G["rhs"]):
+        assert rel(x[r].ravel()[G["idx"]], G["values"][k]) <= 1e-4, r
     P = op.Problem(v, cfg.h, cfg.freq, cfg.npml, ga_table)
     A = op.assemble(P)
     B = op.point_sources(P, nodes[:4])
     for r in range(4):
         br = B[r].ravel()
-        assert np.linalg.norm(br - A @ x[r].ravel()) / np.linalg.norm(br) <= 3e-6
+        assert np.linalg.norm(br - A @ x[r].ravel()) / np.linalg.norm(br) <= 1.5e-6
 
 
 def test_solver_edge_cases(hz, ctx, table):
@@ -108,10 +137,18 @@ def test_solver_edge_cases(hz, ctx, table):
     b[1].zero_()                                    # b = 0 → x = 0, converged at iteration 0
     x = C.alloc_field(3)
     x[2].normal_()                                  # non-zero initial guess
-    st, rel, its, stats = hz.hz_solve(C, b, x, rtol=1e-6)
+    st, relres, its, stats = hz.hz_solve(C, b, x, rtol=1e-6)
     assert st == hz.HZ_OK and its[1] == 0 and float(x[1].abs().max()) == 0.0
-    assert np.all(rel <= 1e-6)
+    assert np.all(relres <= 1e-6)
     x2 = C.alloc_field(3)
-    st, rel, its, stats = hz.hz_solve(C, b, x2, rtol=1e-12, max_iter=7)
+    st, relres, its, stats = hz.hz_solve(C, b, x2, rtol=1e-12, max_iter=7)
     assert st == hz.HZ_NOT_CONVERGED and its[0] == 7
     assert stats["apply_launches"] > 0 and stats["kernel_launches"] >= stats["apply_launches"]
+    # host (numpy) buffers through the same ABI: staged by the library, same answer
+    bh = b.cpu().numpy()
+    xh = np.zeros_like(bh)
+    st2, rel2, its2, _ = hz.hz_solve(C, bh, xh, rtol=1e-6)
+    x3 = C.alloc_field(3)
+    st3, rel3, its3, _ = hz.hz_solve(C, b, x3, rtol=1e-6)
+    assert st2 == hz.HZ_OK and np.array_equal(its2, its3)
+    assert np.array_equal(xh, x3.cpu().numpy())
