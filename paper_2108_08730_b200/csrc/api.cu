@@ -150,6 +150,7 @@ struct hz_coeffs {
   DBuf ctab_f, ctab_d;         // [n_g_dev][CTAB_STRIDE] pre-scaled class coefficients (apply)
   DBuf pml_f[6], pml_d[6];     // dm x,y,z ; dp x,y,z (complex float / complex double)
   int lo[3], hi[3];
+  int tab_lo = 0, tab_n = 2;   // table rows covering the model's G range (staged in smem by the apply)
   std::vector<std::complex<double>> am_h[3], ap_h[3];  // host copies for export
   DBuf partials, tickets;      // apply epilogue scratch
   int zc = 1, nchunks = 1;
@@ -310,6 +311,8 @@ ApplyParams<R, S> make_params(const hz_coeffs* c) {
   p.w = c->w.as<S>();
   p.tab = sizeof(R) == 4 ? c->tab_f.as<R>() : c->tab_d.as<R>();
   p.ctab = sizeof(R) == 4 ? c->ctab_f.as<R>() : c->ctab_d.as<R>();
+  p.tab_lo = c->tab_lo;
+  p.tab_n = c->tab_n;
   p.invih2 = (R)(c->h * c->h);
   p.inv2ih2 = (R)(c->h * c->h / 2.0);
   p.inv3ih2 = (R)(c->h * c->h / 3.0);
@@ -362,7 +365,8 @@ hz_status apply_launch(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs, int e
   const int K = epi_k(epi);
   if (K > 0) {
     auto* cc = const_cast<hz_coeffs*>(c);
-    const long long nb = apply_nblocks_x<R>(c->grid.nx, c->grid.ny) * c->nchunks;
+    ApplyParams<R, S> pp = p;
+    const long long nb = apply_plan<R, S>(pp);
     HZ_CUDA(cc->partials.ensure(sizeof(double) * (size_t)nb * K * nrhs));
     if (cc->tickets.n < sizeof(unsigned) * (size_t)nrhs) {
       HZ_CUDA(cc->tickets.ensure(sizeof(unsigned) * (size_t)nrhs));
@@ -534,6 +538,18 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
   HZ_CUDA(c->w.ensure((size_t)(g->nz_local + 2) * plane * sizeof(R)));
   HZ_CUDA(launch_winv<R>(c->v.as<R>(), c->w.as<R>(), (long long)(g->nz_local + 2) * plane, s));
   count_launch();
+  // ---- table rows the apply stages in shared memory: G range of the model (all ranks) ± 1 row
+  {
+    const double inv_fh = 1.0 / (freq * g->h);
+    auto row_of = [&](double vv) {
+      const double sidx = (vv * inv_fh - c->g_min) / c->dg;
+      return (int)std::floor(std::fmin(std::fmax(sidx, 0.0), (double)(c->n_g_dev - 1)));
+    };
+    const int lo_r = std::max(0, std::min(row_of(vmin) - 1, c->n_g_dev - 2));
+    const int hi_r = std::max(lo_r + 1, std::min(row_of(vmax) + 2, c->n_g_dev - 1));
+    c->tab_lo = lo_r;
+    c->tab_n = hi_r - lo_r + 1;
+  }
   // ---- PML (host, double) → device deltas δ± = a± − 1/h²
   c->v_pml = (c->pml.v_pml > 0) ? c->pml.v_pml : vmax;
   const int ns[3] = {g->nx, g->ny, g->nz_global};
@@ -597,6 +613,11 @@ hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, c
   const hz_grid& g = *grid;
   if (g.nx < 3 || g.ny < 3 || g.nz_global < 3 || g.nz_local < 1 || g.z0 < 0 || g.z0 + g.nz_local > g.nz_global) {
     set_error("hz_assemble_coeffs: bad grid (dims >= 3, slab inside the global grid; S:156)");
+    return HZ_ERR_INVALID_ARG;
+  }
+  if ((long long)(g.nz_local + 2) * g.nx * g.ny >= (1LL << 31)) {
+    set_error("hz_assemble_coeffs: slab of >= 2^31 points per field (32-bit offsets in the apply); "
+              "split the grid over more z-slabs");
     return HZ_ERR_INVALID_ARG;
   }
   if (!(g.h > 0) || !(freq_hz > 0)) { set_error("hz_assemble_coeffs: need h > 0 and f > 0 (S:172)"); return HZ_ERR_DOMAIN; }

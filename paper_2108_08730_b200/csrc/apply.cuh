@@ -55,10 +55,14 @@ struct ApplyParams {
   long long fstride;          // (nzl+2)*plane: per-RHS field stride (elements)
   long long nlanes;           // nstrips*nx (set by the launcher)
   int zc, nchunks;            // z planes per CTA chunk, number of chunks
-  int nbx, nrhs;              // CTAs along the flattened (strip, x) axis; RHS in the launch
+  int nbx, nrhs;              // CTAs over all (strip, x-tile) warps of one z-chunk; RHS in the launch
+  // interior "box" (no PML, no boundary) covered by the lean launch: strips [box_s0, box_s1),
+  // x-tiles [box_t0, box_t1), z-chunks [box_c0, box_c1); box_nbx CTAs per chunk
+  int box_s0, box_s1, box_t0, box_t1, box_c0, box_c1, box_nbx;
   const S* v;                 // [nzl+2][ny][nx] velocity incl. halo planes
   const S* w;                 // [nzl+2][ny][nx] 1/v² incl. halo planes (apply input)
   const R* ctab;              // [n_g][CTAB_STRIDE] pre-scaled class coefficients + differences
+  int tab_lo, tab_n;          // rows [tab_lo, tab_lo + tab_n) cover every G of the model (staged in smem)
   const CS* u;                // [nrhs][nzl+2][ny][nx]
   const CS* ulo;              // optional low part of u (mixed-precision residual of the c64 solver:
                               // u = u + ulo in fp64; only read when R != S), else null

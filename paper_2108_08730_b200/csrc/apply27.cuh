@@ -38,11 +38,26 @@
 
 namespace hz {
 
-constexpr int CTAB_STRIDE = 16;  // c0 c1 c2 c3 m0 m1 m2 m3 | dc0..dc3 dm0..dm3
-
 template <typename R> struct Vec4;
 template <> struct Vec4<float> { typedef float4 T; };
 template <> struct Vec4<double> { typedef double4 T; };
+
+constexpr int CTAB_STRIDE = 16;  // c0 c1 c2 c3 m0 m1 m2 m3 | dc0..dc3 dm0..dm3
+// shared-memory row pitch of the staged table (elements): 20 floats / 18 doubles spread the rows of
+// neighbouring G over the 32 banks (lanes of a warp read different rows)
+template <typename R> struct SmemPitch { enum { V = 20 }; };
+template <> struct SmemPitch<double> { enum { V = 18 }; };
+
+template <typename R>
+__device__ __forceinline__ typename Vec4<R>::T lds4(const R* p);
+template <>
+__device__ __forceinline__ float4 lds4<float>(const float* p) { return *reinterpret_cast<const float4*>(p); }
+template <>
+__device__ __forceinline__ double4 lds4<double>(const double* p) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0];
+  const double2 b = reinterpret_cast<const double2*>(p)[1];
+  return make_double4(a.x, a.y, b.x, b.y);
+}
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ double4 ldg4(const double* p) {
@@ -54,6 +69,13 @@ __device__ __forceinline__ double4 ldg4(const double* p) {
 template <typename R>
 struct Coef8 {
   R c0, c1, c2, c3, m0, m1, m2, m3;
+};
+// Register state of one output row: c1..c3, m1..m3.  The centre coefficients follow from the stencil's
+// exact sum rules: c0 = −(6c1 + 12c2 + 8c3) (the stiffness annihilates constants, App. A) and
+// m0 = ω² − 6m1 − 12m2 − 8m3 (Σ class mass weights = 1); for Eq. "10" m0 = ω²w0 − … likewise.
+template <typename R>
+struct Coef6 {
+  R c1, c2, c3, m1, m2, m3;
 };
 
 // a2 + a3: G = v/(f h), clamp (A13), linear interpolation of the pre-scaled class coefficients
@@ -113,12 +135,18 @@ struct PlaneRegs {
 constexpr int XT = 30;
 
 #ifndef HZ_MINB_F
-#define HZ_MINB_F 4
+#define HZ_MINB_F 3
 #endif
 template <typename R> struct ApplyBounds { enum { MINB = HZ_MINB_F }; };
 template <> struct ApplyBounds<double> { enum { MINB = 2 }; };
 
-template <typename R, typename S, int NY, int W, bool COLLOC, int EPI>
+// The apply is two launches of this template (same arithmetic per point, so results do not depend on
+// which launch computes a point):
+//   INTERIOR = true : the "box" — warps whose footprint is inside the grid and outside the x/y PML,
+//                     for z-chunks whose output planes are outside the z PML: no PML code, no load
+//                     predicates, 32-bit element offsets from per-CTA uniform base pointers.
+//   INTERIOR = false: every other (warp, z-chunk); class form + per-axis PML corrections.
+template <typename R, typename S, int NY, int W, bool COLLOC, int EPI, bool INTERIOR>
 __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(ApplyParams<R, S> p) {
   typedef typename Cx<R>::T C;
   typedef typename Cx<S>::T CS;
@@ -126,25 +154,49 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
   constexpr int K = epi_k(EPI);
   const unsigned FULL = 0xffffffffu;
 
-  // ---- block → (rhs, x-block, z-chunk); rhs fastest so the RHS of one tile share w through L2
+  // ---- block → (rhs, warp group, z-chunk); rhs fastest so the RHS of one tile share w through L2
   const int nrhs = p.nrhs;
   const int bid = blockIdx.x;
   const int rhs = bid % nrhs;
   const int tile = bid / nrhs;
-  const int xb = tile % p.nbx;
-  const int chunk = tile / p.nbx;
+  const int nbx = INTERIOR ? p.box_nbx : p.nbx;
+  const int xb = tile % nbx;
+  const int chunk = (INTERIOR ? p.box_c0 : 0) + tile / nbx;
   if (p.active != nullptr && p.active[rhs] == 0) return;   // converged RHS (uniform per CTA)
 
+  // stage the used rows of the coefficient table in shared memory
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* stab = reinterpret_cast<R*>(smem_raw);
+  constexpr int SP = SmemPitch<R>::V;
+  for (int e = threadIdx.x; e < p.tab_n * CTAB_STRIDE; e += 32 * W) {
+    const int r = e / CTAB_STRIDE, k = e - r * CTAB_STRIDE;
+    stab[r * SP + k] = p.ctab[(long long)(p.tab_lo + r) * CTAB_STRIDE + k];
+  }
+  __syncthreads();
+
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ntx = (p.nx + XT - 1) / XT;
-  const int gw = xb * W + warp;                 // global warp index over (strip, x-tile)
-  const int strip = gw / ntx;
-  const int xt = gw - strip * ntx;
-  const int nstrips = (p.ny + NY - 1) / NY;
-  const bool warp_ok = strip < nstrips;
+  const int nx = p.nx, ny = p.ny;
+  const int ntx = (nx + XT - 1) / XT;
+  const int nstrips = (ny + NY - 1) / NY;
+  const int gw = xb * W + warp;
+  int strip, xt;
+  bool warp_ok;
+  if (INTERIOR) {
+    const int bw = p.box_t1 - p.box_t0;
+    strip = p.box_s0 + gw / bw;
+    xt = p.box_t0 + gw % bw;
+    warp_ok = strip < p.box_s1;
+  } else {
+    strip = gw / ntx;
+    xt = gw - strip * ntx;
+    warp_ok = strip < nstrips;
+    // warps of the box skip the z-chunks the interior launch covers
+    if (warp_ok && strip >= p.box_s0 && strip < p.box_s1 && xt >= p.box_t0 && xt < p.box_t1 &&
+        chunk >= p.box_c0 && chunk < p.box_c1)
+      warp_ok = false;
+  }
   const int x = xt * XT - 1 + lane;
   const int y0 = strip * NY;
-  const int nx = p.nx;
   const bool xin = warp_ok && x >= 0 && x < nx;
   const bool is_out = xin && lane >= 1 && lane <= XT;     // this lane produces outputs
 
@@ -152,46 +204,77 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
 #pragma unroll
   for (int r = 0; r < NY + 2; r++) {
     const int y = y0 - 1 + r;
-    if (xin && y >= 0 && y < p.ny) rmask |= 1u << r;
+    if (xin && y >= 0 && y < ny) rmask |= 1u << r;
   }
-  // warp-uniform: x- or y-PML among this warp's output points?
-  bool col_pml = is_out && (x < p.lo[0] || x > p.hi[0]);
+  bool gen_col = false;
+  if (!INTERIOR) {   // warp-uniform: x- or y-PML among this warp's output points?
+    bool col_pml = is_out && (x < p.lo[0] || x > p.hi[0]);
 #pragma unroll
-  for (int i = 0; i < NY; i++) {
-    const int y = y0 + i;
-    col_pml = col_pml || (is_out && y < p.ny && (y < p.lo[1] || y > p.hi[1]));
+    for (int i = 0; i < NY; i++) {
+      const int y = y0 + i;
+      col_pml = col_pml || (is_out && y < ny && (y < p.lo[1] || y > p.hi[1]));
+    }
+#ifndef HZ_NO_PML
+    gen_col = __any_sync(FULL, col_pml);
+#endif
   }
-  const bool gen_col = __any_sync(FULL, col_pml);
 
   const int zc0 = chunk * p.zc;
-  const int zc1 = min(zc0 + p.zc, p.nzl);
-  const long long plane = p.plane;
-  const long long rofs = (long long)rhs * p.fstride;
-  const long long lbase = (long long)(y0 - 1) * nx + x;   // (storage plane 0, row y0-1, column x)
-  const CS* __restrict__ ub = p.u + rofs + lbase;
-  const CS* __restrict__ ulb = (MIXED && p.ulo != nullptr) ? p.ulo + rofs + lbase : nullptr;
-  const S* __restrict__ wb = MIXED ? p.v + lbase : p.w + lbase;
+  const int zc1 = warp_ok ? min(zc0 + p.zc, p.nzl) : zc0 - 2;   // idle warps skip the march
+  const int plane = (int)p.plane;                                // host checks fstride < 2^31
+  // uniform per-CTA bases + 32-bit per-lane element offsets
+  const CS* __restrict__ ubase = p.u + (long long)rhs * p.fstride;
+  const CS* __restrict__ ulbase = (MIXED && p.ulo != nullptr) ? p.ulo + (long long)rhs * p.fstride : nullptr;
+  const S* __restrict__ wbase = MIXED ? p.v : p.w;
+  const int loff = (y0 - 1) * nx + x;          // (storage plane 0, row y0-1, column x); < 0 only if masked
   const C czv = czero(R(0));
   const int zlo = p.lo[2], zhi = p.hi[2];
   const int zbase = p.z0;
+  // warp-uniform: the whole footprint inside the grid (no load predicates)
+  const bool full_tile = INTERIOR || (warp_ok && (xt * XT - 1 >= 0) && (xt * XT + XT <= nx - 1) &&
+                                      (y0 - 1 >= 0) && (y0 + NY <= ny - 1));
 
   // fetch plane pl (local index; storage index pl+1)
   auto fetch = [&](PlaneRegs<R, NY>& P, int pl) {
+    const int off = loff + (pl + 1) * plane;
+    if (!MIXED && (INTERIOR || (full_tile && zbase + pl >= 0 && zbase + pl < p.nzg))) {
+#pragma unroll
+      for (int r = 0; r < NY + 2; r++) {
+        P.u[r] = to_cx(ldg_c(ubase + (unsigned)(off + r * nx)), R(0));
+        P.w[r] = (R)__ldg(wbase + (unsigned)(off + r * nx));
+      }
+      return;
+    }
     const int zg = zbase + pl;
     const unsigned m = (zg >= 0 && zg < p.nzg) ? rmask : 0u;
-    const long long pb = (long long)(pl + 1) * plane;
-    const CS* up = ub + pb;
-    const S* wp = wb + pb;
 #pragma unroll
     for (int r = 0; r < NY + 2; r++) {
       const bool ok = (m >> r) & 1u;
+      const unsigned o = (unsigned)(off + r * nx);
       if (!MIXED) {
-        P.u[r] = ok ? to_cx(ldg_c(up + r * nx), R(0)) : czv;
-        P.w[r] = ok ? (R)__ldg(wp + r * nx) : R(0);
+        P.u[r] = ok ? to_cx(ldg_c(ubase + o), R(0)) : czv;
+        P.w[r] = ok ? (R)__ldg(wbase + o) : R(0);
       } else {
-        P.u[r] = ok ? load_u<R, S>(ub, ulb, pb + (long long)r * nx) : czv;
-        const R vv = ok ? (R)__ldg(wp + r * nx) : R(1);
+        P.u[r] = ok ? load_u<R, S>(ubase, ulbase, o) : czv;
+        const R vv = ok ? (R)__ldg(wbase + o) : R(1);
         P.w[r] = ok ? R(1) / (vv * vv) : R(0);
+      }
+    }
+  };
+  // own-row w of plane pl, for the coefficients (prefetched one plane earlier than the field)
+  auto fetch_w = [&](R (&wc)[NY], int pl) {
+    const int zg = zbase + pl;
+    const bool pin = INTERIOR || (zg >= 0 && zg < p.nzg);
+    const int off = loff + (pl + 1) * plane + nx;
+#pragma unroll
+    for (int i = 0; i < NY; i++) {
+      const bool ok = INTERIOR || (pin && ((rmask >> (i + 1)) & 1u));
+      const unsigned o = (unsigned)(off + i * nx);
+      if (!MIXED) {
+        wc[i] = ok ? (R)__ldg(wbase + o) : R(0);
+      } else {
+        const R vv = ok ? (R)__ldg(wbase + o) : R(1);
+        wc[i] = ok ? R(1) / (vv * vv) : R(0);
       }
     }
   };
@@ -202,7 +285,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
 
   // PML x coefficients of this lane (gen_col warps): δ± = a± − h⁻²
   C dxm = czv, dxp = czv;
-  if (gen_col && xin) {
+  if (!INTERIOR && gen_col && xin) {
     dxm = p.dm[0][x];
     dxp = p.dp[0][x];
   }
@@ -210,52 +293,63 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
   const R s_k1 = p.inv_fh * p.inv_dg, s_k0 = -p.g_min * p.inv_dg, s_max = (R)(p.n_g - 1);
 
   // coefficients of output rows of plane pl+1 from w of that plane (a2 + a3)
-  auto coefs = [&](Coef8<R> (&cn)[NY], const PlaneRegs<R, NY>& Pn, bool valid) {
+  auto coefs = [&](Coef6<R> (&cn)[NY], R (&m0n)[NY], const R (&wc)[NY], bool valid) {
 #pragma unroll
     for (int i = 0; i < NY; i++) {
-      const R wn = Pn.w[i + 1];
+      const R wn = wc[i];
       if (valid) {
-        const R vv = (wn > R(0)) ? rsqrt_r(wn) : R(0);
+        const R vv = rsqrt_r(wn);                           // w > 0 on valid rows
         R sidx = fma(vv, s_k1, s_k0);                      // (G − g_min)/ΔG, G = v/(f h)
         sidx = fmin(fmax(sidx, R(0)), s_max);              // clamp (A13)
         const int ii = min((int)sidx, p.n_g - 2);
         const R tau = sidx - (R)ii;
-        const R* row = p.ctab + ii * CTAB_STRIDE;
+        const int li = min(max(ii - p.tab_lo, 0), p.tab_n - 2);   // staged range covers the model's G
+        const R* row = stab + li * SP;
         typedef typename Vec4<R>::T V4;
-        const V4 a = ldg4(row), b = ldg4(row + 4), da = ldg4(row + 8), db = ldg4(row + 12);
-        cn[i].c0 = fma(tau, da.x, a.x);
+        const V4 a = lds4<R>(row), b = lds4<R>(row + 4), da = lds4<R>(row + 8), db = lds4<R>(row + 12);
         cn[i].c1 = fma(tau, da.y, a.y);
         cn[i].c2 = fma(tau, da.z, a.z);
         cn[i].c3 = fma(tau, da.w, a.w);
-        cn[i].m0 = fma(tau, db.x, b.x);
         cn[i].m1 = fma(tau, db.y, b.y);
         cn[i].m2 = fma(tau, db.z, b.z);
         cn[i].m3 = fma(tau, db.w, b.w);
         if (COLLOC) {   // Eq. "10": ω²/κ0 for all 27 neighbours → m·w0 multiplies the u class sums
-          cn[i].m0 *= wn;
           cn[i].m1 *= wn;
           cn[i].m2 *= wn;
           cn[i].m3 *= wn;
         }
+        m0n[i] = COLLOC ? wn : R(1);
       } else {
-        cn[i] = Coef8<R>{R(0), R(0), R(0), R(0), R(0), R(0), R(0), R(0)};
+        cn[i] = Coef6<R>{R(0), R(0), R(0), R(0), R(0), R(0)};
+        m0n[i] = R(0);
       }
     }
   };
+  const R w2 = p.w2;
+  // centre coefficients from the sum rules (m0 needs the ω² scale: ω²·(1 or w0) in m0s)
+  auto c0_of = [](const Coef6<R>& c) { return -fma(R(6), c.c1, fma(R(12), c.c2, R(8) * c.c3)); };
+  auto m0_of = [&](const Coef6<R>& c, R m0s) { return fma(w2, m0s, -fma(R(6), c.m1, fma(R(12), c.m2, R(8) * c.m3))); };
 
   // One input plane pl.  cP: coefficients of output pl-1 (overwritten with those of pl+1);
   // cC: of output pl.  aP: partial of output pl-1 (overwritten with the first partial of pl+1);
   // aC: partial of output pl.  Roles alternate between two slots → no register rotation.
-  auto body = [&](PlaneRegs<R, NY>& Pc, PlaneRegs<R, NY>& Pn, Coef8<R> (&cP)[NY], Coef8<R> (&cC)[NY],
-                  C (&aP)[NY], C (&aC)[NY], int pl) {
+  auto body = [&](PlaneRegs<R, NY>& Pc, PlaneRegs<R, NY>& Pn, Coef6<R> (&cP)[NY], Coef6<R> (&cC)[NY],
+                  R (&mP)[NY], R (&mC)[NY], C (&aP)[NY], C (&aC)[NY], R (&wcN)[NY], R (&wcF)[NY], int pl) {
+    // wcN: own-row w of plane pl+1 (fetched one iteration ago); wcF receives plane pl+2
     if (pl + 1 <= zc1) fetch(Pn, pl + 1);   // prefetch: in flight while plane pl is consumed
+    if (pl + 2 < zc1) fetch_w(wcF, pl + 2);
     const bool do_prev = (pl - 1 >= zc0);
     const bool do_next = (pl + 1 < zc1);
     const int zg = zbase + pl;
-    const bool zp_prev = do_prev && (zg - 1 < zlo || zg - 1 > zhi);
-    const bool zp_cur = (pl >= zc0 && pl < zc1) && (zg < zlo || zg > zhi);
-    const bool zp_next = do_next && (zg + 1 < zlo || zg + 1 > zhi);
-    const bool zcorr = zp_prev || zp_cur || zp_next;
+    bool zp_prev = false, zp_cur = false, zp_next = false, zcorr = false;
+    if (!INTERIOR) {
+      zp_prev = do_prev && (zg - 1 < zlo || zg - 1 > zhi);
+      zp_cur = (pl >= zc0 && pl < zc1) && (zg < zlo || zg > zhi);
+      zp_next = do_next && (zg + 1 < zlo || zg + 1 > zhi);
+#ifndef HZ_NO_PML
+      zcorr = zp_prev || zp_cur || zp_next;
+#endif
+    }
 
     // ---- in-plane x sums: X = u(x-1) + u(x+1), Xq = q(x-1) + q(x+1), q = u·w
     C X[NY + 2], q[NY + 2], Xq[NY + 2];
@@ -271,10 +365,10 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
         Xq[r] = cfma(wbv, b, cscale(wa, a));
       }
     }
-    Coef8<R> cN[NY];
-    coefs(cN, Pn, do_next);
+    Coef6<R> cN[NY];
+    R mN[NY];
+    coefs(cN, mN, wcN, do_next);
 
-    C outv[NY];
 #pragma unroll
     for (int i = 0; i < NY; i++) {
       const C u0 = Pc.u[i + 1];
@@ -293,10 +387,10 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
       a = cfma(cP[i].m2, Q1, a);
       a = cfma(cP[i].m3, Q2, a);
       C b = aC[i];
-      b = cfma(cC[i].c0, u0, b);
+      b = cfma(c0_of(cC[i]), u0, b);
       b = cfma(cC[i].c1, P1, b);
       b = cfma(cC[i].c2, P2, b);
-      b = cfma(cC[i].m0, Q0, b);
+      b = cfma(m0_of(cC[i], mC[i]), Q0, b);
       b = cfma(cC[i].m1, Q1, b);
       b = cfma(cC[i].m2, Q2, b);
       C c = cscale(cN[i].c1, u0);
@@ -306,7 +400,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
       c = cfma(cN[i].m2, Q1, c);
       c = cfma(cN[i].m3, Q2, c);
       // ---- PML corrections (A8): a± = h⁻² + δ±; warp/plane-uniform branches
-      if (gen_col || zcorr) {
+      if (!INTERIOR && (gen_col || zcorr)) {
         // transverse weights from the class coefficients: t2 = c3 h²/3, t1 = t2 + c2 h²/2, t0 = c1 h² + 4 t1
         const R pt2 = cP[i].c3 * i3h, pt1 = fma(cP[i].c2, i2h, pt2), pt0 = fma(cP[i].c1, i1h, R(4) * pt1);
         const R ct2 = cC[i].c3 * i3h, ct1 = fma(cC[i].c2, i2h, ct2), ct0 = fma(cC[i].c1, i1h, R(4) * ct1);
@@ -357,20 +451,13 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
           }
         }
       }
-      outv[i] = a;
       aC[i] = b;          // output pl: "prev" of the next plane (slot roles swap)
       aP[i] = c;          // output pl+1: "cur" of the next plane
       cP[i] = cN[i];      // coefficients of pl+1 take the slot of pl-1
-    }
-
-    // ---- finalize outputs of plane pl-1, epilogue
-    if (do_prev && is_out) {
-      const long long ob = rofs + lbase + (long long)pl * plane;   // storage index of local plane pl-1
-#pragma unroll
-      for (int i = 0; i < NY; i++) {
-        if (!((rmask >> (i + 1)) & 1u)) continue;
-        const long long o = ob + (long long)(i + 1) * nx;
-        const C a = outv[i];
+      mP[i] = mN[i];
+      // ---- finalize output (row i, plane pl-1), epilogue
+      if (do_prev && is_out && (INTERIOR || ((rmask >> (i + 1)) & 1u))) {
+        const long long o = (long long)rhs * p.fstride + (unsigned)(loff + pl * plane + (i + 1) * nx);
         if (EPI == EPI_RESID) {
           const C bb = to_cx(ldg_c(p.bvec + o), R(0));
           const C rr = csub(bb, a);
@@ -395,39 +482,37 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
   };
 
   PlaneRegs<R, NY> A, B;
-  Coef8<R> c0s[NY], c1s[NY];
+  Coef6<R> c0s[NY], c1s[NY];
+  R m0a[NY], m0b[NY];
   C a0s[NY], a1s[NY];
 #pragma unroll
   for (int i = 0; i < NY; i++) {
-    c0s[i] = Coef8<R>{R(0), R(0), R(0), R(0), R(0), R(0), R(0), R(0)};
+    c0s[i] = Coef6<R>{R(0), R(0), R(0), R(0), R(0), R(0)};
     c1s[i] = c0s[i];
+    m0a[i] = m0b[i] = R(0);
     a0s[i] = czv;
     a1s[i] = czv;
   }
-  fetch(A, zc0 - 1);
-#ifdef HZ_NO_UNROLL
-  for (int pl = zc0 - 1; pl <= zc1; ++pl) {
-    body(A, B, c0s, c1s, a0s, a1s, pl);
-    PlaneRegs<R, NY> T = A; A = B; B = T;
-#pragma unroll
-    for (int i = 0; i < NY; i++) {
-      Coef8<R> t = c0s[i]; c0s[i] = c1s[i]; c1s[i] = t;
-      C ta = a0s[i]; a0s[i] = a1s[i]; a1s[i] = ta;
-    }
+  R w0s[NY], w1s[NY];
+  if (zc1 >= zc0) {
+    fetch(A, zc0 - 1);
+    if (zc0 < zc1) fetch_w(w0s, zc0);
   }
-#else
   int pl = zc0 - 1;
   for (; pl + 1 <= zc1; pl += 2) {
-    body(A, B, c0s, c1s, a0s, a1s, pl);
-    body(B, A, c1s, c0s, a1s, a0s, pl + 1);
+    body(A, B, c0s, c1s, m0a, m0b, a0s, a1s, w0s, w1s, pl);
+    body(B, A, c1s, c0s, m0b, m0a, a1s, a0s, w1s, w0s, pl + 1);
   }
-  if (pl <= zc1) body(A, B, c0s, c1s, a0s, a1s, pl);
-#endif
+  if (pl <= zc1) body(A, B, c0s, c1s, m0a, m0b, a0s, a1s, w0s, w1s, pl);
 
   if (K > 0) {
-    const int nblocks = p.nbx * p.nchunks;
+    // both launches share the partials / ticket: the general one owns blocks [0, nb_gen), the
+    // interior one [nb_gen, nb_gen + nb_int); the last block overall reduces in a fixed order
+    const int nb_gen = p.nbx * p.nchunks;
+    const int nblocks = nb_gen + p.box_nbx * (p.box_c1 - p.box_c0);
+    const int slot = INTERIOR ? nb_gen + tile : tile;
     block_grid_reduce<K, 32 * W>(part, p.partials + (long long)rhs * nblocks * K, p.dots + (long long)rhs * K,
-                                 p.tickets + rhs, nblocks, tile);
+                                 p.tickets + rhs, nblocks, slot);
   }
 }
 

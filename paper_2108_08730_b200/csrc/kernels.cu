@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "apply.cuh"
 #include "apply27.cuh"
 #include "kernels.h"
@@ -329,16 +331,67 @@ long long apply_nblocks_x(int nx, int ny) {   // CTAs covering one z-chunk of th
 template long long apply_nblocks_x<float>(int, int);
 template long long apply_nblocks_x<double>(int, int);
 
+// Split of one apply into the general launch (everything) and the interior box launch; returns the
+// total number of CTAs per RHS (partials of the dot epilogues).
+template <typename R, typename S>
+long long apply_plan(ApplyParams<R, S>& p) {
+  constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
+  p.nbx = (int)apply_nblocks_x<R>(p.nx, p.ny);
+  // x-tiles whose outputs lie in [max(lo,1), min(hi, nx-2)] (footprint inside the grid, no x-PML)
+  auto range = [](int lo, int hi, int n, int T, int& a, int& b) {
+    const int l = std::max(lo, 1), h = std::min(hi, n - 2);
+    a = (l + T - 1) / T;
+    b = (h - (T - 1) >= 0) ? (h - (T - 1)) / T + 1 : 0;
+    if (b < a) b = a;
+  };
+  range(p.lo[0], p.hi[0], p.nx, XT, p.box_t0, p.box_t1);
+  range(p.lo[1], p.hi[1], p.ny, NY, p.box_s0, p.box_s1);
+  // z-chunks whose output planes lie in [max(lo,1), min(hi, nzg-2)] (global)
+  const int zl = std::max(p.lo[2], 1) - p.z0, zh = std::min(p.hi[2], p.nzg - 2) - p.z0;
+  p.box_c0 = p.box_c1 = 0;
+  bool found = false;
+  for (int k = 0; k < p.nchunks; k++) {
+    const int a = k * p.zc, e = std::min(a + p.zc, p.nzl) - 1;
+    const bool in = a >= zl && e <= zh;
+    if (in && !found) { p.box_c0 = k; found = true; }
+    if (in) p.box_c1 = k + 1;
+  }
+  const long long bw = (long long)(p.box_s1 - p.box_s0) * (p.box_t1 - p.box_t0);
+  p.box_nbx = (int)((bw + W - 1) / W);
+  if (bw == 0 || p.box_c1 <= p.box_c0) {
+    p.box_nbx = 0;
+    p.box_c0 = p.box_c1 = 0;
+    p.box_s0 = p.box_s1 = p.box_t0 = p.box_t1 = 0;
+  }
+  return (long long)p.nbx * p.nchunks + (long long)p.box_nbx * (p.box_c1 - p.box_c0);
+}
+template long long apply_plan<float, float>(ApplyParams<float, float>&);
+template long long apply_plan<double, double>(ApplyParams<double, double>&);
+template long long apply_plan<double, float>(ApplyParams<double, float>&);
+
+template <typename R, typename S, bool COLLOC, int EPI, bool INTERIOR>
+static cudaError_t launch_one(const ApplyParams<R, S>& p, long long nb, cudaStream_t s) {
+  constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
+  auto kern = apply27_v2<R, S, NY, W, COLLOC, EPI, INTERIOR>;
+  if (nb <= 0) return cudaSuccess;
+  if (nb >= (1LL << 31)) return cudaErrorInvalidConfiguration;
+  const size_t smem = (size_t)p.tab_n * SmemPitch<R>::V * sizeof(R);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  kern<<<(unsigned)nb, 32 * W, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
 template <typename R, typename S, bool COLLOC, int EPI>
 static cudaError_t launch_apply_t(ApplyParams<R, S> p, int nrhs, cudaStream_t s) {
-  constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
-  auto kern = apply27_v2<R, S, NY, W, COLLOC, EPI>;
-  p.nbx = (int)apply_nblocks_x<R>(p.nx, p.ny);
+  apply_plan(p);
   p.nrhs = nrhs;
-  const long long nb = (long long)p.nbx * p.nchunks * nrhs;
-  if (nb >= (1LL << 31)) return cudaErrorInvalidConfiguration;
-  kern<<<(unsigned)nb, 32 * W, 0, s>>>(p);
-  return cudaGetLastError();
+  cudaError_t e = launch_one<R, S, COLLOC, EPI, false>(p, (long long)p.nbx * p.nchunks * nrhs, s);
+  if (e != cudaSuccess) return e;
+  return launch_one<R, S, COLLOC, EPI, true>(p, (long long)p.box_nbx * (p.box_c1 - p.box_c0) * nrhs, s);
 }
 
 template <typename R>
@@ -388,9 +441,9 @@ int apply_occupancy(bool colloc) {
   constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
   int nb = 0;
   if (colloc)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_v2<R, R, NY, W, true, EPI_DOT4>, 32 * W, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_v2<R, R, NY, W, true, EPI_DOT4, true>, 32 * W, 16 * 1024);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_v2<R, R, NY, W, false, EPI_DOT4>, 32 * W, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_v2<R, R, NY, W, false, EPI_DOT4, true>, 32 * W, 16 * 1024);
   return nb > 0 ? nb : 1;
 }
 template int apply_occupancy<float>(bool);

@@ -41,6 +41,7 @@ template <typename R> int apply_ny();
 template <typename R> int apply_warps();
 template <typename R> int apply_occupancy(bool colloc);
 template <typename R> long long apply_nblocks_x(int nx, int ny);   // CTAs along x of one z-chunk
+template <typename R, typename S> long long apply_plan(ApplyParams<R, S>& p);   // CTAs per RHS, both launches
 template <typename R, typename S>
 cudaError_t launch_apply(const ApplyParams<R, S>& p, int nrhs, bool colloc, int epi, cudaStream_t s);
 template <>

@@ -15,6 +15,7 @@ ci = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 nrhs = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 dt = sys.argv[3] if len(sys.argv) > 3 else "c64"
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 20
+npml_override = int(sys.argv[5]) if len(sys.argv) > 5 else None
 cfg = synth.get_config(ci)
 nz = cfg.nz if ci != 5 else 51
 dev = torch.device("cuda", 0)
@@ -23,7 +24,8 @@ rd = torch.float32 if dt == "c64" else torch.float64
 ctx = hz.hz_ctx_create(0)
 T = hz.hz_build_weight_table(4.0, 40.0, 0.1, 1e-2)
 freq = cfg.freqs[-1]
-C = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, nz, cfg.h, torch.from_numpy(v).to(dev, rd), freq, T, npml=cfg.npml,
+C = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, nz, cfg.h, torch.from_numpy(v).to(dev, rd), freq, T,
+                          npml=cfg.npml if npml_override is None else npml_override,
                           dtype=hz.HZ_C64 if dt == "c64" else hz.HZ_C128)
 u = C.alloc_field(nrhs)
 u.real.uniform_(-1, 1)
@@ -46,6 +48,6 @@ npts = cfg.nx * cfg.ny * nz
 esz = 4 if dt == "c64" else 8
 byts = npts * (esz + nrhs * 4 * esz)
 ms = float(np.median(ts))
-print(json.dumps({"cfg": ci, "grid": [cfg.nx, cfg.ny, nz], "nrhs": nrhs, "dtype": dt, "ms_median": ms,
+print(json.dumps({"cfg": ci, "npml": cfg.npml if npml_override is None else npml_override, "grid": [cfg.nx, cfg.ny, nz], "nrhs": nrhs, "dtype": dt, "ms_median": ms,
                   "ms_min": float(np.min(ts)), "gpts_s": npts * nrhs / ms / 1e6, "GBps": byts / ms / 1e6,
                   "frac_of_6543": byts / ms / 1e6 / 6543.4}))
