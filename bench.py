@@ -77,13 +77,6 @@ def dist_env():
     return ws, rank, local
 
 
-def slab(nz, P, r):
-    base, rem = divmod(nz, P)
-    nzl = base + (1 if r < rem else 0)
-    z0 = r * base + min(r, rem)
-    return z0, nzl
-
-
 def workload(args):
     cfg = synth.get_config(args.config)
     freq = args.freq if args.freq is not None else cfg.freqs[-1] if args.config == 4 else cfg.freq
@@ -242,18 +235,13 @@ def run_hz(args):
     dev = torch.device("cuda", local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
-    from paper_2108_08730_b200 import hz
+    from paper_2108_08730_b200 import hz, parallel
 
-    uid = None
-    if ws > 1:
-        obj = [hz.hz_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
-    ctx = hz.hz_ctx_create(local, ws, rank, uid)
+    ctx = parallel.make_context(local)      # NCCL communicator over all ranks (uid via torch.distributed)
 
     cfg, freq, nodes = workload(args)
     nrhs = len(nodes)
-    z0, nzl = slab(cfg.nz, ws, rank)
+    z0, nzl = parallel.slab_partition(cfg.nz, ws, rank)
     rd = torch.float32 if args.dtype == "c64" else torch.float64
     dt_code = hz.HZ_C64 if args.dtype == "c64" else hz.HZ_C128
     v_np = synth.velocity_slab(cfg, z0, nzl, device=dev if cfg.index == 5 else None)
@@ -312,19 +300,13 @@ def run_hz(args):
     clk = clocks.stop()
     st, rel, its, _ = last
 
-    def allreduce(vals, op):
-        t = torch.tensor(vals, dtype=torch.float64, device=dev)
-        if ws > 1:
-            dist.all_reduce(t, op=op)
-        return t.tolist()
-
     pts = sum(s["apply_points_total"] for s in stats)
     abytes = sum(s["apply_bytes_total"] for s in stats)
     ams = sum(s["apply_ms_total"] for s in stats)
     alaunch = sum(s["apply_launches"] for s in stats)
-    (tmax,) = allreduce([tot_ms], dist.ReduceOp.MAX if ws > 1 else None)
-    pts_all, bytes_all = allreduce([pts, abytes], dist.ReduceOp.SUM if ws > 1 else None)
-    (ams_max,) = allreduce([ams], dist.ReduceOp.MAX if ws > 1 else None)
+    (tmax,) = parallel.rank_max([tot_ms], dev)              # the job takes as long as its slowest rank
+    pts_all, bytes_all = parallel.rank_sum([pts, abytes], dev)
+    (ams_max,) = parallel.rank_max([ams], dev)
     ms_per_step = tmax / args.steps
     value = pts_all / (tmax * 1e-3) / 1e9
 
@@ -335,8 +317,8 @@ def run_hz(args):
             one_step(v_host, x_host)
         tot_e, stats_e, _, _ = timed(v_host, x_host, args.steps)
         pts_e = sum(s["apply_points_total"] for s in stats_e)
-        (tmax_e,) = allreduce([tot_e], dist.ReduceOp.MAX if ws > 1 else None)
-        (pts_e_all,) = allreduce([pts_e], dist.ReduceOp.SUM if ws > 1 else None)
+        (tmax_e,) = parallel.rank_max([tot_e], dev)
+        (pts_e_all,) = parallel.rank_sum([pts_e], dev)
         h2d = v_host.numel() * v_host.element_size() + x_host.numel() * x_host.element_size() + nodes.nbytes
         d2h = x_host.numel() * x_host.element_size()
         e2e = {"value": pts_e_all / (tmax_e * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d) * ws,

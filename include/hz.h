@@ -198,6 +198,10 @@ hz_status hz_point_sources(const hz_coeffs* c, int nsrc, const long long* node_x
 /* Number of libhz kernels launched since process start (evidence for the bench's gpu_launches). */
 long long hz_kernel_launch_count(void);
 
+/* libhz keeps device buffers released by destroyed coeffs / solver workspaces in a cache for reuse
+ * (re-assembling and re-solving every step then allocates nothing); this returns the cache to CUDA. */
+void hz_trim_memory(void);
+
 #ifdef __cplusplus
 }
 #endif

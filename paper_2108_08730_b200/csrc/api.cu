@@ -5,6 +5,8 @@
 #include <nccl.h>
 
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -93,17 +95,66 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-// RAII device buffer
+// Caching device allocator: blocks released by DBuf go to a free list and are reused by later
+// requests of a similar size (assemble/solve per step would otherwise cudaMalloc/cudaFree ~8 fields
+// per call, and cudaFree synchronises the device).  hz_trim_memory() returns the cache to CUDA.
+struct BlockCache {
+  std::mutex m;
+  std::multimap<size_t, void*> free;   // size -> block
+  std::map<void*, size_t> size_of;
+  cudaError_t acquire(size_t bytes, void** out) {
+    {
+      std::lock_guard<std::mutex> g(m);
+      auto it = free.lower_bound(bytes);
+      if (it != free.end() && it->first <= 2 * bytes + (1u << 20)) {
+        *out = it->second;
+        free.erase(it);
+        return cudaSuccess;
+      }
+    }
+    cudaError_t e = cudaMalloc(out, bytes);
+    if (e == cudaErrorMemoryAllocation) {   // give the cache back and retry once
+      cudaGetLastError();
+      trim();
+      e = cudaMalloc(out, bytes);
+    }
+    if (e == cudaSuccess) {
+      std::lock_guard<std::mutex> g(m);
+      size_of[*out] = bytes;
+    }
+    return e;
+  }
+  void release(void* p) {
+    std::lock_guard<std::mutex> g(m);
+    auto it = size_of.find(p);
+    if (it == size_of.end()) return;
+    free.emplace(it->second, p);
+  }
+  void trim() {
+    std::lock_guard<std::mutex> g(m);
+    for (auto& kv : free) {
+      cudaFree(kv.second);
+      size_of.erase(kv.second);
+    }
+    free.clear();
+  }
+};
+BlockCache& cache() {
+  static BlockCache* c = new BlockCache;   // never destroyed: blocks outlive static destructors
+  return *c;
+}
+
+// RAII device buffer (cached)
 struct DBuf {
   void* p = nullptr;
   size_t n = 0;
-  ~DBuf() { if (p) cudaFree(p); }
+  ~DBuf() { if (p) cache().release(p); }
   cudaError_t ensure(size_t bytes) {
     if (bytes <= n) return cudaSuccess;
-    if (p) cudaFree(p);
+    if (p) cache().release(p);
     p = nullptr;
     n = 0;
-    cudaError_t e = cudaMalloc(&p, bytes);
+    cudaError_t e = cache().acquire(bytes, &p);
     if (e == cudaSuccess) n = bytes;
     return e;
   }
@@ -165,6 +216,7 @@ extern "C" {
 const char* hz_last_error(void) { return g_err.c_str(); }
 const char* hz_version(void) { return "libhz 0.1 (sm_100a)"; }
 long long hz_kernel_launch_count(void) { return g_launches.load(); }
+void hz_trim_memory(void) { cache().trim(); }
 
 hz_status hz_get_unique_id(unsigned char id[128]) {
   if (!id) { set_error("hz_get_unique_id: id is NULL"); return HZ_ERR_INVALID_ARG; }
@@ -436,24 +488,26 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
     // forward differences for the in-kernel linear interpolation (A13)
     const double ih2d = 1.0 / (g->h * g->h), w2d = c->omega * c->omega;
     std::vector<double> cr((size_t)ng * CTAB_STRIDE, 0.0);
+    std::vector<double> v6((size_t)ng * 6);
     for (int i = 0; i < ng; i++) {
       const double t1 = u[5 * i + 0], t2 = u[5 * i + 1], mu0 = u[5 * i + 2], mu1 = u[5 * i + 3], mu2 = u[5 * i + 4];
       const double t0 = 1.0 - 4.0 * t1 - 4.0 * t2;
       const double mu3 = (1.0 - mu0 - 6.0 * mu1 - 12.0 * mu2) / 8.0;
-      double* o = &cr[(size_t)i * CTAB_STRIDE];
-      o[0] = ih2d * (-6.0 * t0);
-      o[1] = ih2d * (t0 - 4.0 * t1);
-      o[2] = ih2d * (2.0 * t1 - 2.0 * t2);
-      o[3] = ih2d * (3.0 * t2);
-      o[4] = w2d * mu0;
-      o[5] = w2d * mu1;
-      o[6] = w2d * mu2;
-      o[7] = w2d * mu3;
+      double* o = &v6[(size_t)i * 6];
+      o[0] = ih2d * (t0 - 4.0 * t1);        // face   c1
+      o[1] = ih2d * (2.0 * t1 - 2.0 * t2);  // edge   c2
+      o[2] = ih2d * (3.0 * t2);             // corner c3   (centre c0 = −(6c1 + 12c2 + 8c3))
+      o[3] = w2d * mu1;                     // m1 .. m3    (m0 = ω² − 6m1 − 12m2 − 8m3)
+      o[4] = w2d * mu2;
+      o[5] = w2d * mu3;
     }
-    for (int i = 0; i < ng; i++)
-      for (int k = 0; k < 8; k++)
-        cr[(size_t)i * CTAB_STRIDE + 8 + k] =
-            (i + 1 < ng) ? cr[(size_t)(i + 1) * CTAB_STRIDE + k] - cr[(size_t)i * CTAB_STRIDE + k] : 0.0;
+    for (int i = 0; i < ng; i++) {
+      double* o = &cr[(size_t)i * CTAB_STRIDE];
+      for (int k = 0; k < 6; k++) {
+        o[k] = v6[(size_t)i * 6 + k];
+        o[6 + k] = (i + 1 < ng) ? v6[(size_t)(i + 1) * 6 + k] - v6[(size_t)i * 6 + k] : 0.0;
+      }
+    }
     std::vector<float> cr_f(cr.size());
     for (size_t i = 0; i < cr.size(); i++) cr_f[i] = (float)cr[i];
     HZ_CUDA(c->ctab_d.ensure(cr.size() * sizeof(double)));
@@ -630,7 +684,12 @@ hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, c
   return HZ_ERR_INVALID_ARG;
 }
 
-void hz_coeffs_destroy(hz_coeffs* c) { delete c; }
+void hz_coeffs_destroy(hz_coeffs* c) {
+  if (!c) return;
+  // buffers go back to the cache for reuse: let queued work that still reads them finish first
+  cudaDeviceSynchronize();
+  delete c;
+}
 
 hz_status hz_coeffs_export(const hz_coeffs* c, void* record, void* pml_host, int nmax) {
   if (!c) { set_error("hz_coeffs_export: NULL coeffs"); return HZ_ERR_INVALID_ARG; }

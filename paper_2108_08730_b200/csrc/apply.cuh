@@ -54,11 +54,17 @@ struct ApplyParams {
   long long plane;            // nx*ny
   long long fstride;          // (nzl+2)*plane: per-RHS field stride (elements)
   long long nlanes;           // nstrips*nx (set by the launcher)
-  int zc, nchunks;            // z planes per CTA chunk, number of chunks
+  // z-chunks of the local planes: [0, zlo) (if nlow = 1), nint chunks of ≤ zc planes covering
+  // [zlo, zhi) (the planes whose outputs are outside the z-PML and the grid's first/last plane), then
+  // [zhi, nzl) (if non-empty); nchunks = nlow + nint + nhigh.  See chunk_range().
+  int zc, nchunks, zlo, zhi, nlow, nint;
   int nbx, nrhs;              // CTAs over all (strip, x-tile) warps of one z-chunk; RHS in the launch
   // interior "box" (no PML, no boundary) covered by the lean launch: strips [box_s0, box_s1),
   // x-tiles [box_t0, box_t1), z-chunks [box_c0, box_c1); box_nbx CTAs per chunk
   int box_s0, box_s1, box_t0, box_t1, box_c0, box_c1, box_nbx;
+  // complex64 interior launch (apply27_tma): the box as points [tma_x0, tma_x1) × [tma_y0, tma_y1),
+  // tiled by tma_ntx × tma_nty CTA tiles (then box_nbx = tma_ntx · tma_nty)
+  int tma_x0, tma_x1, tma_y0, tma_y1, tma_ntx, tma_nty;
   const S* v;                 // [nzl+2][ny][nx] velocity incl. halo planes
   const S* w;                 // [nzl+2][ny][nx] 1/v² incl. halo planes (apply input)
   const R* ctab;              // [n_g][CTAB_STRIDE] pre-scaled class coefficients + differences
@@ -82,6 +88,20 @@ struct ApplyParams {
   unsigned int* tickets;      // [nrhs]
   const int* active;          // [nrhs] or null
 };
+
+template <typename R, typename S>
+__host__ __device__ __forceinline__ void chunk_range(const ApplyParams<R, S>& p, int k, int& a, int& b) {
+  if (k < p.nlow) {
+    a = 0;
+    b = p.zlo;
+  } else if (k < p.nlow + p.nint) {
+    a = p.zlo + (k - p.nlow) * p.zc;
+    b = a + p.zc < p.zhi ? a + p.zc : p.zhi;
+  } else {
+    a = p.zhi;
+    b = p.nzl;
+  }
+}
 
 // ---------------------------------------------------------------------------------------------
 // Coefficients of one row from its velocity: interpolated (t1, t2, μ0, μ1, μ2) → c0..c3, m0..m3.

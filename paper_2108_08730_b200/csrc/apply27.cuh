@@ -8,8 +8,9 @@
 //  * Data: u (complex, [nrhs][nzl+2][ny][nx]) and w = 1/v² (real, [nzl+2][ny][nx], library-owned) are
 //    the only per-point inputs; the row coefficients are recomputed from w in registers (G = 1/(√w f h)).
 //    The coefficient table is pre-scaled on the host to the class coefficients
-//    (c0..c3 = h⁻²(−6t0, t0−4t1, 2t1−2t2, 3t2), m0..m3 = ω²μ0..3) with forward differences, 16 values per
-//    G row, read through L1 (__ldg of 16-byte vectors): interpolation = 8 FMAs.
+//    (c1..c3 = h⁻²(t0−4t1, 2t1−2t2, 3t2), m1..m3 = ω²μ1..3) with forward differences, 12 values per
+//    G row, staged in shared memory for the model's G range: interpolation = 6 FMAs; c0 and m0 follow
+//    from the sum rules.
 //  * Mapping: a lane owns one x position and a strip of NY consecutive y rows; a warp covers 32
 //    consecutive (strip, x) positions of the flattened strip-row space (no idle lanes for ragged nx:
 //    where x wraps inside a warp the missing neighbours are Dirichlet zeros anyway).  x-neighbours come
@@ -42,11 +43,13 @@ template <typename R> struct Vec4;
 template <> struct Vec4<float> { typedef float4 T; };
 template <> struct Vec4<double> { typedef double4 T; };
 
-constexpr int CTAB_STRIDE = 16;  // c0 c1 c2 c3 m0 m1 m2 m3 | dc0..dc3 dm0..dm3
-// shared-memory row pitch of the staged table (elements): 20 floats / 18 doubles spread the rows of
-// neighbouring G over the 32 banks (lanes of a warp read different rows)
-template <typename R> struct SmemPitch { enum { V = 20 }; };
-template <> struct SmemPitch<double> { enum { V = 18 }; };
+// Table row: the six register coefficients of an output row and their forward differences,
+//   c1 c2 c3 m1 | m2 m3 dc1 dc2 | dc3 dm1 dm2 dm3   (c = h⁻²·class stiffness, m = ω²·per-point mass)
+// c0 and m0 follow from the sum rules (Coef6).  48 bytes (fp32) = 3 × 16-byte shared loads per point.
+constexpr int CTAB_STRIDE = 12;
+// shared-memory row pitch (elements): 12 floats = 48 B puts 8 consecutive rows on distinct banks
+template <typename R> struct SmemPitch { enum { V = 12 }; };
+template <> struct SmemPitch<double> { enum { V = 12 }; };
 
 template <typename R>
 __device__ __forceinline__ typename Vec4<R>::T lds4(const R* p);
@@ -77,30 +80,6 @@ template <typename R>
 struct Coef6 {
   R c1, c2, c3, m1, m2, m3;
 };
-
-// a2 + a3: G = v/(f h), clamp (A13), linear interpolation of the pre-scaled class coefficients
-template <typename R>
-__device__ __forceinline__ Coef8<R> coef_from_v(R v, const R* __restrict__ ctab, int n_g, R g_min, R g_max, R inv_dg,
-                                                R inv_fh) {
-  R G = v * inv_fh;
-  G = fmin(fmax(G, g_min), g_max);
-  const R s = (G - g_min) * inv_dg;
-  const int i = min((int)s, n_g - 2);
-  const R tau = s - (R)i;
-  const R* row = ctab + (long long)i * CTAB_STRIDE;
-  typedef typename Vec4<R>::T V4;
-  const V4 a = ldg4(row), b = ldg4(row + 4), da = ldg4(row + 8), db = ldg4(row + 12);
-  Coef8<R> c;
-  c.c0 = fma(tau, da.x, a.x);
-  c.c1 = fma(tau, da.y, a.y);
-  c.c2 = fma(tau, da.z, a.z);
-  c.c3 = fma(tau, da.w, a.w);
-  c.m0 = fma(tau, db.x, b.x);
-  c.m1 = fma(tau, db.y, b.y);
-  c.m2 = fma(tau, db.z, b.z);
-  c.m3 = fma(tau, db.w, b.w);
-  return c;
-}
 
 // complex × complex (PML path); the rounding is spelled out (no compiler contraction choice) so that
 // every unrolled copy of the kernel body computes bitwise the same value
@@ -206,21 +185,25 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
     const int y = y0 - 1 + r;
     if (xin && y >= 0 && y < ny) rmask |= 1u << r;
   }
-  bool gen_col = false;
-  if (!INTERIOR) {   // warp-uniform: x- or y-PML among this warp's output points?
-    bool col_pml = is_out && (x < p.lo[0] || x > p.hi[0]);
+  bool gen_x = false, gen_y = false;   // warp-uniform: x-PML among the lanes / y-PML among the strip rows
+  if (!INTERIOR) {
+    const bool xp = is_out && (x < p.lo[0] || x > p.hi[0]);
+    bool yp = false;
 #pragma unroll
     for (int i = 0; i < NY; i++) {
       const int y = y0 + i;
-      col_pml = col_pml || (is_out && y < ny && (y < p.lo[1] || y > p.hi[1]));
+      yp = yp || (is_out && y < ny && (y < p.lo[1] || y > p.hi[1]));
     }
 #ifndef HZ_NO_PML
-    gen_col = __any_sync(FULL, col_pml);
+    gen_x = __any_sync(FULL, xp);
+    gen_y = __any_sync(FULL, yp);
 #endif
   }
+  const bool gen_col = gen_x || gen_y;
 
-  const int zc0 = chunk * p.zc;
-  const int zc1 = warp_ok ? min(zc0 + p.zc, p.nzl) : zc0 - 2;   // idle warps skip the march
+  int zc0, zc1;
+  chunk_range(p, chunk, zc0, zc1);
+  if (!warp_ok) zc1 = zc0 - 2;                                   // idle warps skip the march
   const int plane = (int)p.plane;                                // host checks fstride < 2^31
   // uniform per-CTA bases + 32-bit per-lane element offsets
   const CS* __restrict__ ubase = p.u + (long long)rhs * p.fstride;
@@ -285,7 +268,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
 
   // PML x coefficients of this lane (gen_col warps): δ± = a± − h⁻²
   C dxm = czv, dxp = czv;
-  if (!INTERIOR && gen_col && xin) {
+  if (!INTERIOR && gen_x && xin) {
     dxm = p.dm[0][x];
     dxp = p.dp[0][x];
   }
@@ -306,13 +289,13 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
         const int li = min(max(ii - p.tab_lo, 0), p.tab_n - 2);   // staged range covers the model's G
         const R* row = stab + li * SP;
         typedef typename Vec4<R>::T V4;
-        const V4 a = lds4<R>(row), b = lds4<R>(row + 4), da = lds4<R>(row + 8), db = lds4<R>(row + 12);
-        cn[i].c1 = fma(tau, da.y, a.y);
-        cn[i].c2 = fma(tau, da.z, a.z);
-        cn[i].c3 = fma(tau, da.w, a.w);
-        cn[i].m1 = fma(tau, db.y, b.y);
-        cn[i].m2 = fma(tau, db.z, b.z);
-        cn[i].m3 = fma(tau, db.w, b.w);
+        const V4 a = lds4<R>(row), b = lds4<R>(row + 4), d = lds4<R>(row + 8);
+        cn[i].c1 = fma(tau, b.z, a.x);
+        cn[i].c2 = fma(tau, b.w, a.y);
+        cn[i].c3 = fma(tau, d.x, a.z);
+        cn[i].m1 = fma(tau, d.y, a.w);
+        cn[i].m2 = fma(tau, d.z, b.x);
+        cn[i].m3 = fma(tau, d.w, b.y);
         if (COLLOC) {   // Eq. "10": ω²/κ0 for all 27 neighbours → m·w0 multiplies the u class sums
           cn[i].m1 *= wn;
           cn[i].m2 *= wn;
@@ -406,22 +389,28 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
         const R ct2 = cC[i].c3 * i3h, ct1 = fma(cC[i].c2, i2h, ct2), ct0 = fma(cC[i].c1, i1h, R(4) * ct1);
         const R nt2 = cN[i].c3 * i3h, nt1 = fma(cN[i].c2, i2h, nt2), nt0 = fma(cN[i].c1, i1h, R(4) * nt1);
         if (gen_col) {
-          // ΔL1 = δx(u) + δy(u), ΔL2 = δx(Y) + δy(X): the stretched parts of D_x, D_y
-          C dym = czv, dyp = czv;
-          if ((rmask >> (i + 1)) & 1u) {
-            dym = p.dm[1][y0 + i];
-            dyp = p.dp[1][y0 + i];
+          // ΔL1 = δx(u) + δy(u), ΔL2 = δx(Y) + δy(X): the stretched parts of D_x, D_y; the x part only
+          // in warps with x-PML lanes, the y part only for strips with y-PML rows
+          C L1 = czv, L2 = czv;
+          if (gen_x) {
+            const C uL = shfl_up_c(u0, 1), uR = shfl_down_c(u0, 1);
+            const C YL = shfl_up_c(Y, 1), YR = shfl_down_c(Y, 1);
+            L1 = zmulc(dxm, csub(uL, u0));
+            L1 = zfma(dxp, csub(uR, u0), L1);
+            L2 = zmulc(dxm, csub(YL, Y));
+            L2 = zfma(dxp, csub(YR, Y), L2);
           }
-          const C uL = shfl_up_c(u0, 1), uR = shfl_down_c(u0, 1);
-          const C YL = shfl_up_c(Y, 1), YR = shfl_down_c(Y, 1);
-          C L1 = zmulc(dxm, csub(uL, u0));
-          L1 = zfma(dxp, csub(uR, u0), L1);
-          L1 = zfma(dym, csub(Pc.u[i], u0), L1);
-          L1 = zfma(dyp, csub(Pc.u[i + 2], u0), L1);
-          C L2 = zmulc(dxm, csub(YL, Y));
-          L2 = zfma(dxp, csub(YR, Y), L2);
-          L2 = zfma(dym, csub(X[i], X[i + 1]), L2);
-          L2 = zfma(dyp, csub(X[i + 2], X[i + 1]), L2);
+          if (gen_y) {
+            C dym = czv, dyp = czv;
+            if ((rmask >> (i + 1)) & 1u) {
+              dym = p.dm[1][y0 + i];
+              dyp = p.dp[1][y0 + i];
+            }
+            L1 = zfma(dym, csub(Pc.u[i], u0), L1);
+            L1 = zfma(dyp, csub(Pc.u[i + 2], u0), L1);
+            L2 = zfma(dym, csub(X[i], X[i + 1]), L2);
+            L2 = zfma(dyp, csub(X[i + 2], X[i + 1]), L2);
+          }
           a = cfma(pt1, L1, a);
           a = cfma(pt2, L2, a);
           b = cfma(ct0, L1, b);

@@ -5,9 +5,11 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "apply.cuh"
 #include "apply27.cuh"
+#include "apply27_tma.cuh"
 #include "kernels.h"
 
 namespace hz {
@@ -333,35 +335,69 @@ template long long apply_nblocks_x<double>(int, int);
 
 // Split of one apply into the general launch (everything) and the interior box launch; returns the
 // total number of CTAs per RHS (partials of the dot epilogues).
+// complex64 interior launch geometry (apply27_tma)
+constexpr int TMA_NY = 2, TMA_WX = 2, TMA_WY = 4;
+typedef TmaTile<TMA_NY, TMA_WX, TMA_WY> TmaT;
+
 template <typename R, typename S>
 long long apply_plan(ApplyParams<R, S>& p) {
   constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
+  constexpr bool TMA = std::is_same<R, float>::value && std::is_same<S, float>::value;
   p.nbx = (int)apply_nblocks_x<R>(p.nx, p.ny);
-  // x-tiles whose outputs lie in [max(lo,1), min(hi, nx-2)] (footprint inside the grid, no x-PML)
-  auto range = [](int lo, int hi, int n, int T, int& a, int& b) {
-    const int l = std::max(lo, 1), h = std::min(hi, n - 2);
+  // tiles whose outputs lie in [max(lo,1), min(hi, hmax)] (footprint inside the grid, no PML); in x
+  // the TMA rows' 16-byte alignment overhang (≤ 7 elements past the tile) must stay inside the row
+  auto range = [](int lo, int hi, int hmax, int T, int& a, int& b) {
+    const int l = std::max(lo, 1), h = std::min(hi, hmax);
     a = (l + T - 1) / T;
     b = (h - (T - 1) >= 0) ? (h - (T - 1)) / T + 1 : 0;
     if (b < a) b = a;
   };
-  range(p.lo[0], p.hi[0], p.nx, XT, p.box_t0, p.box_t1);
-  range(p.lo[1], p.hi[1], p.ny, NY, p.box_s0, p.box_s1);
-  // z-chunks whose output planes lie in [max(lo,1), min(hi, nzg-2)] (global)
-  const int zl = std::max(p.lo[2], 1) - p.z0, zh = std::min(p.hi[2], p.nzg - 2) - p.z0;
-  p.box_c0 = p.box_c1 = 0;
-  bool found = false;
-  for (int k = 0; k < p.nchunks; k++) {
-    const int a = k * p.zc, e = std::min(a + p.zc, p.nzl) - 1;
-    const bool in = a >= zl && e <= zh;
-    if (in && !found) { p.box_c0 = k; found = true; }
-    if (in) p.box_c1 = k + 1;
+  range(p.lo[0], p.hi[0], TMA ? p.nx - 8 : p.nx - 2, XT, p.box_t0, p.box_t1);
+  range(p.lo[1], p.hi[1], p.ny - 2, NY, p.box_s0, p.box_s1);
+  // z-chunks: planes whose outputs lie in [max(lo,1), min(hi, nzg-2)] (global) are cut into chunks of
+  // ≤ zc planes (the interior chunks); the planes below / above form one chunk each
+  {
+    const int zl = std::min(std::max(std::max(p.lo[2], 1) - p.z0, 0), p.nzl);
+    const int zh = std::max(std::min(std::min(p.hi[2], p.nzg - 2) - p.z0 + 1, p.nzl), zl);   // exclusive
+    if (zh > zl) {
+      p.zlo = zl;
+      p.zhi = zh;
+      p.nlow = zl > 0 ? 1 : 0;
+      p.nint = (zh - zl + p.zc - 1) / p.zc;
+      p.nchunks = p.nlow + p.nint + (zh < p.nzl ? 1 : 0);
+      p.box_c0 = p.nlow;
+      p.box_c1 = p.nlow + p.nint;
+    } else {   // no interior planes: plain chunks, no box
+      p.zlo = 0;
+      p.zhi = p.nzl;
+      p.nlow = 0;
+      p.nint = (p.nzl + p.zc - 1) / p.zc;
+      p.nchunks = p.nint;
+      p.box_c0 = p.box_c1 = 0;
+    }
   }
   const long long bw = (long long)(p.box_s1 - p.box_s0) * (p.box_t1 - p.box_t0);
   p.box_nbx = (int)((bw + W - 1) / W);
-  if (bw == 0 || p.box_c1 <= p.box_c0) {
+  p.tma_x0 = XT * p.box_t0;
+  p.tma_x1 = XT * p.box_t1;
+  p.tma_y0 = NY * p.box_s0;
+  p.tma_y1 = NY * p.box_s1;
+  p.tma_ntx = p.tma_nty = 0;
+  bool empty = bw == 0 || p.box_c1 <= p.box_c0;
+  if (TMA && !empty) {
+    if (p.tma_x1 - p.tma_x0 < TmaT::TX || p.tma_y1 - p.tma_y0 < TmaT::TY) {
+      p.tma_ntx = p.tma_nty = 0;   // box smaller than one TMA tile: the register-path interior launch
+    } else {
+      p.tma_ntx = (p.tma_x1 - p.tma_x0 + TmaT::TX - 1) / TmaT::TX;
+      p.tma_nty = (p.tma_y1 - p.tma_y0 + TmaT::TY - 1) / TmaT::TY;
+      p.box_nbx = p.tma_ntx * p.tma_nty;
+    }
+  }
+  if (empty) {
     p.box_nbx = 0;
     p.box_c0 = p.box_c1 = 0;
     p.box_s0 = p.box_s1 = p.box_t0 = p.box_t1 = 0;
+    p.tma_ntx = p.tma_nty = 0;
   }
   return (long long)p.nbx * p.nchunks + (long long)p.box_nbx * (p.box_c1 - p.box_c0);
 }
@@ -385,13 +421,35 @@ static cudaError_t launch_one(const ApplyParams<R, S>& p, long long nb, cudaStre
   return cudaGetLastError();
 }
 
+template <bool COLLOC, int EPI>
+static cudaError_t launch_tma(const ApplyParams<float, float>& p, long long nb, cudaStream_t s) {
+  auto kern = apply27_tma<TMA_NY, TMA_WX, TMA_WY, COLLOC, EPI>;
+  if (nb <= 0) return cudaSuccess;
+  if (nb >= (1LL << 31)) return cudaErrorInvalidConfiguration;
+  const size_t smem = tma_smem_bytes<TMA_NY, TMA_WX, TMA_WY>(p.tab_n);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  kern<<<(unsigned)nb, 32 * TMA_WX * TMA_WY, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
 template <typename R, typename S, bool COLLOC, int EPI>
 static cudaError_t launch_apply_t(ApplyParams<R, S> p, int nrhs, cudaStream_t s) {
   apply_plan(p);
   p.nrhs = nrhs;
   cudaError_t e = launch_one<R, S, COLLOC, EPI, false>(p, (long long)p.nbx * p.nchunks * nrhs, s);
   if (e != cudaSuccess) return e;
-  return launch_one<R, S, COLLOC, EPI, true>(p, (long long)p.box_nbx * (p.box_c1 - p.box_c0) * nrhs, s);
+  const long long nbox = (long long)p.box_nbx * (p.box_c1 - p.box_c0) * nrhs;
+  if constexpr (std::is_same<R, float>::value && std::is_same<S, float>::value) {
+#ifndef HZ_NO_TMA
+    if (p.tma_ntx > 0) return launch_tma<COLLOC, EPI>(p, nbox, s);
+#endif
+  }
+  return launch_one<R, S, COLLOC, EPI, true>(p, nbox, s);
 }
 
 template <typename R>

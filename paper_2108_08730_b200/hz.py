@@ -68,6 +68,7 @@ _sigs = {
     "hz_last_error": (ct.c_char_p, []),
     "hz_version": (ct.c_char_p, []),
     "hz_kernel_launch_count": (ct.c_longlong, []),
+    "hz_trim_memory": (None, []),
     "hz_get_unique_id": (ct.c_int, [ct.c_char_p]),
     "hz_ctx_create": (ct.c_int, [ct.c_int, ct.c_int, ct.c_int, ct.c_char_p, _P(_vp)]),
     "hz_ctx_destroy": (None, [_vp]),
@@ -126,6 +127,10 @@ def hz_version() -> str:
 
 def hz_kernel_launch_count() -> int:
     return int(_lib.hz_kernel_launch_count())
+
+
+def hz_trim_memory() -> None:
+    _lib.hz_trim_memory()
 
 
 # ------------------------------------------------------------------------------------------------
