@@ -65,6 +65,9 @@ struct ApplyParams {
   // complex64 interior launch (apply27_tma): the box as points [tma_x0, tma_x1) × [tma_y0, tma_y1),
   // tiled by tma_ntx × tma_nty CTA tiles (then box_nbx = tma_ntx · tma_nty)
   int tma_x0, tma_x1, tma_y0, tma_y1, tma_ntx, tma_nty;
+  // general launch work list per RHS: the boundary z-chunks (low, high) × all warps (nbx CTAs each),
+  // then the interior z-chunks × the "frame" of warps outside the box (nbx_frame CTAs each)
+  int nbound, nbx_frame, frame_warps, gen_blocks;
   const S* v;                 // [nzl+2][ny][nx] velocity incl. halo planes
   const S* w;                 // [nzl+2][ny][nx] 1/v² incl. halo planes (apply input)
   const R* ctab;              // [n_g][CTAB_STRIDE] pre-scaled class coefficients + differences

@@ -138,9 +138,25 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
   const int bid = blockIdx.x;
   const int rhs = bid % nrhs;
   const int tile = bid / nrhs;
-  const int nbx = INTERIOR ? p.box_nbx : p.nbx;
-  const int xb = tile % nbx;
-  const int chunk = (INTERIOR ? p.box_c0 : 0) + tile / nbx;
+  // chunk and first warp of this CTA
+  int chunk, gw0;
+  bool frame = false;                    // general launch, interior chunk: warps of the frame only
+  if (INTERIOR) {
+    chunk = p.box_c0 + tile / p.box_nbx;
+    gw0 = (tile % p.box_nbx) * W;
+  } else if (p.nbound == p.nchunks) {    // no box: plain (chunk, warp group) enumeration
+    chunk = tile / p.nbx;
+    gw0 = (tile % p.nbx) * W;
+  } else if (tile < p.nbound * p.nbx) {  // boundary chunks: low (if any), then high
+    const int b = tile / p.nbx;
+    chunk = (b == 0 && p.nlow) ? 0 : p.nchunks - 1;
+    gw0 = (tile % p.nbx) * W;
+  } else {
+    const int t = tile - p.nbound * p.nbx;
+    chunk = p.nlow + t / p.nbx_frame;
+    gw0 = (t % p.nbx_frame) * W;
+    frame = true;
+  }
   if (p.active != nullptr && p.active[rhs] == 0) return;   // converged RHS (uniform per CTA)
 
   // stage the used rows of the coefficient table in shared memory
@@ -157,7 +173,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
   const int nx = p.nx, ny = p.ny;
   const int ntx = (nx + XT - 1) / XT;
   const int nstrips = (ny + NY - 1) / NY;
-  const int gw = xb * W + warp;
+  const int gw = gw0 + warp;
   int strip, xt;
   bool warp_ok;
   if (INTERIOR) {
@@ -165,14 +181,28 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
     strip = p.box_s0 + gw / bw;
     xt = p.box_t0 + gw % bw;
     warp_ok = strip < p.box_s1;
-  } else {
+  } else if (!frame) {
     strip = gw / ntx;
     xt = gw - strip * ntx;
     warp_ok = strip < nstrips;
-    // warps of the box skip the z-chunks the interior launch covers
-    if (warp_ok && strip >= p.box_s0 && strip < p.box_s1 && xt >= p.box_t0 && xt < p.box_t1 &&
-        chunk >= p.box_c0 && chunk < p.box_c1)
-      warp_ok = false;
+  } else {
+    // frame = strips above the box (all tiles), the box's strips outside [box_t0, box_t1), strips below
+    const int bw = p.box_t1 - p.box_t0, side = ntx - bw;
+    const int n_top = p.box_s0 * ntx, n_mid = (p.box_s1 - p.box_s0) * side;
+    warp_ok = gw < p.frame_warps;
+    if (gw < n_top) {
+      strip = gw / ntx;
+      xt = gw - strip * ntx;
+    } else if (gw < n_top + n_mid) {
+      const int k = gw - n_top;
+      strip = p.box_s0 + k / side;
+      const int jx = k - (strip - p.box_s0) * side;
+      xt = jx < p.box_t0 ? jx : jx + bw;
+    } else {
+      const int k = gw - n_top - n_mid;
+      strip = p.box_s1 + k / ntx;
+      xt = k - (strip - p.box_s1) * ntx;
+    }
   }
   const int x = xt * XT - 1 + lane;
   const int y0 = strip * NY;
@@ -497,7 +527,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
   if (K > 0) {
     // both launches share the partials / ticket: the general one owns blocks [0, nb_gen), the
     // interior one [nb_gen, nb_gen + nb_int); the last block overall reduces in a fixed order
-    const int nb_gen = p.nbx * p.nchunks;
+    const int nb_gen = p.gen_blocks;
     const int nblocks = nb_gen + p.box_nbx * (p.box_c1 - p.box_c0);
     const int slot = INTERIOR ? nb_gen + tile : tile;
     block_grid_reduce<K, 32 * W>(part, p.partials + (long long)rhs * nblocks * K, p.dots + (long long)rhs * K,

@@ -64,7 +64,10 @@ struct TmaTile {
   };
 };
 
-constexpr int TMA_STAGES = 4;
+#ifndef HZ_TMA_STAGES
+#define HZ_TMA_STAGES 4
+#endif
+constexpr int TMA_STAGES = HZ_TMA_STAGES;
 
 // dynamic smem: [table tab_n × 12 floats][STAGES × stage][2·STAGES mbarriers]
 template <int NY, int WX, int WY>
@@ -191,6 +194,21 @@ __global__ void __launch_bounds__(32 * WX * WY, 2) apply27_tma(ApplyParams<float
     const float* sw = reinterpret_cast<const float*>(st + (size_t)T::ROWS * T::UBYTES);
     const int us_p = ub0 + (pl + 1) * plane1, ws_p = wb0 + (pl + 1) * plane3;   // row-0 shifts
 
+#ifdef HZ_TMA_NOCOMPUTE
+    // data-movement ceiling experiment: consume the stage, write the centre value, no arithmetic
+    {
+      const C* ur = su + (NY * wy + 1) * T::UP + ((us_p + rpar[1]) & 1) + lane_u;
+      const C u0 = ur[1];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (do_prev && x_ok) p.au[obase0 + (long long)pl * plane] = u0;
+      if (warp == 0 && j + S < nplanes) {
+        mbar_wait(&empty[s], (j / S) & 1);
+        produce(j + S);
+      }
+      return;
+    }
+#endif
     C X[NY + 2], q[NY + 2], Xq[NY + 2], U[NY + 2];
 #pragma unroll
     for (int r = 0; r < NY + 2; r++) {
@@ -324,7 +342,7 @@ __global__ void __launch_bounds__(32 * WX * WY, 2) apply27_tma(ApplyParams<float
   if (j < nplanes) body(c0s, c1s, m0a, m0b, a0s, a1s, j);
 
   if (K > 0) {
-    const int nb_gen = p.nbx * p.nchunks;
+    const int nb_gen = p.gen_blocks;
     const int nblocks = nb_gen + p.box_nbx * (p.box_c1 - p.box_c0);
     block_grid_reduce<K, 32 * NW>(part, p.partials + (long long)rhs * nblocks * K, p.dots + (long long)rhs * K,
                                   p.tickets + rhs, nblocks, nb_gen + tile);

@@ -399,7 +399,20 @@ long long apply_plan(ApplyParams<R, S>& p) {
     p.box_s0 = p.box_s1 = p.box_t0 = p.box_t1 = 0;
     p.tma_ntx = p.tma_nty = 0;
   }
-  return (long long)p.nbx * p.nchunks + (long long)p.box_nbx * (p.box_c1 - p.box_c0);
+  // general work list
+  const int ntx = (p.nx + XT - 1) / XT, nstrips = (p.ny + NY - 1) / NY;
+  const int nhigh = p.nchunks - p.nlow - p.nint;
+  if (p.box_nbx > 0) {
+    p.nbound = p.nlow + nhigh;
+    p.frame_warps = nstrips * ntx - (p.box_s1 - p.box_s0) * (p.box_t1 - p.box_t0);
+    p.nbx_frame = (p.frame_warps + W - 1) / W;
+  } else {   // no box: every chunk is processed whole by the general launch
+    p.nbound = p.nchunks;
+    p.frame_warps = nstrips * ntx;
+    p.nbx_frame = p.nbx;
+  }
+  p.gen_blocks = p.nbound == p.nchunks ? p.nbx * p.nchunks : p.nbound * p.nbx + p.nint * p.nbx_frame;
+  return (long long)p.gen_blocks + (long long)p.box_nbx * (p.box_c1 - p.box_c0);
 }
 template long long apply_plan<float, float>(ApplyParams<float, float>&);
 template long long apply_plan<double, double>(ApplyParams<double, double>&);
@@ -441,7 +454,7 @@ template <typename R, typename S, bool COLLOC, int EPI>
 static cudaError_t launch_apply_t(ApplyParams<R, S> p, int nrhs, cudaStream_t s) {
   apply_plan(p);
   p.nrhs = nrhs;
-  cudaError_t e = launch_one<R, S, COLLOC, EPI, false>(p, (long long)p.nbx * p.nchunks * nrhs, s);
+  cudaError_t e = launch_one<R, S, COLLOC, EPI, false>(p, (long long)p.gen_blocks * nrhs, s);
   if (e != cudaSuccess) return e;
   const long long nbox = (long long)p.box_nbx * (p.box_c1 - p.box_c0) * nrhs;
   if constexpr (std::is_same<R, float>::value && std::is_same<S, float>::value) {
