@@ -351,6 +351,21 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
     // wcN: own-row w of plane pl+1 (fetched one iteration ago); wcF receives plane pl+2
     if (pl + 1 <= zc1) fetch(Pn, pl + 1);   // prefetch: in flight while plane pl is consumed
     if (pl + 2 < zc1) fetch_w(wcF, pl + 2);
+    // epilogue operands of the outputs finalised in this call (plane pl-1), loaded now so their latency
+    // overlaps the plane's arithmetic: r̂0 (DOT1/DOT4/RESID) and s = u (DOT4) or b (RESID)
+    C e1[NY], e2[NY];
+    const bool fin = (pl - 1 >= zc0) && is_out;
+#pragma unroll
+    for (int i = 0; i < NY; i++) {
+      e1[i] = czv;
+      e2[i] = czv;
+      if (K > 0 && fin && (INTERIOR || ((rmask >> (i + 1)) & 1u))) {
+        const long long o = (long long)rhs * p.fstride + (unsigned)(loff + pl * plane + (i + 1) * nx);
+        if (EPI != EPI_RESID || p.rhat != nullptr) e1[i] = to_cx(ldg_c(p.rhat + o), R(0));
+        if (EPI == EPI_DOT4) e2[i] = to_cx(ldg_c(p.u + o), R(0));
+        if (EPI == EPI_RESID) e2[i] = to_cx(ldg_c(p.bvec + o), R(0));
+      }
+    }
     const bool do_prev = (pl - 1 >= zc0);
     const bool do_next = (pl + 1 < zc1);
     const int zg = zbase + pl;
@@ -478,18 +493,17 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
       if (do_prev && is_out && (INTERIOR || ((rmask >> (i + 1)) & 1u))) {
         const long long o = (long long)rhs * p.fstride + (unsigned)(loff + pl * plane + (i + 1) * nx);
         if (EPI == EPI_RESID) {
-          const C bb = to_cx(ldg_c(p.bvec + o), R(0));
-          const C rr = csub(bb, a);
+          const C rr = csub(e2[i], a);
           p.au[o] = from_cx(rr, S(0));
           part[0] += (double)rr.x * (double)rr.x + (double)rr.y * (double)rr.y;
-          if (p.rhat != nullptr) acc_cdot(part[1], part[2], to_cx(ldg_c(p.rhat + o), R(0)), rr);
+          if (p.rhat != nullptr) acc_cdot(part[1], part[2], e1[i], rr);
         } else {
           p.au[o] = from_cx(a, S(0));
           if (EPI == EPI_DOT1) {
-            acc_cdot(part[0], part[1], to_cx(ldg_c(p.rhat + o), R(0)), a);
+            acc_cdot(part[0], part[1], e1[i], a);
           } else if (EPI == EPI_DOT4) {
-            const C sv = to_cx(ldg_c(p.u + o), R(0));
-            const C rh = to_cx(ldg_c(p.rhat + o), R(0));
+            const C sv = e2[i];
+            const C rh = e1[i];
             acc_cdot(part[0], part[1], a, sv);
             part[2] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
             acc_cdot(part[3], part[4], rh, sv);

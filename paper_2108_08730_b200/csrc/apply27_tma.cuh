@@ -76,8 +76,11 @@ __host__ __device__ constexpr size_t tma_smem_bytes(int tab_n) {
          2 * TMA_STAGES * 8;
 }
 
+#ifndef HZ_TMA_MINB
+#define HZ_TMA_MINB 2
+#endif
 template <int NY, int WX, int WY, bool COLLOC, int EPI>
-__global__ void __launch_bounds__(32 * WX * WY, 2) apply27_tma(ApplyParams<float, float> p) {
+__global__ void __launch_bounds__(32 * WX * WY, HZ_TMA_MINB) apply27_tma(ApplyParams<float, float> p) {
   typedef float R;
   typedef float2 C;
   typedef TmaTile<NY, WX, WY> T;
@@ -115,23 +118,25 @@ __global__ void __launch_bounds__(32 * WX * WY, 2) apply27_tma(ApplyParams<float
   const float2* ubase = p.u + (long long)rhs * p.fstride;
   const float* wbase = p.w;
 
-  // producer (warp 0, lane r < ROWS: u row r; lane ROWS + r: w row r) — issue plane j into slot j % S
-  auto produce = [&](int j) {
+  // producer: the 2·ROWS row copies of plane j go into slot j % S; copy c is issued by lane 0 of warp
+  // c % NW (the bulk-copy instruction takes uniform operands, so spreading the copies over the warps
+  // keeps any one warp from lagging behind the others)
+  auto issue_copies = [&](int j) {
     const int s = j % S;
     unsigned char* st = ring + (size_t)s * T::STAGE;
-    if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)T::STAGE);
-    __syncwarp();
-    const int pl = zc0 - 1 + j;                                           // local plane
-    if (lane < 2 * T::ROWS) {
-      const int r = lane < T::ROWS ? lane : lane - T::ROWS;
-      const long long e = (long long)(pl + 1) * plane + (long long)(Y0 - 1 + r) * nx + (X0 - 1);
-      if (lane < T::ROWS) {
-        const uintptr_t a = reinterpret_cast<uintptr_t>(ubase + e) & ~(uintptr_t)15;
-        bulk_g2s(st + (size_t)r * T::UBYTES, reinterpret_cast<const void*>(a), T::UBYTES, &full[s]);
-      } else {
-        const uintptr_t a = reinterpret_cast<uintptr_t>(wbase + e) & ~(uintptr_t)15;
-        bulk_g2s(st + (size_t)T::ROWS * T::UBYTES + (size_t)r * T::WBYTES, reinterpret_cast<const void*>(a), T::WBYTES,
-                 &full[s]);
+    const int pl = zc0 - 1 + j;
+    if (lane == 0) {
+      for (int c = warp; c < 2 * T::ROWS; c += NW) {
+        const int r = c < T::ROWS ? c : c - T::ROWS;
+        const long long e = (long long)(pl + 1) * plane + (long long)(Y0 - 1 + r) * nx + (X0 - 1);
+        if (c < T::ROWS) {
+          const uintptr_t a = reinterpret_cast<uintptr_t>(ubase + e) & ~(uintptr_t)15;
+          bulk_g2s(st + (size_t)r * T::UBYTES, reinterpret_cast<const void*>(a), T::UBYTES, &full[s]);
+        } else {
+          const uintptr_t a = reinterpret_cast<uintptr_t>(wbase + e) & ~(uintptr_t)15;
+          bulk_g2s(st + (size_t)T::ROWS * T::UBYTES + (size_t)r * T::WBYTES, reinterpret_cast<const void*>(a),
+                   T::WBYTES, &full[s]);
+        }
       }
     }
   };
@@ -145,9 +150,10 @@ __global__ void __launch_bounds__(32 * WX * WY, 2) apply27_tma(ApplyParams<float
   }
   // stage the coefficient table (generic proxy) while the first planes stream in
   for (int e = threadIdx.x; e < p.tab_n * CTAB_STRIDE; e += 32 * NW) stab[e] = p.ctab[(long long)p.tab_lo * CTAB_STRIDE + e];
+  if (threadIdx.x == 0)
+    for (int j = 0; j < S && j < nplanes; j++) mbar_expect_tx(&full[j], (uint32_t)T::STAGE);
   __syncthreads();
-  if (warp == 0)
-    for (int j = 0; j < S && j < nplanes; j++) produce(j);
+  for (int j = 0; j < S && j < nplanes; j++) issue_copies(j);
 
   // ---- per-lane geometry
   const int x = X0 + 32 * wx + lane;
@@ -188,6 +194,20 @@ __global__ void __launch_bounds__(32 * WX * WY, 2) apply27_tma(ApplyParams<float
     const int s = j % S;
     const bool do_prev = (pl - 1 >= zc0);
     const bool do_next = (pl + 1 < zc1);
+    // epilogue operands of the outputs finalised in this call (plane pl-1), loaded before the wait and
+    // the arithmetic so their latency is hidden
+    C e1[NY], e2[NY];
+#pragma unroll
+    for (int i = 0; i < NY; i++) {
+      e1[i] = make_float2(0.f, 0.f);
+      e2[i] = make_float2(0.f, 0.f);
+      if (K > 0 && do_prev && x_ok && yl0 + i >= Y0n) {
+        const long long o = obase0 + (long long)pl * plane + (long long)i * nx;
+        if (EPI != EPI_RESID || p.rhat != nullptr) e1[i] = ldg_c(p.rhat + o);
+        if (EPI == EPI_DOT4) e2[i] = ldg_c(p.u + o);
+        if (EPI == EPI_RESID) e2[i] = ldg_c(p.bvec + o);
+      }
+    }
     if (j + 1 < nplanes) mbar_wait(&full[(j + 1) % S], ((j + 1) / S) & 1);
     const unsigned char* st = ring + (size_t)s * T::STAGE;
     const C* su = reinterpret_cast<const C*>(st);
@@ -200,11 +220,12 @@ __global__ void __launch_bounds__(32 * WX * WY, 2) apply27_tma(ApplyParams<float
       const C* ur = su + (NY * wy + 1) * T::UP + ((us_p + rpar[1]) & 1) + lane_u;
       const C u0 = ur[1];
       __syncwarp();
+      if (j + S < nplanes && threadIdx.x == 0) mbar_expect_tx(&full[s], (uint32_t)T::STAGE);
       if (lane == 0) mbar_arrive(&empty[s]);
       if (do_prev && x_ok) p.au[obase0 + (long long)pl * plane] = u0;
-      if (warp == 0 && j + S < nplanes) {
+      if (j + S < nplanes) {
         mbar_wait(&empty[s], (j / S) & 1);
-        produce(j + S);
+        issue_copies(j + S);
       }
       return;
     }
@@ -256,8 +277,10 @@ __global__ void __launch_bounds__(32 * WX * WY, 2) apply27_tma(ApplyParams<float
         mN[i] = COLLOC ? wn : R(1);
       }
     }
-    // stage s is no longer needed by this warp (the next stage stays until the next iteration)
+    // stage s is no longer needed by this warp (the next stage stays until the next iteration); the
+    // refill's byte count is registered before the slot can be released, i.e. before any of its copies
     __syncwarp();
+    if (j + S < nplanes && threadIdx.x == 0) mbar_expect_tx(&full[s], (uint32_t)T::STAGE);
     if (lane == 0) mbar_arrive(&empty[s]);
 
     const long long ob = obase0 + (long long)pl * plane;   // output row yl0 of local plane pl-1
@@ -297,18 +320,17 @@ __global__ void __launch_bounds__(32 * WX * WY, 2) apply27_tma(ApplyParams<float
       if (do_prev && x_ok && yl0 + i >= Y0n) {
         const long long o = ob + (long long)i * nx;
         if (EPI == EPI_RESID) {
-          const C bb = ldg_c(p.bvec + o);
-          const C rr = csub(bb, a);
+          const C rr = csub(e2[i], a);
           p.au[o] = rr;
           part[0] += (double)rr.x * (double)rr.x + (double)rr.y * (double)rr.y;
-          if (p.rhat != nullptr) acc_cdot(part[1], part[2], ldg_c(p.rhat + o), rr);
+          if (p.rhat != nullptr) acc_cdot(part[1], part[2], e1[i], rr);
         } else {
           p.au[o] = a;
           if (EPI == EPI_DOT1) {
-            acc_cdot(part[0], part[1], ldg_c(p.rhat + o), a);
+            acc_cdot(part[0], part[1], e1[i], a);
           } else if (EPI == EPI_DOT4) {
-            const C sv = ldg_c(p.u + o);
-            const C rh = ldg_c(p.rhat + o);
+            const C sv = e2[i];
+            const C rh = e1[i];
             acc_cdot(part[0], part[1], a, sv);
             part[2] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
             acc_cdot(part[3], part[4], rh, sv);
@@ -317,10 +339,10 @@ __global__ void __launch_bounds__(32 * WX * WY, 2) apply27_tma(ApplyParams<float
         }
       }
     }
-    // producer: refill slot s with plane j + S once every warp has released it
-    if (warp == 0 && j + S < nplanes) {
+    // refill slot s with plane j + S once every warp has released it (each warp issues its copies)
+    if (j + S < nplanes) {
       mbar_wait(&empty[s], (j / S) & 1);
-      produce(j + S);
+      issue_copies(j + S);
     }
   };
 

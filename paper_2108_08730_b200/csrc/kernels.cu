@@ -336,7 +336,16 @@ template long long apply_nblocks_x<double>(int, int);
 // Split of one apply into the general launch (everything) and the interior box launch; returns the
 // total number of CTAs per RHS (partials of the dot epilogues).
 // complex64 interior launch geometry (apply27_tma)
-constexpr int TMA_NY = 2, TMA_WX = 2, TMA_WY = 4;
+#ifndef HZ_TMA_NY
+#define HZ_TMA_NY 2
+#endif
+#ifndef HZ_TMA_WX
+#define HZ_TMA_WX 4
+#endif
+#ifndef HZ_TMA_WY
+#define HZ_TMA_WY 2
+#endif
+constexpr int TMA_NY = HZ_TMA_NY, TMA_WX = HZ_TMA_WX, TMA_WY = HZ_TMA_WY;
 typedef TmaTile<TMA_NY, TMA_WX, TMA_WY> TmaT;
 
 template <typename R, typename S>

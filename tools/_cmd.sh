@@ -1,4 +1,3 @@
-timeout 120 python tools/diag_decomp.py 2>&1 | tail -6
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
-for c in "5 1 c64" "5 1 c64 20 0" "3 1 c64" "2 1 c64" "2 4 c64"; do timeout 120 python tools/prof_apply.py $c | cut -c1-150; done
-timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print({k:d[k] for k in ['value','ms_per_step','iterations','relres_max','apply_kernel_gpts_s','apply_share_of_step']}, d['roofline']['frac'])"
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
+for c in "4 1 c64" "4 4 c64"; do timeout 300 python tools/prof_apply.py $c | cut -c1-300; done
+HZ_CFG5_NZ=401 timeout 600 python tools/prof_apply.py 5 1 c64 10 | cut -c1-300

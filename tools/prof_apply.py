@@ -17,7 +17,7 @@ dt = sys.argv[3] if len(sys.argv) > 3 else "c64"
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 20
 npml_override = int(sys.argv[5]) if len(sys.argv) > 5 else None
 cfg = synth.get_config(ci)
-nz = cfg.nz if ci != 5 else 51
+nz = cfg.nz if ci != 5 else int(os.environ.get("HZ_CFG5_NZ", "51"))
 dev = torch.device("cuda", 0)
 v = synth.velocity_slab(cfg, 0, nz, device=dev if ci == 5 else None)
 rd = torch.float32 if dt == "c64" else torch.float64
