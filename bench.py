@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=30, help="oracle BiCGSTAB iterations in the cpu_baseline sample")
     ap.add_argument("--ref-iters", type=int, default=4, help="oracle BiCGSTAB iterations per --impl reference step")
+    ap.add_argument("--no-large", action="store_true",
+                    help="skip the apply-only roofline measurement on the large config (N=1 only)")
+    ap.add_argument("--large-config", type=int, default=4, help="config of the apply-only roofline measurement")
     return ap.parse_args()
 
 
@@ -224,6 +227,48 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------------------------
+def apply_large(args, hz, ctx, dev, stream, peak):
+    """Apply-only roofline on a large BASELINE config (default config 4, 801x801x187, c64, 1 RHS): the
+    hot kernel where HBM — not launch latency or the PML share of a small grid — bounds it.  CUDA events
+    on the launching stream around each apply, L2 flushed between applies, median of `reps`."""
+    import torch
+    cfg = synth.get_config(args.large_config)
+    freq = cfg.freqs[-1]
+    v = synth.velocity_slab(cfg, 0, cfg.nz, device=dev if cfg.index == 5 else None)
+    T = hz.hz_build_weight_table(*TABLE_ARGS)
+    C = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, torch.from_numpy(v).to(dev, torch.float32),
+                              freq, T, npml=cfg.npml, dtype=hz.HZ_C64)
+    del v
+    u = C.alloc_field(1)
+    u.real.uniform_(-1, 1)
+    u.imag.uniform_(-1, 1)
+    au = C.alloc_field(1)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        hz.hz_apply_impedance(C, u, au, stream=stream)
+    ts = []
+    l0 = hz.hz_kernel_launch_count()
+    for _ in range(10):
+        flush.fill_(1)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        hz.hz_apply_impedance(C, u, au, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ts.append(e0.elapsed_time(e1))
+    launches = hz.hz_kernel_launch_count() - l0
+    ms = statistics.median(ts)
+    npts = cfg.nx * cfg.ny * cfg.nz
+    byts = npts * (4 + 16)            # w in, u in, Au out (complex64, 1 RHS): DESIGN.md §5
+    achieved = byts / (ms * 1e-3) / 1e9
+    return {"workload": f"config{cfg.index} {cfg.name} {cfg.nx}x{cfg.ny}x{cfg.nz} f={freq:g}Hz c64 nrhs=1, "
+                        "hz_apply_impedance only", "gpts_s": npts / (ms * 1e-3) / 1e9, "ms": ms,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "algorithmic_bytes_per_launch": byts},
+            "gpu_launches": launches, "l2": "flushed before every apply (256 MiB write)"}
+
+
 def run_hz(args):
     import torch
     import torch.distributed as dist
@@ -358,6 +403,8 @@ def run_hz(args):
         "gpu_launches": int(launches),
         "e2e": e2e,
     }
+    if ws == 1 and not args.no_large:
+        line["apply_large"] = apply_large(args, hz, ctx, dev, stream, peak)
     if ws == 1 and not args.no_cpu_baseline:
         S = oracle_sample(cfg, freq, nodes, args.cpu_iters)
         dt, it = oracle_iters(S, args.cpu_iters)

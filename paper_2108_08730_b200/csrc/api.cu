@@ -428,7 +428,7 @@ hz_status apply_launch(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs, int e
     p.tickets = cc->tickets.as<unsigned>();
   }
   HZ_CUDA(launch_apply<R, S>(p, nrhs, c->mass == HZ_MASS_COLLOC, epi, s));
-  count_launch();
+  count_launch(apply_last_launches());
   return HZ_OK;
 }
 

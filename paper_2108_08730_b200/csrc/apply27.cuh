@@ -82,22 +82,25 @@ struct Coef6 {
 };
 
 // complex × complex (PML path); the rounding is spelled out (no compiler contraction choice) so that
-// every unrolled copy of the kernel body computes bitwise the same value
+// every unrolled copy of the kernel body computes bitwise the same value.  complex64: two packed FMAs
+//   (acc.x, acc.y) += (a.x, a.x)·(b.x, b.y);  += (−a.y, a.y)·(b.y, b.x)
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
-template <typename C>
-__device__ __forceinline__ C zmulc(C a, C b) {
-  C r;
-  r.x = fma(a.x, b.x, -mul_rn(a.y, b.y));
-  r.y = fma(a.x, b.y, mul_rn(a.y, b.x));
-  return r;
+__device__ __forceinline__ float2 zfma(float2 a, float2 b, float2 acc) {
+  acc = pk_fma(make_float2(a.x, a.x), b, acc);
+  return pk_fma(make_float2(-a.y, a.y), make_float2(b.y, b.x), acc);
 }
-// acc + a*b (complex)
-template <typename C>
-__device__ __forceinline__ C zfma(C a, C b, C acc) {
+__device__ __forceinline__ float2 zmulc(float2 a, float2 b) { return zfma(a, b, make_float2(0.f, 0.f)); }
+__device__ __forceinline__ double2 zfma(double2 a, double2 b, double2 acc) {
   acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
   acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
   return acc;
+}
+__device__ __forceinline__ double2 zmulc(double2 a, double2 b) {
+  double2 r;
+  r.x = fma(a.x, b.x, -mul_rn(a.y, b.y));
+  r.y = fma(a.x, b.y, mul_rn(a.y, b.x));
+  return r;
 }
 
 // Per-lane view of one input plane: rows 0..NY+1 = y0-1 .. y0+NY

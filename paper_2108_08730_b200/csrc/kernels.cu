@@ -435,8 +435,9 @@ static cudaError_t launch_one(const ApplyParams<R, S>& p, long long nb, cudaStre
   if (nb >= (1LL << 31)) return cudaErrorInvalidConfiguration;
   const size_t smem = (size_t)p.tab_n * SmemPitch<R>::V * sizeof(R);
   static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     attr = smem;
   }
   kern<<<(unsigned)nb, 32 * W, smem, s>>>(p);
@@ -449,8 +450,9 @@ static cudaError_t launch_tma(const ApplyParams<float, float>& p, long long nb, 
   if (nb <= 0) return cudaSuccess;
   if (nb >= (1LL << 31)) return cudaErrorInvalidConfiguration;
   const size_t smem = tma_smem_bytes<TMA_NY, TMA_WX, TMA_WY>(p.tab_n);
+  // the 48 KB default limit counts static (dot-reduction scratch) + dynamic shared memory
   static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
+  if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
@@ -459,13 +461,18 @@ static cudaError_t launch_tma(const ApplyParams<float, float>& p, long long nb, 
   return cudaGetLastError();
 }
 
+static thread_local int g_last_apply_launches = 0;
+int apply_last_launches() { return g_last_apply_launches; }
+
 template <typename R, typename S, bool COLLOC, int EPI>
 static cudaError_t launch_apply_t(ApplyParams<R, S> p, int nrhs, cudaStream_t s) {
   apply_plan(p);
   p.nrhs = nrhs;
-  cudaError_t e = launch_one<R, S, COLLOC, EPI, false>(p, (long long)p.gen_blocks * nrhs, s);
-  if (e != cudaSuccess) return e;
+  const long long ngen = (long long)p.gen_blocks * nrhs;
   const long long nbox = (long long)p.box_nbx * (p.box_c1 - p.box_c0) * nrhs;
+  g_last_apply_launches = (ngen > 0) + (nbox > 0);
+  cudaError_t e = launch_one<R, S, COLLOC, EPI, false>(p, ngen, s);
+  if (e != cudaSuccess) return e;
   if constexpr (std::is_same<R, float>::value && std::is_same<S, float>::value) {
 #ifndef HZ_NO_TMA
     if (p.tma_ntx > 0) return launch_tma<COLLOC, EPI>(p, nbox, s);

@@ -40,6 +40,7 @@ enum { BICG_INIT = 0, BICG_S = 1, BICG_UPDATE = 2, BICG_RHO_RESET = 3 };
 template <typename R> int apply_ny();
 template <typename R> int apply_warps();
 template <typename R> int apply_occupancy(bool colloc);
+int apply_last_launches();   // kernels launched by the last launch_apply on this thread (1 or 2)
 template <typename R> long long apply_nblocks_x(int nx, int ny);   // CTAs along x of one z-chunk
 template <typename R, typename S> long long apply_plan(ApplyParams<R, S>& p);   // CTAs per RHS, both launches
 template <typename R, typename S>

@@ -56,10 +56,10 @@ def gpu_solve(hz, C, nodes, rtol=1e-6):
 
 
 def golden(ci):
+    """Stored oracle wavefields (None if tools/make_golden_solutions.py has not written them yet: the
+    tests then rely on the oracle-matrix residual checks alone)."""
     path = os.path.join(GOLDEN, f"solve_cfg{ci}.npz")
-    if not os.path.exists(path):
-        pytest.skip(f"{path} missing (run tools/make_golden_solutions.py)")
-    return np.load(path)
+    return np.load(path) if os.path.exists(path) else None
 
 
 def rel(a, b):
@@ -81,7 +81,8 @@ def test_config1_solve_vs_oracle_and_analytic(hz, ctx, table, ga_table, dtype):
     assert np.linalg.norm(b - A @ x[0].ravel()) / np.linalg.norm(b) <= 1.5e-6
     # against the stored oracle wavefield as well (same model: v = 3000 is exact in float32)
     G = golden(1)
-    assert rel(x[0].ravel()[G["idx"]], G["values"][0]) <= 1e-4
+    if G is not None:
+        assert rel(x[0].ravel()[G["idx"]], G["values"][0]) <= 1e-4
     # end to end against the analytic Green's function (north-star check 1)
     src = nodes[0]
     D = metrics.distance(v.shape, src, cfg.h)
@@ -99,15 +100,16 @@ def test_config2_batched_solve(hz, ctx, table, ga_table, dtype):
     nodes = synth.source_nodes(cfg)
     st, relres, its, x = gpu_solve(hz, C, nodes)
     assert st == hz.HZ_OK and np.all(relres <= 1e-6), (st, relres, its)
-    G = golden(2)
-    for k, r in enumerate(G["rhs"]):
-        assert rel(x[r].ravel()[G["idx"]], G["values"][k]) <= 1e-4, r
     P = op.Problem(v, cfg.h, cfg.freq, cfg.npml, ga_table)
     A = op.assemble(P)
     B = op.point_sources(P, nodes)
     for r in range(len(nodes)):
         br = B[r].ravel()
         assert np.linalg.norm(br - A @ x[r].ravel()) / np.linalg.norm(br) <= 1.5e-6
+    G = golden(2)
+    if G is not None:
+        for k, r in enumerate(G["rhs"]):
+            assert rel(x[r].ravel()[G["idx"]], G["values"][k]) <= 1e-4, r
 
 
 def test_config3_batched_solve(hz, ctx, table, ga_table):
@@ -118,15 +120,16 @@ def test_config3_batched_solve(hz, ctx, table, ga_table):
     nodes = synth.source_nodes(cfg)
     st, relres, its, x = gpu_solve(hz, C, nodes)
     assert st == hz.HZ_OK and np.all(relres <= 1e-6), (st, relres, its)
-    G = golden(3)
-    for k, r in enumerate(G["rhs"]):
-        assert rel(x[r].ravel()[G["idx"]], G["values"][k]) <= 1e-4, r
     P = op.Problem(v, cfg.h, cfg.freq, cfg.npml, ga_table)
     A = op.assemble(P)
     B = op.point_sources(P, nodes[:4])
     for r in range(4):
         br = B[r].ravel()
         assert np.linalg.norm(br - A @ x[r].ravel()) / np.linalg.norm(br) <= 1.5e-6
+    G = golden(3)
+    if G is not None:
+        for k, r in enumerate(G["rhs"]):
+            assert rel(x[r].ravel()[G["idx"]], G["values"][k]) <= 1e-4, r
 
 
 def test_solver_edge_cases(hz, ctx, table):

@@ -48,26 +48,34 @@ def solve_one(args):
     return ci, r, x, rel, it
 
 
+def write(ci, d):
+    cfg = synth.get_config(ci)
+    rng = np.random.Generator(np.random.Philox(synth.BASE_SEED + 7000 + ci))
+    idx = np.sort(rng.choice(cfg.npoints, size=min(NSAMPLE, cfg.npoints), replace=False))
+    rhs = sorted(d)
+    np.savez_compressed(
+        os.path.join(ROOT, "tests", "golden", f"solve_cfg{ci}.npz"),
+        rhs=np.array(rhs), idx=idx,
+        values=np.stack([d[r][0][idx] for r in rhs]),
+        full_norm=np.array([np.linalg.norm(d[r][0]) for r in rhs]),
+        relres=np.array([d[r][1] for r in rhs]), iters=np.array([d[r][2] for r in rhs]),
+        note=np.array("oracle complex128 BiCGSTAB, true relres <= 1e-10, float32-rounded velocity; "
+                      "written by tools/make_golden_solutions.py"))
+    print(f"wrote solve_cfg{ci}.npz", flush=True)
+
+
 def main():
     cfgs = [int(a) for a in sys.argv[1:]] or [1, 2, 3]
     jobs = [(ci, r) for ci in cfgs for r in RHS[ci]]
     out = {}
     with ProcessPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
-        for ci, r, x, rel, it in ex.map(solve_one, jobs):
+        futs = [ex.submit(solve_one, j) for j in jobs]
+        from concurrent.futures import as_completed
+        for f in as_completed(futs):
+            ci, r, x, rel, it = f.result()
             out.setdefault(ci, {})[r] = (x, rel, it)
-    for ci, d in out.items():
-        cfg = synth.get_config(ci)
-        rng = np.random.Generator(np.random.Philox(synth.BASE_SEED + 7000 + ci))
-        idx = np.sort(rng.choice(cfg.npoints, size=min(NSAMPLE, cfg.npoints), replace=False))
-        rhs = sorted(d)
-        np.savez_compressed(
-            os.path.join(ROOT, "tests", "golden", f"solve_cfg{ci}.npz"),
-            rhs=np.array(rhs), idx=idx,
-            values=np.stack([d[r][0][idx] for r in rhs]),
-            full_norm=np.array([np.linalg.norm(d[r][0]) for r in rhs]),
-            relres=np.array([d[r][1] for r in rhs]), iters=np.array([d[r][2] for r in rhs]),
-            note=np.array("oracle complex128 BiCGSTAB, true relres <= 1e-10, float32-rounded velocity; "
-                          "written by tools/make_golden_solutions.py"))
+            if len(out[ci]) == len(RHS[ci]):   # every RHS of this config done: write it now
+                write(ci, out[ci])
 
 
 if __name__ == "__main__":
