@@ -102,9 +102,9 @@ __global__ void __launch_bounds__(32 * WX * WY, HZ_TMA_MINB) apply27_tma(ApplyPa
   const int X0 = min(X0n, p.tma_x1 - T::TX), Y0 = min(Y0n, p.tma_y1 - T::TY);
   if (p.active != nullptr && p.active[rhs] == 0) return;
 
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* stab = reinterpret_cast<float*>(smem_raw);
-  unsigned char* ring = smem_raw + (((size_t)p.tab_n * 12 * 4 + 127) / 128) * 128;
+  extern __shared__ __align__(1024) unsigned char smem_tma[];   // own symbol: alignment not shared with other kernels
+  float* stab = reinterpret_cast<float*>(smem_tma);
+  unsigned char* ring = smem_tma + (((size_t)p.tab_n * 12 * 4 + 127) / 128) * 128;
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)S * T::STAGE);
   uint64_t* empty = full + S;
 
