@@ -224,3 +224,23 @@ def test_domain_errors(hz, ctx, table):
     assert e.value.status == -2
     with pytest.raises(hz.HzError):
         assemble(hz, ctx, table, np.full((5, 2, 5), 2000.0), 10.0, 5.0, 1, "c64")
+
+
+@pytest.mark.parametrize("mass", ["eq8", "colloc"])
+def test_apply_tma_box_tiles(hz, ctx, table, ga_table, mass):
+    """Grid whose PML-free box is wider than a bulk-copy (TMA) tile: odd nx (rows alternate 16-byte
+    alignment), clamped overlapping last tiles in x and y, 3 RHS — full oracle comparison (the interior
+    launch is apply27_tma here, the frame the general launch)."""
+    rng = np.random.default_rng(77)
+    nz, ny, nx, h, f, npml = 21, 27, 301, 20.0, 8.0, 4
+    v = rng.uniform(1600.0, 4200.0, (nz, ny, nx))
+    u = synth.random_field((3, nz, ny, nx), seed=9)
+    C = assemble(hz, ctx, table, v, h, f, npml, "c64", mass=mass)
+    l0 = hz.hz_kernel_launch_count()
+    got = gpu_apply(hz, C, u)
+    assert hz.hz_kernel_launch_count() - l0 == 2          # general (frame) + interior (box) launches
+    ref = op.apply(op.assemble(oracle_problem(v, h, f, npml, ga_table, "c64", mass=mass)), u)
+    assert rel(got, ref) <= TOL["c64"], rel(got, ref)
+    # every point checked individually as well (a missed or doubly-written tile would show locally)
+    err = np.abs(got - ref) / (np.abs(ref) + 1e-3 * np.abs(ref).max())
+    assert err.max() <= 1e-4, np.unravel_index(err.argmax(), err.shape)
