@@ -205,6 +205,15 @@ struct hz_coeffs {
   std::vector<std::complex<double>> am_h[3], ap_h[3];  // host copies for export
   DBuf partials, tickets;      // apply epilogue scratch
   int zc = 1, nchunks = 1;
+  // complex64 RHS-fused apply: tile geometry, and per number of RHS groups a work list
+  // {tile, z0, z1, mode} (x/y-PML items, then z-PML, then PML-free), built on first use
+  struct CpPlan {
+    DBuf work;
+    int n_xy = 0, n_z = 0, n_lean = 0;
+  };
+  bool cp_on = false;
+  int cp_tx = 0, cp_ns = 0, cp_ntx = 0, cp_nty = 0;
+  std::map<int, std::unique_ptr<CpPlan>> cp_plans;
   std::unique_ptr<SolverWork> work;
   size_t esz() const { return dtype == HZ_C64 ? 4 : 8; }   // real element size
   long long plane() const { return (long long)grid.nx * grid.ny; }
@@ -413,12 +422,16 @@ hz_status allreduce_sum(const hz_coeffs* c, double* buf, size_t n, cudaStream_t 
 }
 
 template <typename R, typename S>
+hz_status cp_attach(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs);
+
+template <typename R, typename S>
 hz_status apply_launch(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs, int epi, cudaStream_t s) {
   const int K = epi_k(epi);
+  if (epi != EPI_RESID) HZ_TRY(cp_attach(c, p, nrhs));
   if (K > 0) {
     auto* cc = const_cast<hz_coeffs*>(c);
     ApplyParams<R, S> pp = p;
-    const long long nb = apply_plan<R, S>(pp);
+    const long long nb = apply_slots<R, S>(pp);
     HZ_CUDA(cc->partials.ensure(sizeof(double) * (size_t)nb * K * nrhs));
     if (cc->tickets.n < sizeof(unsigned) * (size_t)nrhs) {
       HZ_CUDA(cc->tickets.ensure(sizeof(unsigned) * (size_t)nrhs));
@@ -429,6 +442,118 @@ hz_status apply_launch(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs, int e
   }
   HZ_CUDA(launch_apply<R, S>(p, nrhs, c->mass == HZ_MASS_COLLOC, epi, s));
   count_launch(apply_last_launches());
+  return HZ_OK;
+}
+
+// Tile geometry of the complex64 RHS-fused apply (apply27_cp): tx ≤ 64 columns with ntx = ⌈nx/64⌉
+// tiles per row (tx = ⌈nx/ntx⌉, the last tile clamped inside the grid), 2·ns rows with tx·ns ≤ 256.
+hz_status cp_geometry(hz_coeffs* c) {
+  const int nx = c->grid.nx, ny = c->grid.ny;
+  const int ntx = (nx + 63) / 64;
+  const int tx = (nx + ntx - 1) / ntx;
+  int ns = std::min(CP_NSMAX, CP_NT / tx);
+  ns = std::max(1, std::min(ns, ny / 2));
+  if ((2 * ns + 2) * (tx + 2) > CP_KS * CP_NT) { set_error("cp_geometry: tile too large"); return HZ_ERR_INVALID_ARG; }
+  c->cp_tx = tx;
+  c->cp_ns = ns;
+  c->cp_ntx = ntx;
+  c->cp_nty = (ny + 2 * ns - 1) / (2 * ns);
+  c->cp_on = getenv("HZ_NO_CP") == nullptr;
+  return HZ_OK;
+}
+
+// Work list for `ngroups` RHS groups.  A tile with x/y-PML outputs marches the whole slab (its list is
+// x/y); the others are split at the z-PML boundaries into z-PML items (the planes below / above) and
+// PML-free items.  Each list's z-segments are cut into chunks whose count balances the list over
+// whole waves of resident CTAs (SMs × CTAs/SM of that variant) against the 2 extra halo planes a
+// chunk reads (env HZ_CP_ZC forces a chunk length).
+const hz_coeffs::CpPlan* cp_plan(hz_coeffs* c, int ngroups, int nr) {
+  const int key = ngroups * 8 + nr;
+  auto it = c->cp_plans.find(key);
+  if (it != c->cp_plans.end()) return it->second.get();
+  const hz_grid& g = c->grid;
+  const int nx = g.nx, ny = g.ny, nzl = g.nz_local;
+  const int tx = c->cp_tx, TY = 2 * c->cp_ns, ntx = c->cp_ntx, ntiles = ntx * c->cp_nty;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->ctx->device);
+  int force = 0;
+  if (const char* e = getenv("HZ_CP_ZC")) force = atoi(e);
+  // number of chunks of a segment of `len` planes shared by `nt` tiles
+  auto nchunks = [&](int nt, int len, int mode) {
+    if (len <= 0 || nt <= 0) return 1;
+    if (force > 0) return std::max(1, (len + force - 1) / force);
+    const double slots = (double)sms * cp_occupancy(c->tab_n, c->cp_ns, mode, nr);
+    int best = 1;
+    double best_eff = -1;
+    for (int n = 1; n <= std::max(1, len / 4); n++) {
+      const double waves = (double)nt * n * ngroups / slots;
+      const double L = (double)len / n;
+      const double eff = waves / std::ceil(waves) * L / (L + 2.0);
+      if (eff > best_eff + 1e-9) { best_eff = eff; best = n; }
+    }
+    return best;
+  };
+  auto cut = [](std::vector<int4>& v, int t, int a, int b, int n, int mode) {
+    if (b <= a) return;
+    n = std::min(n, b - a);
+    for (int k = 0; k < n; k++)
+      v.push_back(make_int4(t, a + (int)((long long)(b - a) * k / n), a + (int)((long long)(b - a) * (k + 1) / n), mode));
+  };
+  const int zl = std::min(std::max(c->lo[2] - g.z0, 0), nzl);
+  const int zh = std::min(std::max(c->hi[2] - g.z0 + 1, zl), nzl);
+  std::vector<int> xy_tiles, in_tiles;
+  for (int t = 0; t < ntiles; t++) {
+    const int X0 = std::min((t % ntx) * tx, nx - tx), Y0 = std::min((t / ntx) * TY, ny - TY);
+    const bool xy = X0 < c->lo[0] || X0 + tx - 1 > c->hi[0] || Y0 < c->lo[1] || Y0 + TY - 1 > c->hi[1];
+    (xy ? xy_tiles : in_tiles).push_back(t);
+  }
+  const int n_xy = nchunks((int)xy_tiles.size(), nzl, CP_PMLXY);
+  const int n_lean = nchunks((int)in_tiles.size(), zh - zl, CP_LEAN);
+  std::vector<int4> vxy, vz, vl;
+  for (int k = 0; k < n_xy; k++)   // chunk-major: concurrently running CTAs share z-planes in L2
+    for (int t : xy_tiles) {
+      const int a = (int)((long long)nzl * k / n_xy), b = (int)((long long)nzl * (k + 1) / n_xy);
+      if (b > a) vxy.push_back(make_int4(t, a, b, CP_PMLXY));
+    }
+  for (int t : in_tiles) {
+    cut(vz, t, 0, zl, 1, CP_PMLZ);
+    cut(vz, t, zh, nzl, 1, CP_PMLZ);
+  }
+  for (int k = 0; k < n_lean; k++)
+    for (int t : in_tiles) {
+      const int a = zl + (int)((long long)(zh - zl) * k / n_lean), b = zl + (int)((long long)(zh - zl) * (k + 1) / n_lean);
+      if (b > a) vl.push_back(make_int4(t, a, b, CP_LEAN));
+    }
+  std::unique_ptr<hz_coeffs::CpPlan> pl(new hz_coeffs::CpPlan);
+  pl->n_xy = (int)vxy.size();
+  pl->n_z = (int)vz.size();
+  pl->n_lean = (int)vl.size();
+  vxy.insert(vxy.end(), vz.begin(), vz.end());
+  vxy.insert(vxy.end(), vl.begin(), vl.end());
+  if (pl->work.ensure(std::max<size_t>(1, vxy.size()) * sizeof(int4)) != cudaSuccess) return nullptr;
+  if (!vxy.empty() && cudaMemcpy(pl->work.p, vxy.data(), vxy.size() * sizeof(int4), cudaMemcpyHostToDevice) != cudaSuccess)
+    return nullptr;
+  auto* raw = pl.get();
+  c->cp_plans[key] = std::move(pl);
+  return raw;
+}
+
+// complex64 launches go through apply27_cp: point the params at the work list for this RHS count
+template <typename R, typename S>
+hz_status cp_attach(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs) {
+  if (!(sizeof(R) == 4 && sizeof(S) == 4 && c->cp_on)) return HZ_OK;
+  const int nr = cp_group(nrhs), ng = (nrhs + nr - 1) / nr;
+  const hz_coeffs::CpPlan* pl = cp_plan(const_cast<hz_coeffs*>(c), ng, nr);
+  if (!pl) { set_error("cp_plan: device allocation / copy failed"); return HZ_ERR_CUDA; }
+  p.cp_work = pl->work.as<int4>();
+  p.cp_tx = c->cp_tx;
+  p.cp_ns = c->cp_ns;
+  p.cp_ntx = c->cp_ntx;
+  p.cp_nty = c->cp_nty;
+  p.cp_n_pml = pl->n_xy;
+  p.cp_n_pmlz = pl->n_z;
+  p.cp_n_int = pl->n_lean;
+  p.cp_nblocks = pl->n_xy + pl->n_z + pl->n_lean;
   return HZ_OK;
 }
 
@@ -651,6 +776,7 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
     c->zc = (int)((g->nz_local + nch - 1) / nch);
     c->nchunks = (g->nz_local + c->zc - 1) / c->zc;
   }
+  if (sizeof(R) == 4) HZ_TRY(cp_geometry(c.get()));
   if (n_clamped) *n_clamped = (long long)stats[1];
   *out = c.release();
   return stats[1] > 0 ? HZ_WARN_CLAMPED : HZ_OK;

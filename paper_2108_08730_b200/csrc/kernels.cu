@@ -10,6 +10,7 @@
 #include "apply.cuh"
 #include "apply27.cuh"
 #include "apply27_tma.cuh"
+#include "apply27_cp.cuh"
 #include "kernels.h"
 
 namespace hz {
@@ -464,8 +465,67 @@ static cudaError_t launch_tma(const ApplyParams<float, float>& p, long long nb, 
 static thread_local int g_last_apply_launches = 0;
 int apply_last_launches() { return g_last_apply_launches; }
 
+// complex64 RHS-fused launch: x/y-PML tiles, z-PML tiles, PML-free tiles (the work list in that
+// order); blockIdx.y = group of NR right-hand sides
+// rows per thread: 2 (256 threads) where the variant fits 128 registers without spilling, else 1
+// (512 threads): PML-free tiles of one RHS use 2, everything else 1
+template <int NR, int PM> struct CpNY { enum { V = (NR == 1 && PM == CP_LEAN) ? 2 : 1 }; };
+template <int NY, int NR, bool COLLOC, int EPI, int PM>
+static cudaError_t launch_cp_one(const ApplyParams<float, float>& p, int item0, int nitems, int ngroups,
+                                 cudaStream_t s) {
+  if (nitems <= 0) return cudaSuccess;
+  auto kern = apply27_cp<NY, NR, COLLOC, EPI, PM>;
+  const size_t smem = cp_smem_bytes(p.tab_n, p.cp_ns, NR);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  kern<<<dim3((unsigned)nitems, (unsigned)ngroups), CP_THREADS(NY), smem, s>>>(p, item0);
+  return cudaGetLastError();
+}
+
+template <int NR, bool COLLOC, int EPI>
+static cudaError_t launch_cp(const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
+  const int ngroups = (nrhs + NR - 1) / NR;
+  const int nxy = p.cp_n_pml, nz = p.cp_n_pmlz, nl = p.cp_n_int;
+  g_last_apply_launches = (nxy > 0) + (nz > 0) + (nl > 0);
+  cudaError_t e = launch_cp_one<CpNY<NR, CP_PMLXY>::V, NR, COLLOC, EPI, CP_PMLXY>(p, 0, nxy, ngroups, s);
+  if (e != cudaSuccess) return e;
+  e = launch_cp_one<CpNY<NR, CP_PMLZ>::V, NR, COLLOC, EPI, CP_PMLZ>(p, nxy, nz, ngroups, s);
+  if (e != cudaSuccess) return e;
+  return launch_cp_one<CpNY<NR, CP_LEAN>::V, NR, COLLOC, EPI, CP_LEAN>(p, nxy + nz, nl, ngroups, s);
+}
+
+#ifndef HZ_CP_NR
+#define HZ_CP_NR 2
+#endif
+int cp_group(int nrhs) { return nrhs == 1 ? 1 : HZ_CP_NR; }
+
+template <typename R, typename S>
+long long apply_slots(ApplyParams<R, S>& p) {
+  if constexpr (std::is_same<R, float>::value && std::is_same<S, float>::value) {
+#ifndef HZ_NO_CP
+    if (p.cp_work != nullptr) return p.cp_nblocks;
+#endif
+  }
+  return apply_plan(p);
+}
+template long long apply_slots<float, float>(ApplyParams<float, float>&);
+template long long apply_slots<double, double>(ApplyParams<double, double>&);
+template long long apply_slots<double, float>(ApplyParams<double, float>&);
+
 template <typename R, typename S, bool COLLOC, int EPI>
 static cudaError_t launch_apply_t(ApplyParams<R, S> p, int nrhs, cudaStream_t s) {
+  if constexpr (std::is_same<R, float>::value && std::is_same<S, float>::value && EPI != EPI_RESID) {
+#ifndef HZ_NO_CP
+    if (p.cp_work != nullptr) {
+      p.nrhs = nrhs;
+      return cp_group(nrhs) == 1 ? launch_cp<1, COLLOC, EPI>(p, nrhs, s) : launch_cp<HZ_CP_NR, COLLOC, EPI>(p, nrhs, s);
+    }
+#endif
+  }
   apply_plan(p);
   p.nrhs = nrhs;
   const long long ngen = (long long)p.gen_blocks * nrhs;
@@ -535,6 +595,21 @@ int apply_occupancy(bool colloc) {
 }
 template int apply_occupancy<float>(bool);
 template int apply_occupancy<double>(bool);
+
+template <int PM, int NR>
+static int cp_occ(int tab_n, int ns) {
+  constexpr int NY = CpNY<NR, PM>::V;
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_cp<NY, NR, false, EPI_DOT4, PM>, CP_THREADS(NY),
+                                                cp_smem_bytes(tab_n, ns, NR));
+  return nb > 0 ? nb : 1;
+}
+int cp_occupancy(int tab_n, int ns, int mode, int nr) {
+  if (nr == 1)
+    return mode == CP_PMLXY ? cp_occ<CP_PMLXY, 1>(tab_n, ns) : mode == CP_PMLZ ? cp_occ<CP_PMLZ, 1>(tab_n, ns) : cp_occ<CP_LEAN, 1>(tab_n, ns);
+  return mode == CP_PMLXY ? cp_occ<CP_PMLXY, HZ_CP_NR>(tab_n, ns)
+                          : mode == CP_PMLZ ? cp_occ<CP_PMLZ, HZ_CP_NR>(tab_n, ns) : cp_occ<CP_LEAN, HZ_CP_NR>(tab_n, ns);
+}
 
 template <typename R>
 cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s) {

@@ -4,6 +4,7 @@
 
 #include "apply.cuh"
 #include "apply27.cuh"
+#include "apply27_cp.cuh"
 
 namespace hz {
 
@@ -43,6 +44,9 @@ template <typename R> int apply_occupancy(bool colloc);
 int apply_last_launches();   // kernels launched by the last launch_apply on this thread (1 or 2)
 template <typename R> long long apply_nblocks_x(int nx, int ny);   // CTAs along x of one z-chunk
 template <typename R, typename S> long long apply_plan(ApplyParams<R, S>& p);   // CTAs per RHS, both launches
+template <typename R, typename S> long long apply_slots(ApplyParams<R, S>& p);  // dot partial slots per RHS
+int cp_group(int nrhs);                                                           // RHS per CTA (complex64)
+int cp_occupancy(int tab_n, int ns, int mode, int nr);   // CTAs/SM of a complex64 variant (4 dots)
 template <typename R, typename S>
 cudaError_t launch_apply(const ApplyParams<R, S>& p, int nrhs, bool colloc, int epi, cudaStream_t s);
 template <>

@@ -227,10 +227,10 @@ def test_domain_errors(hz, ctx, table):
 
 
 @pytest.mark.parametrize("mass", ["eq8", "colloc"])
-def test_apply_tma_box_tiles(hz, ctx, table, ga_table, mass):
-    """Grid whose PML-free box is wider than a bulk-copy (TMA) tile: odd nx (rows alternate 16-byte
-    alignment), clamped overlapping last tiles in x and y, 3 RHS — full oracle comparison (the interior
-    launch is apply27_tma here, the frame the general launch)."""
+def test_apply_tiled_launches(hz, ctx, table, ga_table, mass):
+    """complex64 tiled launches (x/y-PML tiles, z-PML tiles, PML-free tiles): odd nx (ragged tile width),
+    clamped overlapping last tiles in x and y, 3 RHS (one full RHS pair and a pair with one idle slot)
+    — full oracle comparison, every point individually."""
     rng = np.random.default_rng(77)
     nz, ny, nx, h, f, npml = 21, 27, 301, 20.0, 8.0, 4
     v = rng.uniform(1600.0, 4200.0, (nz, ny, nx))
@@ -238,7 +238,7 @@ def test_apply_tma_box_tiles(hz, ctx, table, ga_table, mass):
     C = assemble(hz, ctx, table, v, h, f, npml, "c64", mass=mass)
     l0 = hz.hz_kernel_launch_count()
     got = gpu_apply(hz, C, u)
-    assert hz.hz_kernel_launch_count() - l0 == 2          # general (frame) + interior (box) launches
+    assert hz.hz_kernel_launch_count() - l0 == 3          # one launch per tile class
     ref = op.apply(op.assemble(oracle_problem(v, h, f, npml, ga_table, "c64", mass=mass)), u)
     assert rel(got, ref) <= TOL["c64"], rel(got, ref)
     # every point checked individually as well (a missed or doubly-written tile would show locally)
