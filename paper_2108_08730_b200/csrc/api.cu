@@ -205,14 +205,13 @@ struct hz_coeffs {
   std::vector<std::complex<double>> am_h[3], ap_h[3];  // host copies for export
   DBuf partials, tickets;      // apply epilogue scratch
   int zc = 1, nchunks = 1;
-  // complex64 RHS-fused apply: tile geometry, and per number of RHS groups a work list
-  // {tile, z0, z1, mode} (x/y-PML items, then z-PML, then PML-free), built on first use
+  // complex64 RHS-fused apply: per (RHS groups, RHS per CTA) a work list of cp_items (x/y-PML tiles
+  // first), built on first use
   struct CpPlan {
     DBuf work;
-    int n_xy = 0, n_z = 0, n_lean = 0;
+    int n_xy = 0, n_in = 0;
   };
   bool cp_on = false;
-  int cp_tx = 0, cp_ns = 0, cp_ntx = 0, cp_nty = 0;
   std::map<int, std::unique_ptr<CpPlan>> cp_plans;
   std::unique_ptr<SolverWork> work;
   size_t esz() const { return dtype == HZ_C64 ? 4 : 8; }   // real element size
@@ -445,91 +444,91 @@ hz_status apply_launch(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs, int e
   return HZ_OK;
 }
 
-// Tile geometry of the complex64 RHS-fused apply (apply27_cp): tx ≤ 64 columns with ntx = ⌈nx/64⌉
-// tiles per row (tx = ⌈nx/ntx⌉, the last tile clamped inside the grid), 2·ns rows with tx·ns ≤ 256.
+// Work lists of the complex64 RHS-fused apply (apply27_cp).  Each axis is cut into bands — the PML
+// slab below, the interior [lo, hi], the PML slab above — and each x/y band rectangle is tiled on its
+// own (tx ≤ 64, tx·ty ≤ 256·NY, (tx+2)(ty+2) ≤ CP_HALO, ty even; the last tile of a band overlaps
+// its neighbour and stores only its own points), so a tile is either wholly in the x/y-PML or wholly
+// outside it (its body then only carries the plane-uniform z-PML corrections).  Tiles march the
+// slab in z-chunks whose count balances the launch over whole waves of resident CTAs (SMs × CTAs/SM)
+// against the 2 extra halo planes a chunk reads (env HZ_CP_ZC forces a chunk length).
+struct CpBand { int a, b; bool pml; };
+static std::vector<CpBand> cp_bands(int n, int lo, int hi) {
+  std::vector<CpBand> v;
+  if (hi < lo) return {{0, n, true}};
+  if (lo > 0) v.push_back({0, lo, true});
+  v.push_back({lo, hi + 1, false});
+  if (hi + 1 < n) v.push_back({hi + 1, n, true});
+  return v;
+}
+struct CpTile { int x0, y0, tx, ty, xs, ys, xe, ye; };
+static void cp_tile_rect(int xa, int xb, int ya, int yb, int maxpts, std::vector<CpTile>& out) {
+  const int w = xb - xa, h = yb - ya;
+  const int ntx = (w + 63) / 64, tx = (w + ntx - 1) / ntx;
+  int tymax = std::min(64, maxpts / tx);
+  while (tymax > 2 && (tx + 2) * (tymax + 2) > CP_HALO) tymax--;
+  tymax = std::max(2, tymax & ~1);
+  int nty = (h + tymax - 1) / tymax;
+  int ty = (h + nty - 1) / nty;
+  ty = std::min(tymax, ty + (ty & 1));
+  nty = (h + ty - 1) / ty;
+  for (int j = 0; j < nty; j++)
+    for (int i = 0; i < ntx; i++) {
+      CpTile t;
+      t.xs = xa + i * tx;
+      t.xe = std::min(t.xs + tx, xb);
+      t.x0 = std::min(t.xs, xb - tx);
+      t.ys = ya + j * ty;
+      t.ye = std::min(t.ys + ty, yb);
+      t.y0 = std::max(0, std::min(t.ys, yb - ty));
+      t.tx = tx;
+      t.ty = ty;
+      out.push_back(t);
+    }
+}
+
 hz_status cp_geometry(hz_coeffs* c) {
-  const int nx = c->grid.nx, ny = c->grid.ny;
-  const int ntx = (nx + 63) / 64;
-  const int tx = (nx + ntx - 1) / ntx;
-  int ns = std::min(CP_NSMAX, CP_NT / tx);
-  ns = std::max(1, std::min(ns, ny / 2));
-  if ((2 * ns + 2) * (tx + 2) > CP_KS * CP_NT) { set_error("cp_geometry: tile too large"); return HZ_ERR_INVALID_ARG; }
-  c->cp_tx = tx;
-  c->cp_ns = ns;
-  c->cp_ntx = ntx;
-  c->cp_nty = (ny + 2 * ns - 1) / (2 * ns);
+  const hz_grid& g = c->grid;
+  if (g.nx > 65535 || g.ny > 65535 || g.nz_local > 65535) { c->cp_on = false; return HZ_OK; }   // item packing
   c->cp_on = getenv("HZ_NO_CP") == nullptr;
   return HZ_OK;
 }
 
-// Work list for `ngroups` RHS groups.  A tile with x/y-PML outputs marches the whole slab (its list is
-// x/y); the others are split at the z-PML boundaries into z-PML items (the planes below / above) and
-// PML-free items.  Each list's z-segments are cut into chunks whose count balances the list over
-// whole waves of resident CTAs (SMs × CTAs/SM of that variant) against the 2 extra halo planes a
-// chunk reads (env HZ_CP_ZC forces a chunk length).
 const hz_coeffs::CpPlan* cp_plan(hz_coeffs* c, int ngroups, int nr) {
   const int key = ngroups * 8 + nr;
   auto it = c->cp_plans.find(key);
   if (it != c->cp_plans.end()) return it->second.get();
   const hz_grid& g = c->grid;
-  const int nx = g.nx, ny = g.ny, nzl = g.nz_local;
-  const int tx = c->cp_tx, TY = 2 * c->cp_ns, ntx = c->cp_ntx, ntiles = ntx * c->cp_nty;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->ctx->device);
-  int force = 0;
-  if (const char* e = getenv("HZ_CP_ZC")) force = atoi(e);
-  // number of chunks of a segment of `len` planes shared by `nt` tiles
-  auto nchunks = [&](int nt, int len, int mode) {
-    if (len <= 0 || nt <= 0) return 1;
-    if (force > 0) return std::max(1, (len + force - 1) / force);
-    const double slots = (double)sms * cp_occupancy(c->tab_n, c->cp_ns, mode, nr);
-    int best = 1;
+  const int nzl = g.nz_local;
+  std::vector<CpTile> xy, in;
+  for (const CpBand& by : cp_bands(g.ny, c->lo[1], c->hi[1]))
+    for (const CpBand& bx : cp_bands(g.nx, c->lo[0], c->hi[0]))
+      cp_tile_rect(bx.a, bx.b, by.a, by.b, CP_TILE_PTS(cp_rows(nr)), (bx.pml || by.pml) ? xy : in);
+  int nch = 1;
+  if (const char* e = getenv("HZ_CP_ZC")) nch = std::max(1, (nzl + std::max(1, atoi(e)) - 1) / std::max(1, atoi(e)));
+  else {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->ctx->device);
+    const double slots = (double)sms * cp_occupancy(c->tab_n, nr);
+    const double nt = (double)(xy.size() + in.size());
     double best_eff = -1;
-    for (int n = 1; n <= std::max(1, len / 4); n++) {
-      const double waves = (double)nt * n * ngroups / slots;
-      const double L = (double)len / n;
+    for (int n = 1; n <= std::max(1, nzl / 4); n++) {
+      const double waves = nt * n * ngroups / slots;
+      const double L = (double)nzl / n;
       const double eff = waves / std::ceil(waves) * L / (L + 2.0);
-      if (eff > best_eff + 1e-9) { best_eff = eff; best = n; }
+      if (eff > best_eff + 1e-9) { best_eff = eff; nch = n; }
     }
-    return best;
-  };
-  auto cut = [](std::vector<int4>& v, int t, int a, int b, int n, int mode) {
-    if (b <= a) return;
-    n = std::min(n, b - a);
-    for (int k = 0; k < n; k++)
-      v.push_back(make_int4(t, a + (int)((long long)(b - a) * k / n), a + (int)((long long)(b - a) * (k + 1) / n), mode));
-  };
-  const int zl = std::min(std::max(c->lo[2] - g.z0, 0), nzl);
-  const int zh = std::min(std::max(c->hi[2] - g.z0 + 1, zl), nzl);
-  std::vector<int> xy_tiles, in_tiles;
-  for (int t = 0; t < ntiles; t++) {
-    const int X0 = std::min((t % ntx) * tx, nx - tx), Y0 = std::min((t / ntx) * TY, ny - TY);
-    const bool xy = X0 < c->lo[0] || X0 + tx - 1 > c->hi[0] || Y0 < c->lo[1] || Y0 + TY - 1 > c->hi[1];
-    (xy ? xy_tiles : in_tiles).push_back(t);
   }
-  const int n_xy = nchunks((int)xy_tiles.size(), nzl, CP_PMLXY);
-  const int n_lean = nchunks((int)in_tiles.size(), zh - zl, CP_LEAN);
-  std::vector<int4> vxy, vz, vl;
-  for (int k = 0; k < n_xy; k++)   // chunk-major: concurrently running CTAs share z-planes in L2
-    for (int t : xy_tiles) {
-      const int a = (int)((long long)nzl * k / n_xy), b = (int)((long long)nzl * (k + 1) / n_xy);
-      if (b > a) vxy.push_back(make_int4(t, a, b, CP_PMLXY));
-    }
-  for (int t : in_tiles) {
-    cut(vz, t, 0, zl, 1, CP_PMLZ);
-    cut(vz, t, zh, nzl, 1, CP_PMLZ);
+  std::vector<int4> vxy, vin;
+  for (int k = 0; k < nch; k++) {   // chunk-major: concurrently running CTAs share z-planes in L2
+    const int a = (int)((long long)nzl * k / nch), b = (int)((long long)nzl * (k + 1) / nch);
+    if (b <= a) continue;
+    for (const CpTile& t : xy) vxy.push_back(cp_item(t.x0, t.y0, t.tx, t.ty, t.xs, t.ys, t.xe, t.ye, a, b, CP_PMLXY));
+    for (const CpTile& t : in) vin.push_back(cp_item(t.x0, t.y0, t.tx, t.ty, t.xs, t.ys, t.xe, t.ye, a, b, CP_PMLZ));
   }
-  for (int k = 0; k < n_lean; k++)
-    for (int t : in_tiles) {
-      const int a = zl + (int)((long long)(zh - zl) * k / n_lean), b = zl + (int)((long long)(zh - zl) * (k + 1) / n_lean);
-      if (b > a) vl.push_back(make_int4(t, a, b, CP_LEAN));
-    }
   std::unique_ptr<hz_coeffs::CpPlan> pl(new hz_coeffs::CpPlan);
   pl->n_xy = (int)vxy.size();
-  pl->n_z = (int)vz.size();
-  pl->n_lean = (int)vl.size();
-  vxy.insert(vxy.end(), vz.begin(), vz.end());
-  vxy.insert(vxy.end(), vl.begin(), vl.end());
+  pl->n_in = (int)vin.size();
+  vxy.insert(vxy.end(), vin.begin(), vin.end());
   if (pl->work.ensure(std::max<size_t>(1, vxy.size()) * sizeof(int4)) != cudaSuccess) return nullptr;
   if (!vxy.empty() && cudaMemcpy(pl->work.p, vxy.data(), vxy.size() * sizeof(int4), cudaMemcpyHostToDevice) != cudaSuccess)
     return nullptr;
@@ -546,14 +545,9 @@ hz_status cp_attach(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs) {
   const hz_coeffs::CpPlan* pl = cp_plan(const_cast<hz_coeffs*>(c), ng, nr);
   if (!pl) { set_error("cp_plan: device allocation / copy failed"); return HZ_ERR_CUDA; }
   p.cp_work = pl->work.as<int4>();
-  p.cp_tx = c->cp_tx;
-  p.cp_ns = c->cp_ns;
-  p.cp_ntx = c->cp_ntx;
-  p.cp_nty = c->cp_nty;
   p.cp_n_pml = pl->n_xy;
-  p.cp_n_pmlz = pl->n_z;
-  p.cp_n_int = pl->n_lean;
-  p.cp_nblocks = pl->n_xy + pl->n_z + pl->n_lean;
+  p.cp_n_int = pl->n_in;
+  p.cp_nblocks = pl->n_xy + pl->n_in;
   return HZ_OK;
 }
 

@@ -68,12 +68,10 @@ struct ApplyParams {
   // general launch work list per RHS: the boundary z-chunks (low, high) × all warps (nbx CTAs each),
   // then the interior z-chunks × the "frame" of warps outside the box (nbx_frame CTAs each)
   int nbound, nbx_frame, frame_warps, gen_blocks;
-  // complex64 RHS-fused launch (apply27_cp): tiles of cp_tx columns × 2·cp_ns rows (cp_ntx × cp_nty of
-  // them, the last of each row/column clamped inside the grid); work items {tile, z0, z1, mode} — first
-  // cp_n_pml with x/y-PML outputs, then cp_n_pmlz with z-PML outputs only, then cp_n_int without;
-  // cp_nblocks = dot partial slots per RHS
+  // complex64 RHS-fused launch (apply27_cp): work items (cp_item) — first cp_n_pml x/y-PML tiles,
+  // then cp_n_int tiles outside the x/y-PML; cp_nblocks = dot partial slots per RHS
   const int4* cp_work;
-  int cp_tx, cp_ns, cp_ntx, cp_nty, cp_n_pml, cp_n_pmlz, cp_n_int, cp_nblocks;
+  int cp_n_pml, cp_n_int, cp_nblocks;
   const S* v;                 // [nzl+2][ny][nx] velocity incl. halo planes
   const S* w;                 // [nzl+2][ny][nx] 1/v² incl. halo planes (apply input)
   const R* ctab;              // [n_g][CTAB_STRIDE] pre-scaled class coefficients + differences

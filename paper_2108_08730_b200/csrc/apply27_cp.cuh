@@ -4,17 +4,19 @@
 // App. A.5; PML per-axis corrections, reading A8), organised for the BiCGSTAB regime — several RHS,
 // grids of ~10⁶ points, 40% of them in the PML — where the register-path launches were latency bound
 // (12 warps/SM, one plane of loads in flight) and recomputed the coefficients once per RHS:
-//  * One CTA (8 warps) owns a tile of tx × (2·ns) output columns/rows (tx ≤ 64, chosen per grid so
-//    that tx·ns ≈ 256 threads: no idle lanes for ragged nx such as 101) for NR right-hand sides and
-//    marches a z-chunk.  Thread t owns column t % tx and the 2 rows of strip t / tx.
+//  * One CTA owns a tile of tx × ty output columns/rows (tx ≤ 64, tx·ty ≤ 512: 512/NY threads, each
+//    owning column t % tx and NY rows of strip t / tx; no idle lanes for ragged widths such as 101)
+//    for NR right-hand sides and marches a z-chunk.  The host cuts the grid into x/y bands — the PML
+//    slabs of each axis and the interior — and tiles each band separately, so a tile is either wholly
+//    in the x/y-PML or wholly outside it.
 //  * Each plane's w tile and the NR u tiles (+1 halo row/column) are copied global → shared by
 //    cp.async (4/8-byte, zero-filled outside the grid: the Dirichlet boundary costs no branch) into a
 //    ring of HZ_CP_STAGES planes; two planes are in flight while one is consumed.
 //  * Per plane and point the coefficients (table interpolation, PML transverse weights) are computed
 //    once and used for all NR fields; per field the 9 in-plane neighbours come from shared memory.
-//  * Two instantiations: PML = true for tiles with any output point in the PML (warp-uniform x / y /
-//    plane-uniform z corrections, exactly the register path's), PML = false for the rest.  A
-//    correction with δ = 0 adds exact zeros, so both compute bitwise the same value for a point.
+//  * Three instantiations: x/y-PML tiles (x / y corrections in warp-uniform branches plus the plane-
+//    uniform z corrections, the register path's A8 form), z-PML-only tiles, PML-free tiles.  A
+//    correction with δ = 0 adds exact zeros, so all compute bitwise the same value for a point.
 //  * Dot epilogues accumulate per thread in fp32 (HZ_CP_DOT_F64 = 1: fp64 as the register path) and
 //    reduce per block and grid in fp64 in a fixed order.
 #pragma once
@@ -25,15 +27,14 @@
 
 namespace hz {
 
-// Tile geometry is shared by all variants: tx ≤ 64 columns × TY = 2·ns rows with tx·ns ≤ 256.  A
-// variant with NY rows per thread runs CP_THREADS(NY) = 512/NY threads; the halo tile
-// (TY + 2)·(tx + 2) ≤ 768 elements is copied with CP_SLOTS(NY) elements per thread.
-constexpr int CP_NT = 256;        // positions (column, 2-row strip) per tile
-constexpr int CP_PMAX = 66;       // shared row pitch (elements): tx ≤ 64 + 2 halo columns
-constexpr int CP_NSMAX = 16;      // strips per tile (TY ≤ 32)
-constexpr int CP_KS = 3;          // (2·ns + 2)·(tx + 2) ≤ CP_KS·CP_NT
-__host__ __device__ constexpr int CP_THREADS(int ny) { return 512 / ny; }
-__host__ __device__ constexpr int CP_SLOTS(int ny) { return (CP_KS * CP_NT + CP_THREADS(ny) - 1) / CP_THREADS(ny); }
+// A CTA has CP_THREADS = 256 threads; with NY rows per thread its tile is tx × ty points (tx ≤ 64,
+// tx·ty ≤ 256·NY, (tx+2)·(ty+2) ≤ CP_HALO, ty even), the halo tile copied with CP_SLOTS elements
+// per thread.  Shared rows have pitch tx + 2.
+constexpr int CP_NTHR = 256;
+constexpr int CP_HALO = 768;
+__host__ __device__ constexpr int CP_THREADS(int) { return CP_NTHR; }
+__host__ __device__ constexpr int CP_TILE_PTS(int ny) { return CP_NTHR * ny; }
+__host__ __device__ constexpr int CP_SLOTS(int) { return (CP_HALO + CP_NTHR - 1) / CP_NTHR; }
 // PML mode of a work item: 0 none, 1 z-PML output planes only, 2 x/y-PML columns/rows (+ z)
 enum { CP_LEAN = 0, CP_PMLZ = 1, CP_PMLXY = 2 };
 #ifndef HZ_CP_STAGES
@@ -53,12 +54,17 @@ constexpr int CP_STAGES = HZ_CP_STAGES;
 #define HZ_CP_DOT_F64 0
 #endif
 
-// bytes of one ring stage: w rows then NR u tiles, ROWS = 2·ns + 2 rows of CP_PMAX elements
-__host__ __device__ constexpr size_t cp_stage_bytes(int ns, int nr) {
-  return (size_t)(2 * ns + 2) * CP_PMAX * (4 + 8 * nr);
+// bytes of one ring stage: the w halo tile then NR u halo tiles, CP_HALO elements each
+__host__ __device__ constexpr size_t cp_stage_bytes(int nr) { return (size_t)CP_HALO * (4 + 8 * nr); }
+__host__ __device__ constexpr size_t cp_smem_bytes(int tab_n, int nr) {
+  return (((size_t)tab_n * 12 * 4 + 127) / 128) * 128 + (size_t)CP_STAGES * cp_stage_bytes(nr);
 }
-__host__ __device__ constexpr size_t cp_smem_bytes(int tab_n, int ns, int nr) {
-  return (((size_t)tab_n * 12 * 4 + 127) / 128) * 128 + (size_t)CP_STAGES * cp_stage_bytes(ns, nr);
+// work item {x0 | y0 << 16, tx | ty << 8 | (xs − x0) << 16 | (ys − y0) << 24, z0 | z1 << 16,
+// (xe − x0) | (ye − y0) << 8 | mode << 16}: the tile computes [x0, x0+tx) × [y0, y0+ty) and stores
+// [xs, xe) × [ys, ye) (tiles overlap where a band is not a multiple of the tile), planes [z0, z1)
+__host__ __device__ inline int4 cp_item(int x0, int y0, int tx, int ty, int xs, int ys, int xe, int ye, int z0, int z1, int mode) {
+  return make_int4(x0 | (y0 << 16), tx | (ty << 8) | ((xs - x0) << 16) | ((ys - y0) << 24), z0 | (z1 << 16),
+                   (xe - x0) | ((ye - y0) << 8) | (mode << 16));
 }
 
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t n) {
@@ -93,9 +99,58 @@ __device__ __forceinline__ float2 zfma_c(float2 d, float2 dn, float2 b, float2 a
 }
 __device__ __forceinline__ float2 zneg_sw(float2 d) { return make_float2(-d.y, d.y); }
 
-// Work item: tile index (ty·ntx + tx), output planes [z0, z1) of the slab (local indices)
+// Dot epilogue reduction of one CTA for its NR right-hand sides (all K values at once, fixed order):
+// warp shuffles (fp64) → per-warp sums in shared memory → one thread per (RHS, value) writes the
+// block's partial; the last CTA of the RHS group (ticket of the group's first RHS) reduces the
+// partials of all CTAs with one warp per (RHS, value): lanes stride the blocks, then a shuffle tree.
+template <int NR, int K, int NT>
+__device__ __forceinline__ void cp_reduce(const DotT (&part)[NR][K], const bool (&act)[NR], const ApplyParams<float, float>& p,
+                                          int rhs0, int slot) {
+  constexpr int NWARP = NT / 32;
+  __shared__ double red[NWARP][NR * K];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblocks = p.cp_nblocks;
+#pragma unroll
+  for (int r = 0; r < NR; r++)
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      double v = (double)part[r][k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][r * K + k] = v;
+    }
+  __syncthreads();
+  if (threadIdx.x < NR * K) {
+    const int r = threadIdx.x / K, k = threadIdx.x - r * K;
+    if (act[r]) {
+      double v = 0.0;
+      for (int w = 0; w < NWARP; w++) v += red[w][threadIdx.x];
+      p.partials[((long long)(rhs0 + r) * nblocks + slot) * K + k] = v;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(p.tickets + rhs0, 1u) == (unsigned)nblocks - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int q = warp; q < NR * K; q += NWARP) {
+    const int r = q / K, k = q - r * K;
+    if (!act[r]) continue;
+    const volatile double* pp = p.partials + (long long)(rhs0 + r) * nblocks * K + k;
+    double v = 0.0;
+    for (int b = lane; b < nblocks; b += 32) v += pp[(long long)b * K];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) p.dots[(long long)(rhs0 + r) * K + k] = v;
+  }
+  if (threadIdx.x == 0) p.tickets[rhs0] = 0u;
+}
+
+// Work item: see cp_item (local plane indices)
 template <int NY, int NR, bool COLLOC, int EPI, int PM>
-__global__ void __launch_bounds__(CP_THREADS(NY), 512 / CP_THREADS(NY)) apply27_cp(ApplyParams<float, float> p, int item0) {
+__device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int item0) {
   typedef float R;
   typedef float2 C;
   constexpr bool PML = PM != CP_LEAN;
@@ -119,20 +174,21 @@ __global__ void __launch_bounds__(CP_THREADS(NY), 512 / CP_THREADS(NY)) apply27_
   if (!any) return;   // uniform per CTA
 
   const int nx = p.nx, ny = p.ny;
-  const int tx = p.cp_tx, ns = p.cp_ns, TY = 2 * ns, ROWS = TY + 2;
-  const int ttx = item.x % p.cp_ntx, tty = item.x / p.cp_ntx;
-  const int X0n = ttx * tx, Y0n = tty * TY;
-  const int X0 = min(X0n, nx - tx), Y0 = min(Y0n, ny - TY);   // clamped tiles (overlap, not stored twice)
-  const int zc0 = item.y, zc1 = item.z;
+  const int X0 = item.x & 0xffff, Y0 = item.x >> 16;
+  const int tx = item.y & 0xff, TY = (item.y >> 8) & 0xff;
+  const int X0n = X0 + ((item.y >> 16) & 0xff), Y0n = Y0 + (item.y >> 24);
+  const int X1n = X0 + (item.w & 0xff), Y1n = Y0 + ((item.w >> 8) & 0xff);
+  const int ROWS = TY + 2, P = tx + 2;   // halo tile rows, shared row pitch
+  const int zc0 = item.z & 0xffff, zc1 = item.z >> 16;
   const int nplanes = zc1 - zc0 + 2;   // input planes zc0-1 .. zc1
   const int plane = (int)p.plane;      // host: (nzl + 2)·plane < 2^31 (32-bit offsets within a field)
 
   extern __shared__ __align__(1024) unsigned char smem_cp[];
   float* stab = reinterpret_cast<float*>(smem_cp);
   unsigned char* ring = smem_cp + (((size_t)p.tab_n * 12 * 4 + 127) / 128) * 128;
-  const uint32_t stage_bytes = (uint32_t)cp_stage_bytes(ns, NR);
-  const uint32_t wbytes = (uint32_t)ROWS * CP_PMAX * 4;   // w rows of a stage; the u tiles follow
-  const uint32_t ubytes = (uint32_t)ROWS * CP_PMAX * 8;
+  const uint32_t stage_bytes = (uint32_t)cp_stage_bytes(NR);
+  const uint32_t wbytes = (uint32_t)CP_HALO * 4;   // w halo tile of a stage; the u tiles follow
+  const uint32_t ubytes = (uint32_t)CP_HALO * 8;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
 
   // ---- copy slots: element e = tid + k·NT of the (ROWS × (tx+2)) halo tile.  Elements outside the
@@ -144,10 +200,10 @@ __global__ void __launch_bounds__(CP_THREADS(NY), 512 / CP_THREADS(NY)) apply27_
 #pragma unroll
   for (int k = 0; k < KS; k++) {
     const int e = tid + k * NT;
-    const int r = e / (tx + 2), cc = e - r * (tx + 2);
+    const int r = e / P, cc = e - r * P;
     const int gx = X0 - 1 + cc, gy = Y0 - 1 + r;
     const bool in_tile = r < ROWS;
-    sdst[k] = in_tile ? 4u * (uint32_t)(r * CP_PMAX + cc) : ~0u;
+    sdst[k] = in_tile ? 4u * (uint32_t)e : ~0u;
     gin[k] = in_tile && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
     goff[k] = gin[k] ? gy * nx + gx : 0;
   }
@@ -185,11 +241,11 @@ __global__ void __launch_bounds__(CP_THREADS(NY), 512 / CP_THREADS(NY)) apply27_
   const int s_ = pt / tx, c_ = pt - s_ * tx;
   const int x = X0 + c_;
   const int yl0 = Y0 + NY * s_;
-  const bool x_ok = pos_ok && x >= X0n;
-  const int sbase = (NY * s_) * CP_PMAX + c_;   // stage element of (row y0-1, column x-1)
+  const bool x_ok = pos_ok && x >= X0n && x < X1n;
+  const int sbase = (NY * s_) * P + c_;   // stage element of (row y0-1, column x-1)
   bool st_ok[NY];
 #pragma unroll
-  for (int i = 0; i < NY; i++) st_ok[i] = x_ok && yl0 + i >= Y0n;
+  for (int i = 0; i < NY; i++) st_ok[i] = x_ok && yl0 + i >= Y0n && yl0 + i < Y1n;
 
   // PML deltas of this thread's column / rows (warp-uniform use); dn = (−δ.y, δ.y)
   bool gen_x = false, gen_y = false;
@@ -278,16 +334,16 @@ __global__ void __launch_bounds__(CP_THREADS(NY), 512 / CP_THREADS(NY)) apply27_
     float wa[NY + 2], w0[NY + 2], wb[NY + 2];
 #pragma unroll
     for (int r = 0; r < NY + 2; r++) {
-      wa[r] = sw[r * CP_PMAX];
-      w0[r] = sw[r * CP_PMAX + 1];
-      wb[r] = sw[r * CP_PMAX + 2];
+      wa[r] = sw[r * P];
+      w0[r] = sw[r * P + 1];
+      wb[r] = sw[r * P + 2];
     }
     // ---- coefficients of the output rows of plane pl+1 (w from the next stage) into the free slot
     {
       const float* swn = reinterpret_cast<const float*>(ring + (size_t)((j + 1) % S) * stage_bytes) + sbase;
 #pragma unroll
       for (int i = 0; i < NY; i++) {
-        const R wn = do_next ? swn[(1 + i) * CP_PMAX + 1] : R(1);
+        const R wn = do_next ? swn[(1 + i) * P + 1] : R(1);
         const R vv = rsqrt_r(wn);
         R sidx = fma(vv, s_k1, s_k0);
         sidx = fmin(fmax(sidx, R(0)), s_max);
@@ -327,7 +383,7 @@ __global__ void __launch_bounds__(CP_THREADS(NY), 512 / CP_THREADS(NY)) apply27_
       C X[NY + 2], q[NY + 2], Xq[NY + 2], U[NY + 2];
 #pragma unroll
       for (int k = 0; k < NY + 2; k++) {
-        const C a = su[k * CP_PMAX], u0 = su[k * CP_PMAX + 1], b = su[k * CP_PMAX + 2];
+        const C a = su[k * P], u0 = su[k * P + 1], b = su[k * P + 2];
         U[k] = u0;
         X[k] = cadd(a, b);
         if (!COLLOC) {
@@ -373,10 +429,10 @@ __global__ void __launch_bounds__(CP_THREADS(NY), 512 / CP_THREADS(NY)) apply27_
             // ΔL1 = δx(u) + δy(u), ΔL2 = δx(Y) + δy(X) (A8); x-neighbour columns from shared memory
             C L1 = make_float2(0.f, 0.f), L2 = L1;
             if (gen_x) {
-              const C YL = cadd(su[i * CP_PMAX], su[(i + 2) * CP_PMAX]);
-              const C YR = cadd(su[i * CP_PMAX + 2], su[(i + 2) * CP_PMAX + 2]);
-              L1 = zfma_c(dxm, dxmn, csub(su[(i + 1) * CP_PMAX], u0), L1);
-              L1 = zfma_c(dxp, dxpn, csub(su[(i + 1) * CP_PMAX + 2], u0), L1);
+              const C YL = cadd(su[i * P], su[(i + 2) * P]);
+              const C YR = cadd(su[i * P + 2], su[(i + 2) * P + 2]);
+              L1 = zfma_c(dxm, dxmn, csub(su[(i + 1) * P], u0), L1);
+              L1 = zfma_c(dxp, dxpn, csub(su[(i + 1) * P + 2], u0), L1);
               L2 = zfma_c(dxm, dxmn, csub(YL, Y), L2);
               L2 = zfma_c(dxp, dxpn, csub(YR, Y), L2);
             }
@@ -445,30 +501,28 @@ __global__ void __launch_bounds__(CP_THREADS(NY), 512 / CP_THREADS(NY)) apply27_
     for (int r = 0; r < NR; r++) as0[r][i] = as1[r][i] = as2[r][i] = ss0[r][i] = ss1[r][i] = ss2[r][i] = make_float2(0.f, 0.f);
   }
   // roles (prev, cur, next) = (0,1,2), (1,2,0), (2,0,1); the s slots (prev, cur) rotate likewise
-  int j = 0;
-  for (; j + 2 < nplanes; j += 3) {
+  // (the ragged end is guarded inside the loop: three body copies, not five — instruction cache)
+  for (int j = 0; j < nplanes; j += 3) {
     body(cs0, cs1, cs2, ms0, ms1, ms2, as0, as1, as2, ss0, ss1, j);
+    if (j + 1 >= nplanes) break;
     body(cs1, cs2, cs0, ms1, ms2, ms0, as1, as2, as0, ss1, ss2, j + 1);
+    if (j + 2 >= nplanes) break;
     body(cs2, cs0, cs1, ms2, ms0, ms1, as2, as0, as1, ss2, ss0, j + 2);
   }
-  if (j < nplanes) body(cs0, cs1, cs2, ms0, ms1, ms2, as0, as1, as2, ss0, ss1, j);
-  if (j + 1 < nplanes) body(cs1, cs2, cs0, ms1, ms2, ms0, as1, as2, as0, ss1, ss2, j + 1);
   cp_wait<0>();
 
-  if (K > 0) {
-    const int nblocks = p.cp_nblocks;
-    const int slot = item0 + blockIdx.x;
-#pragma unroll
-    for (int r = 0; r < NR; r++) {
-      if (!act[r]) continue;   // uniform
-      double pd[K > 0 ? K : 1];
-#pragma unroll
-      for (int k = 0; k < K; k++) pd[k] = (double)part[r][k];
-      const int rr = rhs0 + r;
-      block_grid_reduce<K, NT>(pd, p.partials + (long long)rr * nblocks * K, p.dots + (long long)rr * K,
-                               p.tickets + rr, nblocks, slot);
-    }
-  }
+  if constexpr (K > 0) cp_reduce<NR, K, NT>(part, act, p, rhs0, item0 + blockIdx.x);
+}
+
+// One launch for every tile class: the work item's mode selects the x/y-PML body or the body with the
+// plane-uniform z corrections only (which costs no more than a PML-free body on non-PML planes), so
+// CTAs of both classes share the GPU; x/y-PML items come first (heavier, scheduled first).
+template <int NY, int NR, bool COLLOC, int EPI>
+__global__ void __launch_bounds__(CP_NTHR, 2) apply27_cp(ApplyParams<float, float> p, int item0) {
+  if ((p.cp_work[item0 + blockIdx.x].w >> 16) == CP_PMLXY)
+    cp_body<NY, NR, COLLOC, EPI, CP_PMLXY>(p, item0);
+  else
+    cp_body<NY, NR, COLLOC, EPI, CP_PMLZ>(p, item0);
 }
 
 }  // namespace hz

@@ -465,43 +465,38 @@ static cudaError_t launch_tma(const ApplyParams<float, float>& p, long long nb, 
 static thread_local int g_last_apply_launches = 0;
 int apply_last_launches() { return g_last_apply_launches; }
 
-// complex64 RHS-fused launch: x/y-PML tiles, z-PML tiles, PML-free tiles (the work list in that
-// order); blockIdx.y = group of NR right-hand sides
-// rows per thread: 2 (256 threads) where the variant fits 128 registers without spilling, else 1
-// (512 threads): PML-free tiles of one RHS use 2, everything else 1
-template <int NR, int PM> struct CpNY { enum { V = (NR == 1 && PM == CP_LEAN) ? 2 : 1 }; };
-template <int NY, int NR, bool COLLOC, int EPI, int PM>
-static cudaError_t launch_cp_one(const ApplyParams<float, float>& p, int item0, int nitems, int ngroups,
-                                 cudaStream_t s) {
+// complex64 RHS-fused launch: one launch over the work list (x/y-PML items, then the rest);
+// blockIdx.y = group of NR right-hand sides.  Rows per thread: 2 for one RHS, else 1 so that the
+// two-RHS body fits 128 registers (2 CTAs of 256 threads per SM).
+#ifndef HZ_CP_NY1
+#define HZ_CP_NY1 2
+#endif
+template <int NR> struct CpNY { enum { V = NR == 1 ? HZ_CP_NY1 : 1 }; };
+
+template <int NR, bool COLLOC, int EPI>
+static cudaError_t launch_cp(const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
+  constexpr int NY = CpNY<NR>::V;
+  const int ngroups = (nrhs + NR - 1) / NR;
+  const int nitems = p.cp_n_pml + p.cp_n_int;
+  g_last_apply_launches = nitems > 0 ? 1 : 0;
   if (nitems <= 0) return cudaSuccess;
-  auto kern = apply27_cp<NY, NR, COLLOC, EPI, PM>;
-  const size_t smem = cp_smem_bytes(p.tab_n, p.cp_ns, NR);
+  auto kern = apply27_cp<NY, NR, COLLOC, EPI>;
+  const size_t smem = cp_smem_bytes(p.tab_n, NR);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  kern<<<dim3((unsigned)nitems, (unsigned)ngroups), CP_THREADS(NY), smem, s>>>(p, item0);
+  kern<<<dim3((unsigned)nitems, (unsigned)ngroups), CP_THREADS(NY), smem, s>>>(p, 0);
   return cudaGetLastError();
-}
-
-template <int NR, bool COLLOC, int EPI>
-static cudaError_t launch_cp(const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
-  const int ngroups = (nrhs + NR - 1) / NR;
-  const int nxy = p.cp_n_pml, nz = p.cp_n_pmlz, nl = p.cp_n_int;
-  g_last_apply_launches = (nxy > 0) + (nz > 0) + (nl > 0);
-  cudaError_t e = launch_cp_one<CpNY<NR, CP_PMLXY>::V, NR, COLLOC, EPI, CP_PMLXY>(p, 0, nxy, ngroups, s);
-  if (e != cudaSuccess) return e;
-  e = launch_cp_one<CpNY<NR, CP_PMLZ>::V, NR, COLLOC, EPI, CP_PMLZ>(p, nxy, nz, ngroups, s);
-  if (e != cudaSuccess) return e;
-  return launch_cp_one<CpNY<NR, CP_LEAN>::V, NR, COLLOC, EPI, CP_LEAN>(p, nxy + nz, nl, ngroups, s);
 }
 
 #ifndef HZ_CP_NR
 #define HZ_CP_NR 2
 #endif
 int cp_group(int nrhs) { return nrhs == 1 ? 1 : HZ_CP_NR; }
+int cp_rows(int nr) { return nr == 1 ? (int)CpNY<1>::V : (int)CpNY<HZ_CP_NR>::V; }
 
 template <typename R, typename S>
 long long apply_slots(ApplyParams<R, S>& p) {
@@ -596,20 +591,15 @@ int apply_occupancy(bool colloc) {
 template int apply_occupancy<float>(bool);
 template int apply_occupancy<double>(bool);
 
-template <int PM, int NR>
-static int cp_occ(int tab_n, int ns) {
-  constexpr int NY = CpNY<NR, PM>::V;
+template <int NR>
+static int cp_occ(int tab_n) {
+  constexpr int NY = CpNY<NR>::V;
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_cp<NY, NR, false, EPI_DOT4, PM>, CP_THREADS(NY),
-                                                cp_smem_bytes(tab_n, ns, NR));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_cp<NY, NR, false, EPI_DOT4>, CP_THREADS(NY),
+                                                cp_smem_bytes(tab_n, NR));
   return nb > 0 ? nb : 1;
 }
-int cp_occupancy(int tab_n, int ns, int mode, int nr) {
-  if (nr == 1)
-    return mode == CP_PMLXY ? cp_occ<CP_PMLXY, 1>(tab_n, ns) : mode == CP_PMLZ ? cp_occ<CP_PMLZ, 1>(tab_n, ns) : cp_occ<CP_LEAN, 1>(tab_n, ns);
-  return mode == CP_PMLXY ? cp_occ<CP_PMLXY, HZ_CP_NR>(tab_n, ns)
-                          : mode == CP_PMLZ ? cp_occ<CP_PMLZ, HZ_CP_NR>(tab_n, ns) : cp_occ<CP_LEAN, HZ_CP_NR>(tab_n, ns);
-}
+int cp_occupancy(int tab_n, int nr) { return nr == 1 ? cp_occ<1>(tab_n) : cp_occ<HZ_CP_NR>(tab_n); }
 
 template <typename R>
 cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s) {

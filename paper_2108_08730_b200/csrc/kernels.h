@@ -46,7 +46,9 @@ template <typename R> long long apply_nblocks_x(int nx, int ny);   // CTAs along
 template <typename R, typename S> long long apply_plan(ApplyParams<R, S>& p);   // CTAs per RHS, both launches
 template <typename R, typename S> long long apply_slots(ApplyParams<R, S>& p);  // dot partial slots per RHS
 int cp_group(int nrhs);                                                           // RHS per CTA (complex64)
-int cp_occupancy(int tab_n, int ns, int mode, int nr);   // CTAs/SM of a complex64 variant (4 dots)
+int cp_occupancy(int tab_n, int nr);
+int cp_rows(int nr);   // rows per thread (NY) of the complex64 apply for NR RHS per CTA
+   // CTAs/SM of the complex64 apply (NR RHS per CTA, 4 dots)
 template <typename R, typename S>
 cudaError_t launch_apply(const ApplyParams<R, S>& p, int nrhs, bool colloc, int epi, cudaStream_t s);
 template <>
