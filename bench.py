@@ -393,7 +393,7 @@ def run_hz(args):
         "status": int(st),
         "apply_kernel_gpts_s": pts_all / (ams_max * 1e-3) / 1e9 if ams_max > 0 else None,
         "apply_share_of_step": ams / tot_ms if tot_ms > 0 else None,
-        "roofline": {"bound": "hbm", "kernel": "apply27_kernel (fused a2-a6 + BiCGSTAB dot epilogues)",
+        "roofline": {"bound": "hbm", "kernel": "apply27_cp (RHS-fused coefficient build + 27-point apply + BiCGSTAB dot epilogues, a2-a6)",
                      "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None,
                      "traffic": (traffic if traffic is not None else None),
