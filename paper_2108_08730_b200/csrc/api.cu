@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "hz_debug.h"
 #include "hz_internal.h"
 #include "kernels.h"
 
@@ -470,6 +471,7 @@ static void cp_tile_rect(int xa, int xb, int ya, int yb, int maxpts, std::vector
   int nty = (h + tymax - 1) / tymax;
   int ty = (h + nty - 1) / nty;
   ty = std::min(tymax, ty + (ty & 1));
+  if (ty > h && h >= 2) ty = h & ~1;   // stay inside the band (a 1-row band borrows a neighbour row)
   nty = (h + ty - 1) / ty;
   for (int j = 0; j < nty; j++)
     for (int i = 0; i < ntx; i++) {
@@ -536,6 +538,32 @@ const hz_coeffs::CpPlan* cp_plan(hz_coeffs* c, int ngroups, int nr) {
   c->cp_plans[key] = std::move(pl);
   return raw;
 }
+
+}  // namespace
+
+extern "C" int hz_debug_plan_tiles(int nx, int ny, int lo_x, int hi_x, int lo_y, int hi_y, int rows_per_thread,
+                                   int* out, int max_tiles) {
+  if (nx < 3 || ny < 3 || nx > 65535 || ny > 65535 || (rows_per_thread != 1 && rows_per_thread != 2) ||
+      (max_tiles > 0 && out == nullptr))
+    return -1;
+  std::vector<CpTile> xy, in;
+  for (const CpBand& by : cp_bands(ny, lo_y, hi_y))
+    for (const CpBand& bx : cp_bands(nx, lo_x, hi_x))
+      cp_tile_rect(bx.a, bx.b, by.a, by.b, CP_TILE_PTS(rows_per_thread), (bx.pml || by.pml) ? xy : in);
+  int n = 0;
+  for (int cls = 0; cls < 2; cls++)
+    for (const CpTile& t : cls == 0 ? xy : in) {
+      if (n < max_tiles) {
+        int* o = out + 9 * n;
+        o[0] = t.x0; o[1] = t.y0; o[2] = t.tx; o[3] = t.ty; o[4] = t.xs; o[5] = t.ys; o[6] = t.xe; o[7] = t.ye;
+        o[8] = cls == 0 ? 1 : 0;
+      }
+      n++;
+    }
+  return n;
+}
+
+namespace {
 
 // complex64 launches go through apply27_cp: point the params at the work list for this RHS count
 template <typename R, typename S>

@@ -28,6 +28,17 @@ def test_exports_every_declared_symbol():
     assert set(names) == set(hz.EXPORTED)
 
 
+def test_exports_debug_hooks():
+    """include/hz_debug.h (test hooks, not the north-star ABI) is exported too."""
+    import ctypes
+    lib = ctypes.CDLL(hz._LIBPATH)
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "hz_debug.h")).read(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(hz_[a-z_0-9]+)\s*\(", src)))
+    assert names == ["hz_debug_plan_tiles"]
+    for n in names:
+        assert hasattr(lib, n), n
+
+
 def test_library_is_sm100a():
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", hz._LIBPATH],

@@ -2,6 +2,7 @@
 coefficient record, PML arrays, operator apply (several tiles + ragged tails, both precisions, both
 mass formulations, batched RHS), decomposition invariance, point sources, and sampled rows at the
 full BASELINE sizes in the launch configuration bench.py times."""
+import os
 import zlib
 
 import numpy as np
@@ -244,3 +245,22 @@ def test_apply_tiled_launches(hz, ctx, table, ga_table, mass):
     # every point checked individually as well (a missed or doubly-written tile would show locally)
     err = np.abs(got - ref) / (np.abs(ref) + 1e-3 * np.abs(ref).max())
     assert err.max() <= 1e-4, np.unravel_index(err.argmax(), err.shape)
+
+
+def test_apply_reference_path_c64(hz, ctx, table, ga_table):
+    """HZ_NO_CP=1 (read at assemble) routes complex64 through the register-path / bulk-copy kernels kept
+    as the A/B reference: same oracle parity as the default RHS-fused launch."""
+    rng = np.random.default_rng(78)
+    nz, ny, nx, h, f, npml = 19, 23, 301, 20.0, 8.0, 4
+    v = rng.uniform(1600.0, 4200.0, (nz, ny, nx))
+    u = synth.random_field((2, nz, ny, nx), seed=10)
+    os.environ["HZ_NO_CP"] = "1"
+    try:
+        C = assemble(hz, ctx, table, v, h, f, npml, "c64")
+    finally:
+        del os.environ["HZ_NO_CP"]
+    l0 = hz.hz_kernel_launch_count()
+    got = gpu_apply(hz, C, u)
+    assert hz.hz_kernel_launch_count() - l0 == 2          # general + bulk-copy interior launches
+    ref = op.apply(op.assemble(oracle_problem(v, h, f, npml, ga_table, "c64")), u)
+    assert rel(got, ref) <= TOL["c64"], rel(got, ref)
