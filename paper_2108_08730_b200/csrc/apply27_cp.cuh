@@ -67,11 +67,18 @@ __host__ __device__ inline int4 cp_item(int x0, int y0, int tx, int ty, int xs, 
                    (xe - x0) | ((ye - y0) << 8) | (mode << 16));
 }
 
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t n) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
+// 4 / 8-byte async copies global → shared; zfill = true writes zeros instead (src not read)
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, bool zfill) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n cp.async.ca.shared.global [%0], [%1], 4, p;\n}\n" ::"r"(dst),
+      "l"(src), "r"((int)zfill)
+      : "memory");
 }
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, uint32_t n) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool zfill) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n cp.async.ca.shared.global [%0], [%1], 8, p;\n}\n" ::"r"(dst),
+      "l"(src), "r"((int)zfill)
+      : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -192,40 +199,46 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
 
   // ---- copy slots: element e = tid + k·NT of the (ROWS × (tx+2)) halo tile.  Elements outside the
-  // grid copy 0 bytes (zero fill) from a valid address (element 0 of the same plane).
+  // grid copy 0 bytes (zero fill) from a valid address (element 0 of the same plane).  Addresses are a
+  // uniform base + an unsigned 32-bit element offset (host: fstride < 2^31, so r·fstride + offset < 2^32
+  // for the NR ≤ 2 fields of a group).
   const int tid = threadIdx.x;
   int goff[KS];        // in-plane element offset y·nx + x (0 outside the grid)
   uint32_t sdst[KS];   // byte offset of the w element in a stage (~0u: no element for this slot)
-  bool gin[KS];
+  bool gout[KS];       // element outside the grid: zero fill
 #pragma unroll
   for (int k = 0; k < KS; k++) {
     const int e = tid + k * NT;
     const int r = e / P, cc = e - r * P;
     const int gx = X0 - 1 + cc, gy = Y0 - 1 + r;
     const bool in_tile = r < ROWS;
+    const bool gin = in_tile && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
     sdst[k] = in_tile ? 4u * (uint32_t)e : ~0u;
-    gin[k] = in_tile && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
-    goff[k] = gin[k] ? gy * nx + gx : 0;
+    gout[k] = !gin;
+    goff[k] = gin ? gy * nx + gx : 0;
   }
-  const float2* ug[NR];
-#pragma unroll
-  for (int r = 0; r < NR; r++) ug[r] = p.u + (long long)(rhs0 + r) * p.fstride;
+  const uint32_t fs = (uint32_t)p.fstride;
+  const float2* __restrict__ ug0 = p.u + (long long)rhs0 * p.fstride;
+#ifndef HZ_CP_NO_OPAQUE
+  asm("mov.b64 %0, %0;" : "+l"(ug0));   // keep the group's base in a register (not re-derived per use)
+#endif
+  const float* __restrict__ wg = p.w;
   auto issue = [&](int j) {
     if (j < nplanes) {
       const int pl = zc0 - 1 + j;
       const int zg = p.z0 + pl;
-      const bool zin = zg >= 0 && zg < p.nzg;
+      const bool zout = !(zg >= 0 && zg < p.nzg);
       const int po = (pl + 1) * plane;
       const uint32_t st = ring_s + (uint32_t)(j % S) * stage_bytes;
 #pragma unroll
       for (int k = 0; k < KS; k++) {
         if (sdst[k] == ~0u) continue;
-        const bool ok = zin && gin[k];
-        const int o = goff[k] + po;
-        cp_async4(st + sdst[k], p.w + o, ok ? 4u : 0u);
+        const bool zf = zout || gout[k];
+        const uint32_t o = (uint32_t)(goff[k] + po);
+        cp_async4(st + sdst[k], wg + o, zf);
 #pragma unroll
         for (int r = 0; r < NR; r++)
-          if (act[r]) cp_async8(st + wbytes + (uint32_t)r * ubytes + 2u * sdst[k], ug[r] + o, ok ? 8u : 0u);
+          if (act[r]) cp_async8(st + wbytes + (uint32_t)r * ubytes + 2u * sdst[k], ug0 + (o + (uint32_t)r * fs), zf);
       }
     }
     cp_commit();
@@ -292,7 +305,13 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
     for (int k = 0; k < (K > 0 ? K : 1); k++) part[r][k] = DotT(0);
 
   // output / epilogue element of (row yl0, column x) in plane storage 0 of each RHS: + pl·plane
-  const long long orow = (long long)yl0 * nx + x;
+  const uint32_t orow = (uint32_t)(yl0 * nx + x);
+  const float2* __restrict__ rh0 = p.rhat + (long long)rhs0 * p.fstride;
+  float2* __restrict__ au0 = p.au + (long long)rhs0 * p.fstride;
+#ifndef HZ_CP_NO_OPAQUE
+  asm("mov.b64 %0, %0;" : "+l"(rh0));
+  asm("mov.b64 %0, %0;" : "+l"(au0));
+#endif
 
   // One input plane j (local pl = zc0-1+j).  Three register slots per quantity rotate through the
   // roles prev (output pl-1) / cur (output pl) / next (output pl+1) over three consecutive calls, so no
@@ -312,7 +331,7 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
       for (int i = 0; i < NY; i++) {
         e1[r][i] = make_float2(0.f, 0.f);
         if (K > 0 && act[r] && do_prev && st_ok[i])
-          e1[r][i] = ldg_c(p.rhat + (long long)(rhs0 + r) * p.fstride + orow + (oplane + i * nx));
+          e1[r][i] = ldg_c(rh0 + ((uint32_t)r * fs + orow + (uint32_t)(oplane + i * nx)));
       }
     // planes j and j+1 have landed (own copies), then every thread's copies; the slot of plane j-1
     // is free (all threads are past iteration j-1) and receives plane j+S-1
@@ -474,8 +493,7 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
         aN[r][i] = c;   // output pl+1: "cur" of the next call (a's slot is free after this call)
         if (EPI == EPI_DOT4) sC[r][i] = u0;   // s of output pl: "prev" s of the next call
         if (do_prev && st_ok[i]) {
-          const long long o = (long long)(rhs0 + r) * p.fstride + orow + (oplane + i * nx);
-          p.au[o] = a;
+          au0[(uint32_t)r * fs + orow + (uint32_t)(oplane + i * nx)] = a;
           if (EPI == EPI_DOT1) {
             cp_cdot(part[r][0], part[r][1], e1[r][i], a);
           } else if (EPI == EPI_DOT4) {
