@@ -520,13 +520,31 @@ const hz_coeffs::CpPlan* cp_plan(hz_coeffs* c, int ngroups, int nr) {
       if (eff > best_eff + 1e-9) { best_eff = eff; nch = n; }
     }
   }
-  std::vector<int4> vxy, vin;
+  // tiles outside the x/y-PML: the z-PML slabs [0, zl) and [zh, nzl) are items of their own (z-PML
+  // body), the planes between are cut like the x/y-PML tiles' slab (PML-free body)
+  const int zl = std::min(std::max(c->lo[2] - g.z0, 0), nzl);
+  const int zh = std::min(std::max(c->hi[2] - g.z0 + 1, zl), nzl);
+  const int nin = std::max(1, (int)std::lround((double)nch * (zh - zl) / std::max(1, nzl)));
+  auto item = [](const CpTile& t, int a, int b, int mode) {
+    return cp_item(t.x0, t.y0, t.tx, t.ty, t.xs, t.ys, t.xe, t.ye, a, b, mode);
+  };
+  std::vector<int4> vxy, vz, vin;
   for (int k = 0; k < nch; k++) {   // chunk-major: concurrently running CTAs share z-planes in L2
     const int a = (int)((long long)nzl * k / nch), b = (int)((long long)nzl * (k + 1) / nch);
-    if (b <= a) continue;
-    for (const CpTile& t : xy) vxy.push_back(cp_item(t.x0, t.y0, t.tx, t.ty, t.xs, t.ys, t.xe, t.ye, a, b, CP_PMLXY));
-    for (const CpTile& t : in) vin.push_back(cp_item(t.x0, t.y0, t.tx, t.ty, t.xs, t.ys, t.xe, t.ye, a, b, CP_PMLZ));
+    if (b > a)
+      for (const CpTile& t : xy) vxy.push_back(item(t, a, b, CP_PMLXY));
   }
+  for (const CpTile& t : in) {
+    if (zl > 0) vz.push_back(item(t, 0, zl, CP_PMLZ));
+    if (zh < nzl) vz.push_back(item(t, zh, nzl, CP_PMLZ));
+  }
+  for (int k = 0; k < nin; k++) {
+    const int a = zl + (int)((long long)(zh - zl) * k / nin), b = zl + (int)((long long)(zh - zl) * (k + 1) / nin);
+    if (b > a)
+      for (const CpTile& t : in) vin.push_back(item(t, a, b, CP_LEAN));
+  }
+  vz.insert(vz.end(), vin.begin(), vin.end());
+  vin.swap(vz);
   std::unique_ptr<hz_coeffs::CpPlan> pl(new hz_coeffs::CpPlan);
   pl->n_xy = (int)vxy.size();
   pl->n_in = (int)vin.size();

@@ -532,15 +532,19 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
   if constexpr (K > 0) cp_reduce<NR, K, NT>(part, act, p, rhs0, item0 + blockIdx.x);
 }
 
-// One launch for every tile class: the work item's mode selects the x/y-PML body or the body with the
-// plane-uniform z corrections only (which costs no more than a PML-free body on non-PML planes), so
-// CTAs of both classes share the GPU; x/y-PML items come first (heavier, scheduled first).
+// One launch for every tile class: the work item's mode selects the x/y-PML body, the body with the
+// plane-uniform z corrections (chunks touching the z-PML) or the PML-free body, so CTAs of all classes
+// share the GPU; x/y-PML items come first (heavier, scheduled first).  The PML-free body is a separate
+// instantiation because the mere presence of the z-PML code costs ~20% (registers / scheduling).
 template <int NY, int NR, bool COLLOC, int EPI>
 __global__ void __launch_bounds__(CP_NTHR, 2) apply27_cp(ApplyParams<float, float> p, int item0) {
-  if ((p.cp_work[item0 + blockIdx.x].w >> 16) == CP_PMLXY)
+  const int mode = p.cp_work[item0 + blockIdx.x].w >> 16;
+  if (mode == CP_PMLXY)
     cp_body<NY, NR, COLLOC, EPI, CP_PMLXY>(p, item0);
-  else
+  else if (mode == CP_PMLZ)
     cp_body<NY, NR, COLLOC, EPI, CP_PMLZ>(p, item0);
+  else
+    cp_body<NY, NR, COLLOC, EPI, CP_LEAN>(p, item0);
 }
 
 }  // namespace hz
