@@ -529,8 +529,13 @@ const hz_coeffs::CpPlan* cp_plan(hz_coeffs* c, int ngroups, int nr) {
     return cp_item(t.x0, t.y0, t.tx, t.ty, t.xs, t.ys, t.xe, t.ye, a, b, mode);
   };
   std::vector<int4> vxy, vz, vin;
-  for (int k = 0; k < nch; k++) {   // chunk-major: concurrently running CTAs share z-planes in L2
-    const int a = (int)((long long)nzl * k / nch), b = (int)((long long)nzl * (k + 1) / nch);
+  // x/y-PML tiles cost more per point: cut them into proportionally shorter chunks (HZ_CP_XYF, default
+  // 1.5) so their CTAs end with the others
+  double xyf = 1.5;
+  if (const char* e = getenv("HZ_CP_XYF")) xyf = atof(e);
+  const int nxy = std::max(1, std::min(std::max(1, nzl / 2), (int)std::lround(nch * xyf)));
+  for (int k = 0; k < nxy; k++) {   // chunk-major: concurrently running CTAs share z-planes in L2
+    const int a = (int)((long long)nzl * k / nxy), b = (int)((long long)nzl * (k + 1) / nxy);
     if (b > a)
       for (const CpTile& t : xy) vxy.push_back(item(t, a, b, CP_PMLXY));
   }

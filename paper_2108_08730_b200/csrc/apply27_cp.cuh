@@ -56,8 +56,14 @@ constexpr int CP_STAGES = HZ_CP_STAGES;
 
 // bytes of one ring stage: the w halo tile then NR u halo tiles, CP_HALO elements each
 __host__ __device__ constexpr size_t cp_stage_bytes(int nr) { return (size_t)CP_HALO * (4 + 8 * nr); }
-__host__ __device__ constexpr size_t cp_smem_bytes(int tab_n, int nr) {
-  return (((size_t)tab_n * 12 * 4 + 127) / 128) * 128 + (size_t)CP_STAGES * cp_stage_bytes(nr);
+// DOT4 reads its s operand (the centre u of the previous plane) back from the ring, which keeps one
+// more plane resident: one more stage, same lookahead
+#ifndef HZ_CP_S_SMEM
+#define HZ_CP_S_SMEM 0
+#endif
+__host__ __device__ constexpr int cp_stages(int epi) { return CP_STAGES + ((HZ_CP_S_SMEM && epi == 2) ? 1 : 0); }
+__host__ __device__ constexpr size_t cp_smem_bytes(int tab_n, int nr, int epi) {
+  return (((size_t)tab_n * 12 * 4 + 127) / 128) * 128 + (size_t)cp_stages(epi) * cp_stage_bytes(nr);
 }
 // work item {x0 | y0 << 16, tx | ty << 8 | (xs − x0) << 16 | (ys − y0) << 24, z0 | z1 << 16,
 // (xe − x0) | (ye − y0) << 8 | mode << 16}: the tile computes [x0, x0+tx) × [y0, y0+ty) and stores
@@ -165,7 +171,9 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
   constexpr int NT = CP_THREADS(NY);
   constexpr int KS = CP_SLOTS(NY);
   constexpr int K = epi_k(EPI);
-  constexpr int S = CP_STAGES;
+  constexpr bool SSM = HZ_CP_S_SMEM && EPI == EPI_DOT4;   // s operand from the ring
+  constexpr int S = cp_stages(EPI);
+  constexpr int L = SSM ? S - 2 : S - 1;                   // planes issued ahead
   const unsigned FULL = 0xffffffffu;
 
   // ---- block → (work item, RHS group)
@@ -243,7 +251,7 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
     }
     cp_commit();
   };
-  for (int j = 0; j < S - 1; j++) issue(j);
+  for (int j = 0; j < L; j++) issue(j);
 
   // stage the coefficient table while the first planes stream in
   for (int e = tid; e < p.tab_n * CTAB_STRIDE; e += NT) stab[e] = p.ctab[(long long)p.tab_lo * CTAB_STRIDE + e];
@@ -333,11 +341,12 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
         if (K > 0 && act[r] && do_prev && st_ok[i])
           e1[r][i] = ldg_c(rh0 + ((uint32_t)r * fs + orow + (uint32_t)(oplane + i * nx)));
       }
-    // planes j and j+1 have landed (own copies), then every thread's copies; the slot of plane j-1
-    // is free (all threads are past iteration j-1) and receives plane j+S-1
-    cp_wait<S - 3>();
+    // planes j and j+1 have landed (own copies), then every thread's copies; the slot of plane j+L-S
+    // (j-1, or j-2 when the previous plane's centre is still read) is free — every thread is past the
+    // iteration that last read it — and receives plane j+L
+    cp_wait<L - 2>();
     __syncthreads();
-    issue(j + S - 1);
+    issue(j + L);
 
     const unsigned char* st = ring + (size_t)(j % S) * stage_bytes;
     const float* sw = reinterpret_cast<const float*>(st) + sbase;
@@ -491,13 +500,17 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
         }
         aC[r][i] = b;   // output pl: "prev" of the next call
         aN[r][i] = c;   // output pl+1: "cur" of the next call (a's slot is free after this call)
-        if (EPI == EPI_DOT4) sC[r][i] = u0;   // s of output pl: "prev" s of the next call
+        if (EPI == EPI_DOT4 && !SSM) sC[r][i] = u0;   // s of output pl: "prev" s of the next call
         if (do_prev && st_ok[i]) {
           au0[(uint32_t)r * fs + orow + (uint32_t)(oplane + i * nx)] = a;
           if (EPI == EPI_DOT1) {
             cp_cdot(part[r][0], part[r][1], e1[r][i], a);
           } else if (EPI == EPI_DOT4) {
-            const C sv = sP[r][i];
+            C sv;
+            if (SSM)   // centre u of plane pl-1, still resident in the previous stage
+              sv = reinterpret_cast<const C*>(ring + (size_t)((j + S - 1) % S) * stage_bytes + wbytes + (size_t)r * ubytes)[sbase + (i + 1) * P + 1];
+            else
+              sv = sP[r][i];
             cp_cdot(part[r][0], part[r][1], a, sv);
             cp_norm(part[r][2], a);
             cp_cdot(part[r][3], part[r][4], e1[r][i], sv);

@@ -481,7 +481,7 @@ static cudaError_t launch_cp(const ApplyParams<float, float>& p, int nrhs, cudaS
   g_last_apply_launches = nitems > 0 ? 1 : 0;
   if (nitems <= 0) return cudaSuccess;
   auto kern = apply27_cp<NY, NR, COLLOC, EPI>;
-  const size_t smem = cp_smem_bytes(p.tab_n, NR);
+  const size_t smem = cp_smem_bytes(p.tab_n, NR, EPI);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -596,7 +596,7 @@ static int cp_occ(int tab_n) {
   constexpr int NY = CpNY<NR>::V;
   int nb = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_cp<NY, NR, false, EPI_DOT4>, CP_THREADS(NY),
-                                                cp_smem_bytes(tab_n, NR));
+                                                cp_smem_bytes(tab_n, NR, EPI_DOT4));
   return nb > 0 ? nb : 1;
 }
 int cp_occupancy(int tab_n, int nr) { return nr == 1 ? cp_occ<1>(tab_n) : cp_occ<HZ_CP_NR>(tab_n); }
