@@ -244,29 +244,48 @@ def apply_large(args, hz, ctx, dev, stream, peak):
     u.imag.uniform_(-1, 1)
     au = C.alloc_field(1)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for _ in range(3):
-        hz.hz_apply_impedance(C, u, au, stream=stream)
-    ts = []
-    l0 = hz.hz_kernel_launch_count()
-    for _ in range(10):
-        flush.fill_(1)
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        hz.hz_apply_impedance(C, u, au, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ts.append(e0.elapsed_time(e1))
+
+    def time_apply(Cx, reps=10):
+        for _ in range(3):
+            hz.hz_apply_impedance(Cx, u, au, stream=stream)
+        out = []
+        nonlocal_l0[0] = hz.hz_kernel_launch_count()
+        for _ in range(reps):
+            flush.fill_(1)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            hz.hz_apply_impedance(Cx, u, au, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            out.append(e0.elapsed_time(e1))
+        return out
+
+    nonlocal_l0 = [0]
+    ts = time_apply(C)
+    l0 = nonlocal_l0[0]
     launches = hz.hz_kernel_launch_count() - l0
     ms = statistics.median(ts)
     npts = cfg.nx * cfg.ny * cfg.nz
+    # the same apply with non-adaptive weights (a one-row table: the same weights at every point, like the
+    # paper's G4 / Gm comparison stencils) — the adaptive lookup costs no bytes and
+    # little time ("no overhead")
+    v = synth.velocity_slab(cfg, 0, cfg.nz, device=dev if cfg.index == 5 else None)
+    Tm = hz.hz_table_import(12.0, 0.1, T.rows5()[80][None])   # the GA row at G = 12, everywhere
+    Cm = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, torch.from_numpy(v).to(dev, torch.float32),
+                               freq, Tm, npml=cfg.npml, dtype=hz.HZ_C64)
+    del v
+    ms_m = statistics.median(time_apply(Cm))
+    del Cm
     byts = npts * (4 + 16)            # w in, u in, Au out (complex64, 1 RHS): DESIGN.md §5
     achieved = byts / (ms * 1e-3) / 1e9
     return {"workload": f"config{cfg.index} {cfg.name} {cfg.nx}x{cfg.ny}x{cfg.nz} f={freq:g}Hz c64 nrhs=1, "
                         "hz_apply_impedance only", "gpts_s": npts / (ms * 1e-3) / 1e9, "ms": ms,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "algorithmic_bytes_per_launch": byts},
-            "gpu_launches": launches, "l2": "flushed before every apply (256 MiB write)"}
+            "gpu_launches": launches, "l2": "flushed before every apply (256 MiB write)",
+            "fixed_weights": {"table": "one row (GA weights at G = 12) at every point",
+                              "gpts_s": npts / (ms_m * 1e-3) / 1e9, "ms": ms_m, "adaptive_over_fixed_time": ms / ms_m}}
 
 
 def run_hz(args):

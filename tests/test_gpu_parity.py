@@ -264,3 +264,23 @@ def test_apply_reference_path_c64(hz, ctx, table, ga_table):
     assert hz.hz_kernel_launch_count() - l0 == 2          # general + bulk-copy interior launches
     ref = op.apply(op.assemble(oracle_problem(v, h, f, npml, ga_table, "c64")), u)
     assert rel(got, ref) <= TOL["c64"], rel(got, ref)
+
+
+@pytest.mark.parametrize("which", ["Gm", "G4"])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_apply_non_adaptive_one_row_tables(hz, ctx, which, dtype):
+    """The paper's non-adaptive comparison stencils: a one-row table
+    through hz_table_import gives the same weights at every G (the lookup clamps), on the same kernels —
+    oracle parity with the oracle's own G4 / Gm weights."""
+    from oracle import weights
+    u5 = weights.gm_weights() if which == "Gm" else weights.g4_weights()
+    T1 = hz.hz_table_import(4.0, 0.1, u5[None])
+    wt = weights.WeightTable(4.0, 0.1, np.array([4.0]), u5[None], 0)
+    rng = np.random.default_rng(79)
+    nz, ny, nx, h, f, npml = 17, 21, 67, 25.0, 7.0, 4
+    v = rng.uniform(1500.0, 4500.0, (nz, ny, nx))
+    u = synth.random_field((2, nz, ny, nx), seed=12)
+    C = assemble(hz, ctx, T1, v, h, f, npml, dtype)
+    got = gpu_apply(hz, C, u)
+    ref = op.apply(op.assemble(oracle_problem(v, h, f, npml, wt, dtype)), u)
+    assert rel(got, ref) <= TOL[dtype], rel(got, ref)
