@@ -6,6 +6,7 @@ Follows PAPER.md §2.1 and the adaptive rule of P:36/P:51/P:273/P:446
   S = ws1 S1 + (ws2/3) Σ S2,i + (ws3/4) Σ S3,i
   M: ω²/κ p ⟹ ω² (wm0 p0/κ0 + wm1/6 Σ6 p/κ + wm2/12 Σ12 p/κ + wm3/8 Σ8 p/κ)   (Eq. 8)
   GA: each row uses the weights tabulated at its local G = v/(f h)
+  GAm: each row uses the mean of the weights tabulated at its 27 stencil nodes (reading A19)
 
 with κ = v² (ρ = 1; reading A17) and the PML stretching ∂x̃ = ξx⁻¹ ∂x, ξ = 1 + iγ/ω.
 
@@ -61,13 +62,41 @@ class PointCoefficients:
     k2: np.ndarray           # (ω / v)²
 
 
-def point_coefficients(v, freq, h, table: WeightTable) -> PointCoefficients:
+def average_27(u5):
+    """GAm ("average weights, the averaging being performed over the 27 points"; reading A19):
+    the weight vector of row n is the arithmetic mean of the weight vectors looked up at the row's
+    27 stencil nodes, over the nodes that lie inside the grid (a node on a face / edge / corner of the
+    grid averages 18 / 12 / 8 vectors).  The free weights (ws1, ws2, μ0, μ1, μ2) are averaged; the
+    dependent ones follow from the sum constraints, so the mean satisfies them exactly (the
+    renormalisation of SPEC S:280 is then the identity)."""
+    nz, ny, nx = u5.shape[:3]
+    acc = np.zeros_like(u5)
+    cnt = np.zeros((nz, ny, nx))
+    for dz, dy, dx in OFFSETS:
+        # rows n whose neighbour n + d is in the grid
+        zs = slice(max(0, -dz), nz - max(0, dz))
+        ys = slice(max(0, -dy), ny - max(0, dy))
+        xs = slice(max(0, -dx), nx - max(0, dx))
+        zn = slice(max(0, dz), nz - max(0, -dz))
+        yn = slice(max(0, dy), ny - max(0, -dy))
+        xn = slice(max(0, dx), nx - max(0, -dx))
+        acc[zs, ys, xs] += u5[zn, yn, xn]
+        cnt[zs, ys, xs] += 1.0
+    return acc / cnt[..., None]
+
+
+def point_coefficients(v, freq, h, table: WeightTable, rule: str = "GA") -> PointCoefficients:
     """a2–a5: local G = v/(f h) (Table 1), clamped lookup + linear
-    interpolation of the adaptive weights (A13), stiffness transverse weights t0, t1, t2 (A6),
-    per-point mass weights (A2) and k² = (2πf/v)²."""
+    interpolation of the adaptive weights (A13) — per point ("GA") or averaged over the
+    row's 27 stencil nodes ("GAm", `average_27`) — stiffness transverse weights t0, t1, t2
+    (A6), per-point mass weights (A2) and k² = (2πf/v)²."""
     v = np.asarray(v, dtype=np.float64)
     G = v / (freq * h)
     u5, clamped = lookup(table, G)
+    if rule == "GAm":
+        u5 = average_27(u5)
+    elif rule != "GA":
+        raise ValueError(f"unknown weight rule {rule!r}")
     w7 = u5_to_w7(u5)
     ws1, ws2, ws3 = w7[..., 0], w7[..., 1], w7[..., 2]
     t0 = ws1 + 2.0 / 3.0 * ws2 + 0.5 * ws3
@@ -109,6 +138,7 @@ class Problem:
     r_coeff: float = 1e-3
     v_pml: Optional[float] = None     # None → max(v) (reading A7)
     mass: str = "eq8"                 # "eq8" (default A5) | "colloc"
+    rule: str = "GA"                  # "GA" (row's own weights) | "GAm" (27-point mean, A19)
 
     @property
     def omega(self):
@@ -119,7 +149,7 @@ class Problem:
         return self.v.shape
 
     def coefficients(self) -> PointCoefficients:
-        return point_coefficients(self.v, self.freq, self.h, self.table)
+        return point_coefficients(self.v, self.freq, self.h, self.table, self.rule)
 
     def pml(self):
         vp = float(np.max(self.v)) if self.v_pml is None else float(self.v_pml)
@@ -192,6 +222,23 @@ def apply_rows(prob: Problem, u: np.ndarray, nodes) -> np.ndarray:
     nodes = np.asarray(nodes, dtype=np.int64).reshape(-1, 3)
     I, J, K = nodes[:, 0], nodes[:, 1], nodes[:, 2]
     coef = point_coefficients(prob.v[K, J, I], prob.freq, prob.h, prob.table)
+    if prob.rule == "GAm":   # the 27-node mean at the selected rows only (same rule as average_27)
+        nz, ny, nx = prob.v.shape
+        acc = np.zeros((len(nodes), 5))
+        cnt = np.zeros(len(nodes))
+        for dz, dy, dx in OFFSETS:
+            kk, jj, ii = K + dz, J + dy, I + dx
+            ok = (kk >= 0) & (kk < nz) & (jj >= 0) & (jj < ny) & (ii >= 0) & (ii < nx)
+            vv = prob.v[np.clip(kk, 0, nz - 1), np.clip(jj, 0, ny - 1), np.clip(ii, 0, nx - 1)]
+            u5, _ = lookup(prob.table, vv / (prob.freq * prob.h))
+            acc += np.where(ok[:, None], u5, 0.0)
+            cnt += ok
+        w7 = u5_to_w7(acc / cnt[:, None])
+        coef.w7 = w7
+        coef.t0 = w7[:, 0] + 2.0 / 3.0 * w7[:, 1] + 0.5 * w7[:, 2]
+        coef.t1 = w7[:, 1] / 12.0
+        coef.t2 = w7[:, 2] / 8.0
+        coef.mu = np.stack([w7[:, 3], w7[:, 4] / 6.0, w7[:, 5] / 12.0, w7[:, 6] / 8.0], axis=-1)
     pml = prob.pml()
     nz, ny, nx = prob.v.shape
     out = np.zeros(len(nodes), dtype=np.complex128)

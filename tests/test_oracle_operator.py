@@ -192,3 +192,60 @@ def test_coefficient_identities(ga_table, rng):
     assert np.max(np.abs(c.t0 + 4 * c.t1 + 4 * c.t2 - 1)) < 1e-14
     assert np.max(np.abs(c.mu @ np.array([1, 6, 12, 8]) - 1)) < 1e-14
     assert np.array_equal(c.clamped, (c.G < 4.0) | (c.G > 40.0 + 1e-9))
+
+
+# ---- GAm: weights averaged over the 27 stencil points (reading A19) -------
+def test_gam_equals_ga_on_homogeneous_models(ga_table):
+    """all 27 local G are equal on a homogeneous model, so GAm = GA (to the rounding of a mean
+    of 8–27 equal numbers), with and without PML."""
+    v = np.full((7, 6, 8), 2600.0)
+    for npml in (0, 2):
+        A = op.assemble(op.Problem(v, 25.0, 7.0, npml, ga_table))
+        B = op.assemble(op.Problem(v, 25.0, 7.0, npml, ga_table, rule="GAm"))
+        assert abs(A - B).max() <= 1e-14 * abs(A).max()
+
+
+def test_gam_of_affine_model_inside_one_table_interval(ga_table):
+    """Closed form: within one table interval the interpolated weights are affine in G; for v affine
+    in x, y and z the mean of an affine function over the symmetric 27-point neighbourhood is its
+    value at the centre, so interior rows of GAm equal GA rows exactly (to rounding), while rows on the
+    grid boundary (one-sided neighbourhoods) must differ."""
+    nz, ny, nx = 6, 5, 7
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    h, f = 25.0, 7.0
+    G0 = 12.03                                  # G range 12.03 .. 12.09: inside [12.0, 12.1]
+    v = (G0 + 0.002 * x + 0.003 * y + 0.004 * z) * f * h
+    cga = op.point_coefficients(v, f, h, ga_table, "GA")
+    cgm = op.point_coefficients(v, f, h, ga_table, "GAm")
+    inner = (slice(1, -1), slice(1, -1), slice(1, -1))
+    assert np.allclose(cgm.w7[inner], cga.w7[inner], rtol=0, atol=1e-14)
+    # boundary rows: the one-sided mean is the weight at the neighbourhood's centroid, not the node
+    assert np.abs(cgm.w7[0, 2, 3] - cga.w7[0, 2, 3]).max() > 1e-7
+
+
+def test_gam_sum_constraints_and_counts(ga_table, rng):
+    """The mean keeps ws1+ws2+ws3 = 1 and Σwm = 1; a corner row averages its 8 in-grid
+    nodes: on a model that is v1 at one corner node and v2 elsewhere, the corner row's weights are
+    (w(v1) + 7 w(v2))/8 and the far corner's are w(v2)."""
+    v = rng.uniform(1500.0, 4500.0, (5, 6, 7))
+    c = op.point_coefficients(v, 7.0, 25.0, ga_table, "GAm")
+    assert np.allclose(c.w7[..., :3].sum(-1), 1.0, atol=1e-14)
+    assert np.allclose(c.w7[..., 3:].sum(-1), 1.0, atol=1e-14)
+    v = np.full((4, 4, 4), 3000.0)
+    v[0, 0, 0] = 2000.0
+    c = op.point_coefficients(v, 7.0, 25.0, ga_table, "GAm")
+    w1, _ = weights.lookup(ga_table, 2000.0 / 175.0)
+    w2, _ = weights.lookup(ga_table, 3000.0 / 175.0)
+    assert np.allclose(c.w7[0, 0, 0], weights.u5_to_w7((w1 + 7 * w2) / 8), atol=1e-14)
+    assert np.allclose(c.w7[3, 3, 3], weights.u5_to_w7(w2), atol=1e-14)
+
+
+def test_gam_row_evaluation_matches_assembly(ga_table, rng):
+    """apply_rows (row-by-row, used for sampled parity) and the assembled GAm matrix agree."""
+    v = rng.uniform(1500.0, 4500.0, (6, 7, 8))
+    P = op.Problem(v, 25.0, 7.0, 2, ga_table, rule="GAm")
+    u = rng.standard_normal(v.shape) + 1j * rng.standard_normal(v.shape)
+    full = op.apply(op.assemble(P), u[None])[0]
+    nodes = np.array([[0, 0, 0], [3, 4, 2], [7, 6, 5], [1, 6, 0], [4, 0, 3]])
+    rows = op.apply_rows(P, u, nodes)
+    assert np.allclose(rows, full[nodes[:, 2], nodes[:, 1], nodes[:, 0]], rtol=1e-13, atol=0)
