@@ -58,6 +58,9 @@ typedef enum { HZ_C64 = 0, HZ_C128 = 1 } hz_dtype;
 /* Mass formulation: Eq. 8 (per-neighbour kappa, default A5) or the collocation-kappa
  * variant "Eq. 10". */
 typedef enum { HZ_MASS_EQ8 = 0, HZ_MASS_COLLOC = 1 } hz_mass;
+/* Weight rule of a row: GA = the weights tabulated at the row's own local G; GAm = the mean of
+ * the weights tabulated at the row's 27 stencil nodes (in-grid nodes only; reading A19). */
+typedef enum { HZ_RULE_GA = 0, HZ_RULE_GAM = 1 } hz_rule;
 
 typedef struct hz_ctx hz_ctx;
 typedef struct hz_table hz_table;
@@ -109,7 +112,9 @@ void hz_table_destroy(hz_table* t);
  * neighbouring ranks) into library memory, validates it, counts clamped points, builds the 1-D
  * PML arrays (profile A7, per-axis stretching A8) and uploads the table.  The per-point
  * coefficients (G = v/(f h), lookup + interpolation, t0..t2, mu0..mu3) are
- * NOT stored: every apply recomputes them from v (fused mode, 4 bytes/point).
+ * NOT stored: every apply recomputes them from v (fused mode, 4 bytes/point).  rule = HZ_RULE_GAM
+ * instead stores the 27-node mean weights once ([5][nz_local+2][ny][nx] in the dtype's precision) and
+ * the apply reads them (+20 / 40 bytes per point and apply).
  * grid: this rank's slab of the global grid.  pml->v_pml <= 0 selects max(v) over all ranks.
  * With nranks > 1 the table rows of rank 0 are broadcast so every rank uses identical weights.
  * Returns HZ_WARN_CLAMPED (outputs valid) when *n_clamped > 0.
@@ -132,7 +137,7 @@ typedef struct {
 
 hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, const void* v,
                              double freq_hz, const hz_pml* pml, const hz_table* table, hz_mass mass,
-                             hz_coeffs** out, long long* n_clamped);
+                             hz_rule rule, hz_coeffs** out, long long* n_clamped);
 
 /* Parity export (not on the hot path).  record: [8][nz_local][ny][nx] real (float for C64, double
  * for C128) = (k^2 = (2 pi f / v)^2, t0, t1, t2, mu0, mu1, mu2, mu3) per point (may be NULL).

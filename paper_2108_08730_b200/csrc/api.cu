@@ -190,6 +190,8 @@ struct hz_coeffs {
   hz_dtype dtype = HZ_C64;
   hz_grid grid{};
   hz_mass mass = HZ_MASS_EQ8;
+  hz_rule rule = HZ_RULE_GA;
+  DBuf gam;                    // GAm: [5][nzl+2][ny][nx] 27-node mean weights (t1, t2, mu0, mu1, mu2)
   double freq = 0, omega = 0, h = 0;
   double v_pml = 0;
   hz_pml pml{};
@@ -370,6 +372,7 @@ ApplyParams<R, S> make_params(const hz_coeffs* c) {
   p.nchunks = c->nchunks;
   p.v = c->v.as<S>();
   p.w = c->w.as<S>();
+  p.gam = c->rule == HZ_RULE_GAM ? c->gam.as<S>() : nullptr;
   p.tab = sizeof(R) == 4 ? c->tab_f.as<R>() : c->tab_d.as<R>();
   p.ctab = sizeof(R) == 4 ? c->ctab_f.as<R>() : c->ctab_d.as<R>();
   p.tab_lo = c->tab_lo;
@@ -604,13 +607,14 @@ hz_status cp_attach(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs) {
 
 template <typename R>
 hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double freq, const hz_pml* pml,
-                     const hz_table* table, hz_mass mass, hz_coeffs** out, long long* n_clamped) {
+                     const hz_table* table, hz_mass mass, hz_rule rule, hz_coeffs** out, long long* n_clamped) {
   typedef typename Cx<R>::T C;
   std::unique_ptr<hz_coeffs> c(new hz_coeffs);
   c->ctx = ctx;
   c->dtype = sizeof(R) == 4 ? HZ_C64 : HZ_C128;
   c->grid = *g;
   c->mass = mass;
+  c->rule = rule;
   c->freq = freq;
   c->omega = 2.0 * M_PI * freq;
   c->h = g->h;
@@ -822,6 +826,15 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
     c->nchunks = (g->nz_local + c->zc - 1) / c->zc;
   }
   if (sizeof(R) == 4) HZ_TRY(cp_geometry(c.get()));
+  // ---- GAm: the 27-node mean weights of every owned row, once (A19)
+  if (rule == HZ_RULE_GAM) {
+    HZ_CUDA(c->gam.ensure(5 * (size_t)c->fstride() * sizeof(R)));
+    HZ_CUDA(cudaMemsetAsync(c->gam.p, 0, 5 * (size_t)c->fstride() * sizeof(R), s));
+    ApplyParams<R> gp = make_params<R>(c.get());
+    HZ_CUDA(launch_gam_field<R>(gp, c->gam.as<R>(), s));
+    count_launch();
+    HZ_CUDA(cudaStreamSynchronize(s));
+  }
   if (n_clamped) *n_clamped = (long long)stats[1];
   *out = c.release();
   return stats[1] > 0 ? HZ_WARN_CLAMPED : HZ_OK;
@@ -832,7 +845,7 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
 extern "C" {
 
 hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, const void* v, double freq_hz,
-                             const hz_pml* pml, const hz_table* table, hz_mass mass, hz_coeffs** out,
+                             const hz_pml* pml, const hz_table* table, hz_mass mass, hz_rule rule, hz_coeffs** out,
                              long long* n_clamped) {
   if (!ctx || !grid || !v || !table || !out) { set_error("hz_assemble_coeffs: NULL argument"); return HZ_ERR_INVALID_ARG; }
   const hz_grid& g = *grid;
@@ -849,8 +862,9 @@ hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, c
   if (table->t.n_g < 1) { set_error("hz_assemble_coeffs: empty table"); return HZ_ERR_INVALID_ARG; }
   if (ctx->nranks > 1 && g.nz_local < 1) { set_error("hz_assemble_coeffs: empty slab"); return HZ_ERR_INVALID_ARG; }
   if (cudaSetDevice(ctx->device) != cudaSuccess) { set_error("hz_assemble_coeffs: cudaSetDevice failed"); return HZ_ERR_CUDA; }
-  if (dtype == HZ_C64) return assemble_t<float>(ctx, grid, v, freq_hz, pml, table, mass, out, n_clamped);
-  if (dtype == HZ_C128) return assemble_t<double>(ctx, grid, v, freq_hz, pml, table, mass, out, n_clamped);
+  if (rule != HZ_RULE_GA && rule != HZ_RULE_GAM) { set_error("hz_assemble_coeffs: bad rule"); return HZ_ERR_INVALID_ARG; }
+  if (dtype == HZ_C64) return assemble_t<float>(ctx, grid, v, freq_hz, pml, table, mass, rule, out, n_clamped);
+  if (dtype == HZ_C128) return assemble_t<double>(ctx, grid, v, freq_hz, pml, table, mass, rule, out, n_clamped);
   set_error("hz_assemble_coeffs: bad dtype");
   return HZ_ERR_INVALID_ARG;
 }

@@ -74,6 +74,8 @@ struct ApplyParams {
   int cp_n_pml, cp_n_int, cp_nblocks;
   const S* v;                 // [nzl+2][ny][nx] velocity incl. halo planes
   const S* w;                 // [nzl+2][ny][nx] 1/v² incl. halo planes (apply input)
+  const S* gam;               // GAm rule (A19): [5][nzl+2][ny][nx] row weights (t1, t2, μ0, μ1, μ2)
+                              // averaged over the 27 stencil nodes (stride fstride), or null (GA)
   const R* ctab;              // [n_g][CTAB_STRIDE] pre-scaled class coefficients + differences
   int tab_lo, tab_n;          // rows [tab_lo, tab_lo + tab_n) cover every G of the model (staged in smem)
   const CS* u;                // [nrhs][nzl+2][ny][nx]
@@ -151,6 +153,24 @@ __device__ __forceinline__ RowCoef<R> row_coef(R v, const R* __restrict__ tab, c
   c.m2 = p.w2 * mu2;
   c.m3 = p.w2 * mu3;
   return c;
+}
+
+// GAm row weights (t1, t2, μ0, μ1, μ2 at element idx of the [5][...] field) → the six register
+// coefficients of a row, as the host builds the table rows: c1..c3 = h⁻²(t0 − 4t1, 2t1 − 2t2, 3t2),
+// m1..m3 = ω²(μ1, μ2, μ3), t0 = 1 − 4t1 − 4t2, μ3 = (1 − μ0 − 6μ1 − 12μ2)/8 (A6).
+template <typename R, typename S>
+__device__ __forceinline__ void gam_row(const S* __restrict__ g, long long stride, long long idx, R ih2, R w2, R& c1,
+                                        R& c2, R& c3, R& m1, R& m2, R& m3) {
+  const R t1 = (R)__ldg(g + idx), t2 = (R)__ldg(g + stride + idx);
+  const R mu0 = (R)__ldg(g + 2 * stride + idx), mu1 = (R)__ldg(g + 3 * stride + idx);
+  const R mu2 = (R)__ldg(g + 4 * stride + idx);
+  const R t0 = R(1) - R(4) * (t1 + t2);
+  c1 = ih2 * (t0 - R(4) * t1);
+  c2 = ih2 * (R(2) * (t1 - t2));
+  c3 = ih2 * (R(3) * t2);
+  m1 = w2 * mu1;
+  m2 = w2 * mu2;
+  m3 = w2 * ((R(1) - mu0 - R(6) * mu1 - R(12) * mu2) * R(0.125));
 }
 
 // ---------------------------------------------------------------------------------------------

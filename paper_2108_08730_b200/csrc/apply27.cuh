@@ -309,11 +309,15 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
   const R s_k1 = p.inv_fh * p.inv_dg, s_k0 = -p.g_min * p.inv_dg, s_max = (R)(p.n_g - 1);
 
   // coefficients of output rows of plane pl+1 from w of that plane (a2 + a3)
-  auto coefs = [&](Coef6<R> (&cn)[NY], R (&m0n)[NY], const R (&wc)[NY], bool valid) {
+  auto coefs = [&](Coef6<R> (&cn)[NY], R (&m0n)[NY], const R (&wc)[NY], bool valid, int pl) {
 #pragma unroll
     for (int i = 0; i < NY; i++) {
       const R wn = wc[i];
       if (valid) {
+        if (p.gam != nullptr) {   // GAm: the row's 27-node mean weights (A19)
+          gam_row<R, S>(p.gam, p.fstride, (long long)(pl + 2) * plane + loff + (i + 1) * nx, p.ih2, p.w2, cn[i].c1,
+                        cn[i].c2, cn[i].c3, cn[i].m1, cn[i].m2, cn[i].m3);
+        } else {
         const R vv = rsqrt_r(wn);                           // w > 0 on valid rows
         R sidx = fma(vv, s_k1, s_k0);                      // (G − g_min)/ΔG, G = v/(f h)
         sidx = fmin(fmax(sidx, R(0)), s_max);              // clamp (A13)
@@ -329,6 +333,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
         cn[i].m1 = fma(tau, d.y, a.w);
         cn[i].m2 = fma(tau, d.z, b.x);
         cn[i].m3 = fma(tau, d.w, b.y);
+        }
         if (COLLOC) {   // Eq. "10": ω²/κ0 for all 27 neighbours → m·w0 multiplies the u class sums
           cn[i].m1 *= wn;
           cn[i].m2 *= wn;
@@ -398,7 +403,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
     }
     Coef6<R> cN[NY];
     R mN[NY];
-    coefs(cN, mN, wcN, do_next);
+    coefs(cN, mN, wcN, do_next, pl);
 
 #pragma unroll
     for (int i = 0; i < NY; i++) {

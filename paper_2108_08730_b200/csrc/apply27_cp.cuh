@@ -162,7 +162,7 @@ __device__ __forceinline__ void cp_reduce(const DotT (&part)[NR][K], const bool 
 }
 
 // Work item: see cp_item (local plane indices)
-template <int NY, int NR, bool COLLOC, int EPI, int PM>
+template <int NY, int NR, bool COLLOC, int EPI, int PM, bool GAM>
 __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int item0) {
   typedef float R;
   typedef float2 C;
@@ -372,20 +372,28 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
 #pragma unroll
       for (int i = 0; i < NY; i++) {
         const R wn = do_next ? swn[(1 + i) * P + 1] : R(1);
-        const R vv = rsqrt_r(wn);
-        R sidx = fma(vv, s_k1, s_k0);
-        sidx = fmin(fmax(sidx, R(0)), s_max);
-        const int ii = min((int)sidx, p.n_g - 2);
-        const R tau = sidx - (R)ii;
-        const int li = min(max(ii - p.tab_lo, 0), p.tab_n - 2);
-        const R* row = stab + li * SP;
-        const float4 ta = lds4<R>(row), tb = lds4<R>(row + 4), td = lds4<R>(row + 8);
-        cN[i].c1 = fma(tau, tb.z, ta.x);
-        cN[i].c2 = fma(tau, tb.w, ta.y);
-        cN[i].c3 = fma(tau, td.x, ta.z);
-        cN[i].m1 = fma(tau, td.y, ta.w);
-        cN[i].m2 = fma(tau, td.z, tb.x);
-        cN[i].m3 = fma(tau, td.w, tb.y);
+        if (GAM) {   // GAm: the row's 27-node mean weights (A19), computed at assemble
+          if (do_next)
+            gam_row<R, float>(p.gam, p.fstride, (long long)(pl + 2) * plane + orow + i * nx, p.ih2, w2, cN[i].c1,
+                              cN[i].c2, cN[i].c3, cN[i].m1, cN[i].m2, cN[i].m3);
+          else
+            cN[i] = Coef6<R>{R(0), R(0), R(0), R(0), R(0), R(0)};
+        } else {
+          const R vv = rsqrt_r(wn);
+          R sidx = fma(vv, s_k1, s_k0);
+          sidx = fmin(fmax(sidx, R(0)), s_max);
+          const int ii = min((int)sidx, p.n_g - 2);
+          const R tau = sidx - (R)ii;
+          const int li = min(max(ii - p.tab_lo, 0), p.tab_n - 2);
+          const R* row = stab + li * SP;
+          const float4 ta = lds4<R>(row), tb = lds4<R>(row + 4), td = lds4<R>(row + 8);
+          cN[i].c1 = fma(tau, tb.z, ta.x);
+          cN[i].c2 = fma(tau, tb.w, ta.y);
+          cN[i].c3 = fma(tau, td.x, ta.z);
+          cN[i].m1 = fma(tau, td.y, ta.w);
+          cN[i].m2 = fma(tau, td.z, tb.x);
+          cN[i].m3 = fma(tau, td.w, tb.y);
+        }
         if (COLLOC) {
           cN[i].m1 *= wn;
           cN[i].m2 *= wn;
@@ -549,15 +557,17 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
 // plane-uniform z corrections (chunks touching the z-PML) or the PML-free body, so CTAs of all classes
 // share the GPU; x/y-PML items come first (heavier, scheduled first).  The PML-free body is a separate
 // instantiation because the mere presence of the z-PML code costs ~20% (registers / scheduling).
-template <int NY, int NR, bool COLLOC, int EPI>
+// GAM: rows read their 27-node mean weights (A19) instead of interpolating the table — a separate
+// instantiation (a runtime branch alone slowed the GA kernel by ~5%).
+template <int NY, int NR, bool COLLOC, int EPI, bool GAM>
 __global__ void __launch_bounds__(CP_NTHR, 2) apply27_cp(ApplyParams<float, float> p, int item0) {
   const int mode = p.cp_work[item0 + blockIdx.x].w >> 16;
   if (mode == CP_PMLXY)
-    cp_body<NY, NR, COLLOC, EPI, CP_PMLXY>(p, item0);
+    cp_body<NY, NR, COLLOC, EPI, CP_PMLXY, GAM>(p, item0);
   else if (mode == CP_PMLZ)
-    cp_body<NY, NR, COLLOC, EPI, CP_PMLZ>(p, item0);
+    cp_body<NY, NR, COLLOC, EPI, CP_PMLZ, GAM>(p, item0);
   else
-    cp_body<NY, NR, COLLOC, EPI, CP_LEAN>(p, item0);
+    cp_body<NY, NR, COLLOC, EPI, CP_LEAN, GAM>(p, item0);
 }
 
 }  // namespace hz

@@ -28,7 +28,13 @@ __global__ void record_kernel(ApplyParams<R> p, R w2_over_1, R* __restrict__ rec
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long long)gridDim.x * blockDim.x) {
     const R v = p.v[p.plane + idx];
     R t1, t2, mu0, mu1, mu2;
-    interp_weights<R>(v, tab, p.n_g, p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
+    if (p.gam != nullptr) {   // GAm: the row's 27-node mean weights (A19)
+      const long long e = p.plane + idx;
+      t1 = p.gam[e], t2 = p.gam[p.fstride + e], mu0 = p.gam[2 * p.fstride + e];
+      mu1 = p.gam[3 * p.fstride + e], mu2 = p.gam[4 * p.fstride + e];
+    } else {
+      interp_weights<R>(v, tab, p.n_g, p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
+    }
     rec[0 * n + idx] = w2_over_1 / (v * v);              // k² = ω²/v²
     rec[1 * n + idx] = R(1) - R(4) * (t1 + t2);          // t0
     rec[2 * n + idx] = t1;
@@ -37,6 +43,53 @@ __global__ void record_kernel(ApplyParams<R> p, R w2_over_1, R* __restrict__ rec
     rec[5 * n + idx] = mu1;
     rec[6 * n + idx] = mu2;
     rec[7 * n + idx] = (R(1) - mu0 - R(6) * mu1 - R(12) * mu2) * R(0.125);
+  }
+}
+
+// =============================================================================================
+// GAm rule (reading A19): per owned point, the mean of the interpolated free weights
+// (t1, t2, μ0, μ1, μ2) over the in-grid nodes of its 27-point stencil (v halo planes carry the
+// neighbouring slabs).  One-time, at assemble; out: [5][nzl+2][ny][nx] (halo planes not written).
+// =============================================================================================
+template <typename R>
+__global__ void gam_field_kernel(ApplyParams<R> p, R* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* tab = reinterpret_cast<R*>(smem_raw);
+  for (int i = threadIdx.x; i < p.n_g * TAB_STRIDE; i += blockDim.x) tab[i] = p.tab[i];
+  __syncthreads();
+  const long long n = (long long)p.nzl * p.plane;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long long)gridDim.x * blockDim.x) {
+    const int zl = (int)(idx / p.plane);
+    const int rem = (int)(idx - (long long)zl * p.plane);
+    const int y = rem / p.nx, x = rem - y * p.nx;
+    R a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+    int cnt = 0;
+    for (int dz = -1; dz <= 1; dz++) {
+      const int zg = p.z0 + zl + dz;
+      if (zg < 0 || zg >= p.nzg) continue;
+      for (int dy = -1; dy <= 1; dy++) {
+        if (y + dy < 0 || y + dy >= p.ny) continue;
+        for (int dx = -1; dx <= 1; dx++) {
+          if (x + dx < 0 || x + dx >= p.nx) continue;
+          R t1, t2, mu0, mu1, mu2;
+          interp_weights<R>(p.v[(long long)(zl + 1 + dz) * p.plane + (long long)(y + dy) * p.nx + (x + dx)], tab, p.n_g,
+                            p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
+          a0 += t1;
+          a1 += t2;
+          a2 += mu0;
+          a3 += mu1;
+          a4 += mu2;
+          cnt++;
+        }
+      }
+    }
+    const R ic = R(1) / (R)cnt;
+    const long long e = p.plane + idx;
+    out[e] = a0 * ic;
+    out[p.fstride + e] = a1 * ic;
+    out[2 * p.fstride + e] = a2 * ic;
+    out[3 * p.fstride + e] = a3 * ic;
+    out[4 * p.fstride + e] = a4 * ic;
   }
 }
 
@@ -64,8 +117,13 @@ __global__ void sources_kernel(ApplyParams<R> p, int nsrc, const long long* __re
   R w = ih3;
   if (consistent) {
     R t1, t2, mu0, mu1, mu2;
-    interp_weights<R>(p.v[(long long)(zl + 1) * p.plane + Y * p.nx + X], tab, p.n_g, p.g_min, p.g_max, p.inv_dg,
-                      p.inv_fh, t1, t2, mu0, mu1, mu2);
+    const long long e = (long long)(zl + 1) * p.plane + Y * p.nx + X;
+    if (p.gam != nullptr) {   // GAm: the row's 27-node mean weights (A19)
+      t1 = p.gam[e], t2 = p.gam[p.fstride + e], mu0 = p.gam[2 * p.fstride + e];
+      mu1 = p.gam[3 * p.fstride + e], mu2 = p.gam[4 * p.fstride + e];
+    } else {
+      interp_weights<R>(p.v[e], tab, p.n_g, p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
+    }
     const int cls = (dx != 0) + (dy != 0) + (dz != 0);
     const R mu3 = (R(1) - mu0 - R(6) * mu1 - R(12) * mu2) * R(0.125);
     const R mu = cls == 0 ? mu0 : (cls == 1 ? mu1 : (cls == 2 ? mu2 : mu3));
@@ -473,14 +531,14 @@ int apply_last_launches() { return g_last_apply_launches; }
 #endif
 template <int NR> struct CpNY { enum { V = NR == 1 ? HZ_CP_NY1 : 1 }; };
 
-template <int NR, bool COLLOC, int EPI>
-static cudaError_t launch_cp(const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
+template <int NR, bool COLLOC, int EPI, bool GAM>
+static cudaError_t launch_cp_t(const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
   constexpr int NY = CpNY<NR>::V;
   const int ngroups = (nrhs + NR - 1) / NR;
   const int nitems = p.cp_n_pml + p.cp_n_int;
   g_last_apply_launches = nitems > 0 ? 1 : 0;
   if (nitems <= 0) return cudaSuccess;
-  auto kern = apply27_cp<NY, NR, COLLOC, EPI>;
+  auto kern = apply27_cp<NY, NR, COLLOC, EPI, GAM>;
   const size_t smem = cp_smem_bytes(p.tab_n, NR, EPI);
   static size_t attr = 0;
   if (smem > attr) {
@@ -490,6 +548,10 @@ static cudaError_t launch_cp(const ApplyParams<float, float>& p, int nrhs, cudaS
   }
   kern<<<dim3((unsigned)nitems, (unsigned)ngroups), CP_THREADS(NY), smem, s>>>(p, 0);
   return cudaGetLastError();
+}
+template <int NR, bool COLLOC, int EPI>
+static cudaError_t launch_cp(const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
+  return p.gam != nullptr ? launch_cp_t<NR, COLLOC, EPI, true>(p, nrhs, s) : launch_cp_t<NR, COLLOC, EPI, false>(p, nrhs, s);
 }
 
 #ifndef HZ_CP_NR
@@ -530,7 +592,7 @@ static cudaError_t launch_apply_t(ApplyParams<R, S> p, int nrhs, cudaStream_t s)
   if (e != cudaSuccess) return e;
   if constexpr (std::is_same<R, float>::value && std::is_same<S, float>::value) {
 #ifndef HZ_NO_TMA
-    if (p.tma_ntx > 0) return launch_tma<COLLOC, EPI>(p, nbox, s);
+    if (p.tma_ntx > 0 && p.gam == nullptr) return launch_tma<COLLOC, EPI>(p, nbox, s);
 #endif
   }
   return launch_one<R, S, COLLOC, EPI, true>(p, nbox, s);
@@ -595,7 +657,7 @@ template <int NR>
 static int cp_occ(int tab_n) {
   constexpr int NY = CpNY<NR>::V;
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_cp<NY, NR, false, EPI_DOT4>, CP_THREADS(NY),
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_cp<NY, NR, false, EPI_DOT4, false>, CP_THREADS(NY),
                                                 cp_smem_bytes(tab_n, NR, EPI_DOT4));
   return nb > 0 ? nb : 1;
 }
@@ -610,6 +672,16 @@ cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s) {
 }
 template cudaError_t launch_record<float>(const ApplyParams<float>&, float*, cudaStream_t);
 template cudaError_t launch_record<double>(const ApplyParams<double>&, double*, cudaStream_t);
+
+template <typename R>
+cudaError_t launch_gam_field(const ApplyParams<R>& p, R* out, cudaStream_t s) {
+  const size_t smem = (size_t)p.n_g * TAB_STRIDE * sizeof(R);
+  cudaFuncSetAttribute(gam_field_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  gam_field_kernel<R><<<148 * 8, 256, smem, s>>>(p, out);
+  return cudaGetLastError();
+}
+template cudaError_t launch_gam_field<float>(const ApplyParams<float>&, float*, cudaStream_t);
+template cudaError_t launch_gam_field<double>(const ApplyParams<double>&, double*, cudaStream_t);
 
 template <typename R>
 cudaError_t launch_sources(const ApplyParams<R>& p, int nsrc, const long long* nodes, const double* amps,

@@ -56,6 +56,7 @@ cudaError_t launch_apply<double, float>(const ApplyParams<double, float>& p, int
                                         cudaStream_t s);
 template <typename R> cudaError_t launch_winv(const R* v, R* w, long long n, cudaStream_t s);
 template <typename R> cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s);
+template <typename R> cudaError_t launch_gam_field(const ApplyParams<R>& p, R* out, cudaStream_t s);
 template <typename R>
 cudaError_t launch_sources(const ApplyParams<R>& p, int nsrc, const long long* nodes, const double* amps,
                            int consistent, R ih3, typename Cx<R>::T* b, cudaStream_t s);

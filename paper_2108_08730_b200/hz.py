@@ -23,6 +23,7 @@ _lib = ct.CDLL(_LIBPATH)
 HZ_OK, HZ_NOT_CONVERGED, HZ_BREAKDOWN, HZ_WARN_CLAMPED = 0, 1, 2, 3
 HZ_C64, HZ_C128 = 0, 1
 HZ_MASS_EQ8, HZ_MASS_COLLOC = 0, 1
+HZ_RULE_GA, HZ_RULE_GAM = 0, 1
 STATUS_NAMES = {0: "HZ_OK", 1: "HZ_NOT_CONVERGED", 2: "HZ_BREAKDOWN", 3: "HZ_WARN_CLAMPED",
                 -1: "HZ_ERR_INVALID_ARG", -2: "HZ_ERR_DOMAIN", -3: "HZ_ERR_RANK", -4: "HZ_ERR_OOM",
                 -5: "HZ_ERR_CUDA", -6: "HZ_ERR_NCCL", -7: "HZ_ERR_SOURCE_IN_PML"}
@@ -78,7 +79,7 @@ _sigs = {
     "hz_table_rows": (ct.c_int, [_vp, _P(ct.c_int), _P(ct.c_double), _P(ct.c_double)]),
     "hz_table_destroy": (None, [_vp]),
     "hz_assemble_coeffs": (ct.c_int, [_vp, _P(hz_grid), ct.c_int, _vp, ct.c_double, _P(hz_pml), _vp,
-                                      ct.c_int, _P(_vp), _P(ct.c_longlong)]),
+                                      ct.c_int, ct.c_int, _P(_vp), _P(ct.c_longlong)]),
     "hz_coeffs_export": (ct.c_int, [_vp, _vp, _vp, ct.c_int]),
     "hz_coeffs_destroy": (None, [_vp]),
     "hz_apply_impedance": (ct.c_int, [_vp, _vp, _vp, ct.c_int, _vp]),
@@ -244,7 +245,7 @@ class Coeffs:
 def hz_assemble_coeffs(ctx: Ctx, nx: int, ny: int, nz_global: int, h: float, v, freq: float, table: Table,
                        npml: int = 8, r_coeff: float = 1e-3, v_pml: float = 0.0, z0: int = 0,
                        nz_local: Optional[int] = None, dtype: int = HZ_C64, mass: int = HZ_MASS_EQ8,
-                       v_halo: bool = False) -> Coeffs:
+                       v_halo: bool = False, rule: int = HZ_RULE_GA) -> Coeffs:
     if nz_local is None:
         nz_local = nz_global - z0
     g = hz_grid(nx, ny, nz_global, z0, nz_local, h, 1 if v_halo else 0)
@@ -252,7 +253,7 @@ def hz_assemble_coeffs(ctx: Ctx, nx: int, ny: int, nz_global: int, h: float, v, 
     out = _vp()
     ncl = ct.c_longlong(0)
     st = _check(_lib.hz_assemble_coeffs(ctx._h, ct.byref(g), dtype, _ptr(v), freq, ct.byref(p), table._h, mass,
-                                        ct.byref(out), ct.byref(ncl)), "hz_assemble_coeffs")
+                                        rule, ct.byref(out), ct.byref(ncl)), "hz_assemble_coeffs")
     return Coeffs(out, g, dtype, st, ncl.value, ctx)
 
 

@@ -63,9 +63,9 @@ def gpu_apply(hz, C, u):
     return aud[:, 1:-1].cpu().numpy()
 
 
-def oracle_problem(v, h, f, npml, ga_table, dtype, mass="eq8"):
+def oracle_problem(v, h, f, npml, ga_table, dtype, mass="eq8", rule="GA"):
     # the oracle receives exactly the values the GPU received (float32-rounded for c64)
-    return op.Problem(v.astype(rdt(dtype)).astype(np.float64), h, f, npml, ga_table, mass=mass)
+    return op.Problem(v.astype(rdt(dtype)).astype(np.float64), h, f, npml, ga_table, mass=mass, rule=rule)
 
 
 def rel(a, b):
@@ -284,3 +284,66 @@ def test_apply_non_adaptive_one_row_tables(hz, ctx, which, dtype):
     got = gpu_apply(hz, C, u)
     ref = op.apply(op.assemble(oracle_problem(v, h, f, npml, wt, dtype)), u)
     assert rel(got, ref) <= TOL[dtype], rel(got, ref)
+
+
+@pytest.mark.parametrize("mass", ["eq8", "colloc"])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_apply_gam_rule(hz, ctx, table, ga_table, dtype, mass):
+    """GAm (reading A19): rows use the mean of the weights of their 27 stencil
+    nodes, computed once at assemble; same kernels otherwise — full oracle comparison on a sharp-contrast
+    random model with PML (odd nx: ragged tiles), 2 RHS."""
+    rng = np.random.default_rng(80)
+    nz, ny, nx, h, f, npml = 15, 19, 71, 25.0, 7.0, 3
+    v = rng.uniform(1500.0, 4500.0, (nz, ny, nx))
+    u = synth.random_field((2, nz, ny, nx), seed=13)
+    C = assemble(hz, ctx, table, v, h, f, npml, dtype, mass=mass, rule=hz.HZ_RULE_GAM)
+    got = gpu_apply(hz, C, u)
+    P = oracle_problem(v, h, f, npml, ga_table, dtype, mass=mass, rule="GAm")
+    ref = op.apply(op.assemble(P), u)
+    assert rel(got, ref) <= TOL[dtype], rel(got, ref)
+    # GAm differs from GA on this model by far more than the tolerance (the rule is really applied)
+    ref_ga = op.apply(op.assemble(oracle_problem(v, h, f, npml, ga_table, dtype, mass=mass)), u)
+    assert rel(ref_ga, ref) > 10 * TOL["c64"]
+
+
+def test_gam_record_sources_and_decomposition(hz, ctx, table, ga_table):
+    """GAm through the rest of the ABI: the exported per-point record holds the 27-node mean weights,
+    consistent point sources use them, and a z-slab decomposition (halo planes from the caller) gives
+    the bitwise same apply."""
+    rng = np.random.default_rng(81)
+    nz, ny, nx, h, f, npml = 12, 11, 13, 25.0, 7.0, 2
+    v = rng.uniform(1500.0, 4500.0, (nz, ny, nx)).astype(np.float64)
+    C = assemble(hz, ctx, table, v, h, f, npml, "c128", rule=hz.HZ_RULE_GAM)
+    rec = np.zeros((8, nz, ny, nx))
+    hz.hz_coeffs_export(C, record=rec)
+    coef = op.point_coefficients(v, f, h, ga_table, "GAm")
+    assert np.allclose(rec[1], coef.t0, rtol=0, atol=1e-12)
+    assert np.allclose(rec[4:8], np.moveaxis(coef.mu, -1, 0), rtol=0, atol=1e-12)
+    P = op.Problem(v, h, f, npml, ga_table, rule="GAm")
+    nodes = np.array([[6, 5, 6], [4, 3, 5]])
+    b = C.alloc_field(2)
+    hz.hz_point_sources(C, nodes, b)
+    B = op.point_sources(P, nodes)
+    assert rel(b[:, 1:-1].cpu().numpy(), B) <= 1e-12
+    # slabs
+    u = synth.random_field((1, nz, ny, nx), seed=14)
+    vf = v.astype(np.float32)
+    full = gpu_apply(hz, assemble(hz, ctx, table, vf, h, f, npml, "c64", rule=hz.HZ_RULE_GAM), u)
+    out = np.zeros_like(full)
+    for z0, z1 in ((0, 5), (5, 12)):
+        nzl = z1 - z0
+        vs = np.ones((nzl + 2, ny, nx), np.float32)
+        lo, hi = max(z0 - 1, 0), min(z1 + 1, nz)
+        vs[lo - (z0 - 1):hi - (z0 - 1)] = vf[lo:hi]
+        Cs = hz.hz_assemble_coeffs(ctx, nx, ny, nz, h, torch.from_numpy(vs).cuda(), f, table, npml=npml, z0=z0,
+                                   nz_local=nzl, v_pml=float(vf.max()), v_halo=True, rule=hz.HZ_RULE_GAM)
+        ud = Cs.alloc_field(1)
+        for k in range(nzl + 2):
+            zg = z0 - 1 + k
+            if 0 <= zg < nz:
+                ud[:, k] = torch.from_numpy(u[:, zg]).cuda()
+        aud = Cs.alloc_field(1)
+        hz.hz_apply_impedance(Cs, ud, aud)
+        torch.cuda.synchronize()
+        out[:, z0:z1] = aud[:, 1:-1].cpu().numpy()
+    assert np.array_equal(out, full)
