@@ -1,31 +1,14 @@
-// Fused coefficient build + matrix-free 27-point impedance apply (north-star steps a2–a6).
+// Shared definitions of the fused coefficient build + matrix-free 27-point impedance apply
+// (north-star steps a2–a6): launch parameters, epilogue kinds, the z-chunk ranges, the free-weight
+// interpolation used outside the apply, the GAm row coefficients, the dot-product reductions.
 //
 //   (Au)_n = ω² Σ_d μ_{|d|}(w_n) u_{n+d} / v²_{n+d}                 Eq. 8, A2, A4
 //          + Σ_a Σ_e D_a(n_a,e) Σ_{p,q} T(p,q; w_n) u_{n+e ê_a+p ê_b+q ê_c}   A6 (App. A), A8
 //   w_n = linear interpolation of the Tikhonov table at G = v_n/(f h), clamped   P:36, A13
 //
-// Design (B200): HBM-bound stencil (20 B/point for complex64, nrhs = 1: read u, read v, write Au).
-//  * The coefficients are recomputed from v in registers (no coefficient record in HBM: "fused
-//    mode").  The table (≤ 1024 rows × 12 values) lives in shared memory; per row it stores
-//    (t1, t2, μ0, μ1, μ2) and their forward differences, so the interpolation is 5 FMAs and the
-//    class coefficients follow from t0 = 1 − 4t1 − 4t2 and μ3 = (1 − μ0 − 6μ1 − 12μ2)/8.
-//  * Interior rows use the class-sum form: per plane and point the in-plane sums
-//    P0 = u, P1 = 4 faces, P2 = 4 corners (and the same Q for q = u/v²); the 27-point row is then
-//      c0 U0 + c1 U1 + c2 U2 + c3 U3 + m0 Q0 + … with U1 = P1(k) + P0(k±1), U2 = P2(k) + P1(k±1),
-//      U3 = P2(k±1), c = h⁻²(−6t0, t0−4t1, 2t1−2t2, 3t2), m = ω²μ.
-//  * Thread mapping: a lane owns one x position and a strip of NY consecutive y rows, and the
-//    warp marches a chunk of z planes.  Lanes of a warp cover 32 consecutive (strip, x) positions
-//    of the flattened strip-row space (no padding waste for nx not a multiple of 32); x-neighbours
-//    come from warp shuffles (lanes 0/31 load the warp-edge halo), y-neighbours from the thread's
-//    own strip (+1 halo row each side), z-neighbours by scatter-accumulation into the partial
-//    outputs of planes k−1, k, k+1 (two complex accumulators + two planes of coefficients
-//    persist per point).  No shared memory is used for the field.
-//  * complex64 arithmetic runs on the packed FP32x2 pipe (FFMA2/FADD2).
-//  * PML rows (a few % of the grid) add the stretched per-axis correction
-//      Σ_a δ⁻_a (T_a u(n−ê_a) − T_a u(n)) + δ⁺_a (T_a u(n+ê_a) − T_a u(n)),  δ± = a± − h⁻²
-//    in a divergent slow path that re-reads the 27-neighbourhood from L1/L2.
-//  * Optional epilogues fuse the BiCGSTAB dot products (fp64 accumulation, deterministic
-//    block-then-grid reduction with a last-block ticket).
+// The kernels: apply27_cp.cuh (complex64, RHS-fused, every tile class in one launch),
+// apply27.cuh (register path: complex128 and the fp64 residual of the complex64 solver),
+// apply27_tma.cuh (bulk-copy interior kernel, the HZ_NO_CP reference path).  DESIGN.md §5.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -113,13 +96,10 @@ __host__ __device__ __forceinline__ void chunk_range(const ApplyParams<R, S>& p,
 }
 
 // ---------------------------------------------------------------------------------------------
-// Coefficients of one row from its velocity: interpolated (t1, t2, μ0, μ1, μ2) → c0..c3, m0..m3.
+// Free weights of one row from its velocity: G = v/(f h) clamped, linear interpolation (A13).
+// (The apply kernels interpolate the pre-scaled class-coefficient table instead; this form serves
+// the record export, the consistent sources and the GAm field.)
 // ---------------------------------------------------------------------------------------------
-template <typename R>
-struct RowCoef {
-  R c0, c1, c2, c3, m0, m1, m2, m3;
-};
-
 template <typename R>
 __device__ __forceinline__ void interp_weights(R v, const R* __restrict__ tab, int n_g, R g_min, R g_max,
                                                R inv_dg, R inv_fh, R& t1, R& t2, R& mu0, R& mu1, R& mu2) {
@@ -134,25 +114,6 @@ __device__ __forceinline__ void interp_weights(R v, const R* __restrict__ tab, i
   mu0 = fma(tau, row[7], row[2]);
   mu1 = fma(tau, row[8], row[3]);
   mu2 = fma(tau, row[9], row[4]);
-}
-
-template <typename R, typename S>
-__device__ __forceinline__ RowCoef<R> row_coef(R v, const R* __restrict__ tab, const ApplyParams<R, S>& p) {
-  R t1, t2, mu0, mu1, mu2;
-  interp_weights<R>(v, tab, p.n_g, p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
-  RowCoef<R> c;
-  // t0 = ws1 + 2/3 ws2 + 1/2 ws3 = 1 − 4 t1 − 4 t2 (A6);  class coefficients × h⁻²
-  const R t12 = t1 + t2;
-  c.c0 = p.ih2 * fma((R)24, t12, (R)-6);                 // −6 t0
-  c.c1 = p.ih2 * fma((R)-8, t1, fma((R)-4, t2, (R)1));   // t0 − 4 t1
-  c.c2 = p.ih2 * ((R)2 * (t1 - t2));                     // 2 t1 − 2 t2
-  c.c3 = p.ih2 * ((R)3 * t2);                            // 3 t2
-  const R mu3 = ((R)1 - mu0 - (R)6 * mu1 - (R)12 * mu2) * (R)0.125;   // wm3/8
-  c.m0 = p.w2 * mu0;
-  c.m1 = p.w2 * mu1;
-  c.m2 = p.w2 * mu2;
-  c.m3 = p.w2 * mu3;
-  return c;
 }
 
 // GAm row weights (t1, t2, μ0, μ1, μ2 at element idx of the [5][...] field) → the six register
@@ -173,9 +134,6 @@ __device__ __forceinline__ void gam_row(const S* __restrict__ g, long long strid
   m3 = w2 * ((R(1) - mu0 - R(6) * mu1 - R(12) * mu2) * R(0.125));
 }
 
-// ---------------------------------------------------------------------------------------------
-// PML correction for one row (slow path).  zl: local plane index of the output.
-// ---------------------------------------------------------------------------------------------
 // field value at element idx of this RHS: storage → arithmetic type, plus the compensation term
 // of the double-float iterate in the mixed-precision residual (R = double, S = float)
 template <typename R, typename S>
@@ -186,58 +144,6 @@ __device__ __forceinline__ typename Cx<R>::T load_u(const typename Cx<S>::T* __r
     if (ulb != nullptr) u = cadd(u, to_cx(ldg_c(ulb + idx), R(0)));
   }
   return u;
-}
-
-template <typename R, typename S>
-__device__ __noinline__ typename Cx<R>::T pml_correction(const ApplyParams<R, S>& p, const R* __restrict__ tab,
-                                                         const typename Cx<S>::T* __restrict__ ub,
-                                                         const typename Cx<S>::T* __restrict__ ulb,
-                                                         int x, int y, int zl) {
-  typedef typename Cx<R>::T C;
-  const int zg = p.z0 + zl;
-  C n[3][3][3];
-#pragma unroll
-  for (int dz = 0; dz < 3; dz++)
-#pragma unroll
-    for (int dy = 0; dy < 3; dy++)
-#pragma unroll
-      for (int dx = 0; dx < 3; dx++) {
-        int xx = x + dx - 1, yy = y + dy - 1, zz = zg + dz - 1;
-        bool in = xx >= 0 && xx < p.nx && yy >= 0 && yy < p.ny && zz >= 0 && zz < p.nzg;
-        n[dz][dy][dx] = in ? load_u<R, S>(ub, ulb, (long long)(zl + dz) * p.plane + (long long)yy * p.nx + xx) : czero(R(0));
-      }
-  R t1, t2, mu0, mu1, mu2;
-  const R vv = (R)p.v[(long long)(zl + 1) * p.plane + (long long)y * p.nx + x];
-  interp_weights<R>(vv, tab, p.n_g, p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
-  const R t0 = (R)1 - (R)4 * (t1 + t2);
-  C corr = czero(R(0));
-  const int idx[3] = {x, y, zg};
-#pragma unroll
-  for (int a = 0; a < 3; a++) {
-    if (idx[a] >= p.lo[a] && idx[a] <= p.hi[a]) continue;
-    C T[3];
-#pragma unroll
-    for (int e = 0; e < 3; e++) {
-      C c, f, k;
-      if (a == 0) {        // transverse plane (y, z) at x + e − 1
-        c = n[1][1][e];
-        f = cadd(cadd(n[1][0][e], n[1][2][e]), cadd(n[0][1][e], n[2][1][e]));
-        k = cadd(cadd(n[0][0][e], n[0][2][e]), cadd(n[2][0][e], n[2][2][e]));
-      } else if (a == 1) { // transverse plane (x, z) at y + e − 1
-        c = n[1][e][1];
-        f = cadd(cadd(n[1][e][0], n[1][e][2]), cadd(n[0][e][1], n[2][e][1]));
-        k = cadd(cadd(n[0][e][0], n[0][e][2]), cadd(n[2][e][0], n[2][e][2]));
-      } else {             // transverse plane (x, y) at z + e − 1
-        c = n[e][1][1];
-        f = cadd(cadd(n[e][1][0], n[e][1][2]), cadd(n[e][0][1], n[e][2][1]));
-        k = cadd(cadd(n[e][0][0], n[e][0][2]), cadd(n[e][2][0], n[e][2][2]));
-      }
-      T[e] = cfma(t0, c, cfma(t1, f, cscale(t2, k)));
-    }
-    const C dmv = p.dm[a][idx[a]], dpv = p.dp[a][idx[a]];
-    corr = cadd(corr, cadd(cmul(dmv, csub(T[0], T[1])), cmul(dpv, csub(T[2], T[1]))));
-  }
-  return corr;
 }
 
 // conj(a) * b accumulated in double
