@@ -120,7 +120,10 @@ constexpr int XT = 30;
 #define HZ_MINB_F 3
 #endif
 template <typename R> struct ApplyBounds { enum { MINB = HZ_MINB_F }; };
-template <> struct ApplyBounds<double> { enum { MINB = 2 }; };
+#ifndef HZ_MINB_D
+#define HZ_MINB_D 3
+#endif
+template <> struct ApplyBounds<double> { enum { MINB = HZ_MINB_D }; };
 
 // The apply is two launches of this template (same arithmetic per point, so results do not depend on
 // which launch computes a point):

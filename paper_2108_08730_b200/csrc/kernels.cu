@@ -378,7 +378,7 @@ template <typename R> struct ApplyCfg;
 #define HZ_W_F 4
 #endif
 #ifndef HZ_NY_D
-#define HZ_NY_D 2
+#define HZ_NY_D 1
 #endif
 template <> struct ApplyCfg<float> { enum { NY = HZ_NY_F, WARPS = HZ_W_F }; };
 template <> struct ApplyCfg<double> { enum { NY = HZ_NY_D, WARPS = 4 }; };
