@@ -314,6 +314,19 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
 
   // output / epilogue element of (row yl0, column x) in plane storage 0 of each RHS: + pl·plane
   const uint32_t orow = (uint32_t)(yl0 * nx + x);
+  // GAm: the 5 weights of this thread's rows of the next coefficient plane, loaded one call ahead
+  R gpf[NY][5];
+  auto gam_load = [&](R (&g)[5], int splane, int i) {
+    const long long e = (long long)splane * plane + orow + i * nx;
+#pragma unroll
+    for (int k = 0; k < 5; k++) g[k] = __ldg(p.gam + k * p.fstride + e);
+  };
+  if (GAM) {
+#pragma unroll
+    for (int i = 0; i < NY; i++) {
+      gam_load(gpf[i], zc0 + 1, i);   // rows of output plane zc0 (storage zc0 + 1), used by call j = 0
+    }
+  }
   const float2* __restrict__ rh0 = p.rhat + (long long)rhs0 * p.fstride;
   float2* __restrict__ au0 = p.au + (long long)rhs0 * p.fstride;
 #ifndef HZ_CP_NO_OPAQUE
@@ -372,12 +385,20 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
 #pragma unroll
       for (int i = 0; i < NY; i++) {
         const R wn = do_next ? swn[(1 + i) * P + 1] : R(1);
-        if (GAM) {   // GAm: the row's 27-node mean weights (A19), computed at assemble
-          if (do_next)
-            gam_row<R, float>(p.gam, p.fstride, (long long)(pl + 2) * plane + orow + i * nx, p.ih2, w2, cN[i].c1,
-                              cN[i].c2, cN[i].c3, cN[i].m1, cN[i].m2, cN[i].m3);
-          else
+        if (GAM) {   // GAm: the row's 27-node mean weights (A19), prefetched one plane ahead
+          if (do_next) {
+            const R t1 = gpf[i][0], t2 = gpf[i][1], mu0 = gpf[i][2], mu1 = gpf[i][3], mu2 = gpf[i][4];
+            const R t0 = R(1) - R(4) * (t1 + t2);
+            cN[i].c1 = p.ih2 * (t0 - R(4) * t1);
+            cN[i].c2 = p.ih2 * (R(2) * (t1 - t2));
+            cN[i].c3 = p.ih2 * (R(3) * t2);
+            cN[i].m1 = w2 * mu1;
+            cN[i].m2 = w2 * mu2;
+            cN[i].m3 = w2 * ((R(1) - mu0 - R(6) * mu1 - R(12) * mu2) * R(0.125));
+          } else {
             cN[i] = Coef6<R>{R(0), R(0), R(0), R(0), R(0), R(0)};
+          }
+          if (pl + 2 < zc1) gam_load(gpf[i], pl + 3, i);   // the next call's rows
         } else {
           const R vv = rsqrt_r(wn);
           R sidx = fma(vv, s_k1, s_k0);
