@@ -207,6 +207,25 @@ hz_status hz_solve(const hz_coeffs* c, const void* b, void* x, int nrhs, const h
 hz_status hz_point_sources(const hz_coeffs* c, int nsrc, const long long* node_xyz,
                            const double* amp_re_im, int consistent, void* b, void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Evaluation (not on the hot path)
+ * hz_eqerror: the paper's accuracy metric (Eq. eqerror; reading A20) between two
+ * wavefields of this rank's slab, [nz_local+2][ny][nx] complex of the coeffs' dtype (host or device;
+ * the owned planes are read):
+ *   err = sum W |Re(u_ref - u)| / sum W |Re u_ref|  +  sum W |Im(u_ref - u)| / sum W |Im u_ref|
+ * with W = h * distance to the source node src_xyz (global x, y, z), over the nodes at least
+ * npml_mask nodes away from every face and more than ball_cells nodes from the source.  Sums in fp64
+ * (fixed-order block reduction), summed over the ranks.  HZ_ERR_DOMAIN if a reference sum is 0.
+ * hz_table_dispersion: normalised numerical phase velocity of the table's stencil (P:129-160,
+ * Eq. vtilde) at G[i] (clamped linear interpolation of the table, A13) for the propagation angles
+ * (theta[j], phi[j]) in radians, evaluated on the device in fp64: vtilde[i*nang + j] (host or device
+ * memory; G, theta, phi are host arrays).  HZ_ERR_DOMAIN for G <= 0.
+ * ------------------------------------------------------------------------------------------- */
+hz_status hz_eqerror(const hz_coeffs* c, const void* u_ref, const void* u, const long long src_xyz[3],
+                     int npml_mask, double ball_cells, double* err_out, void* stream);
+hz_status hz_table_dispersion(const hz_table* t, int nG, const double* G, int nang, const double* theta,
+                              const double* phi, double* vtilde, void* stream);
+
 /* Number of libhz kernels launched since process start (evidence for the bench's gpu_launches). */
 long long hz_kernel_launch_count(void);
 

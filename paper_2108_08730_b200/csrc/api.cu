@@ -1000,6 +1000,97 @@ extern "C" hz_status hz_point_sources(const hz_coeffs* c, int nsrc, const long l
 
 
 // ---------------------------------------------------------------------------------------------
+// evaluation: eqerror and the stencil's plane-wave dispersion
+// ---------------------------------------------------------------------------------------------
+template <typename R>
+static hz_status eqerror_t(const hz_coeffs* c, const void* uref, const void* u, const long long* src, int npml,
+                           double ball, double* err, cudaStream_t s) {
+  typedef typename Cx<R>::T C;
+  const size_t fb = (size_t)c->fstride() * sizeof(C);
+  DBuf tr, tu, part;
+  const void* rd = uref;
+  const void* ud = u;
+  if (!is_device_ptr(uref)) { HZ_CUDA(tr.ensure(fb)); HZ_CUDA(cudaMemcpyAsync(tr.p, uref, fb, cudaMemcpyHostToDevice, s)); rd = tr.p; }
+  if (!is_device_ptr(u)) { HZ_CUDA(tu.ensure(fb)); HZ_CUDA(cudaMemcpyAsync(tu.p, u, fb, cudaMemcpyHostToDevice, s)); ud = tu.p; }
+  const int nb = 148 * 4;
+  HZ_CUDA(part.ensure(sizeof(double) * 4 * nb));
+  const hz_grid& g = c->grid;
+  HZ_CUDA(launch_eqerror<R>(reinterpret_cast<const C*>(rd), reinterpret_cast<const C*>(ud), g.nx, g.ny, g.nz_local, g.z0,
+                            g.nz_global, src, g.h, npml, ball, part.as<double>(), nb, s));
+  count_launch();
+  std::vector<double> hp(4 * nb);
+  HZ_CUDA(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * 4 * nb, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  double sum[4] = {0, 0, 0, 0};
+  for (int b = 0; b < nb; b++)
+    for (int k = 0; k < 4; k++) sum[k] += hp[4 * b + k];
+  if (c->ctx->nranks > 1) {
+    DBuf d4;
+    HZ_CUDA(d4.ensure(sizeof(sum)));
+    HZ_CUDA(cudaMemcpyAsync(d4.p, sum, sizeof(sum), cudaMemcpyHostToDevice, s));
+    HZ_TRY(allreduce_sum(c, d4.as<double>(), 4, s));
+    HZ_CUDA(cudaMemcpyAsync(sum, d4.p, sizeof(sum), cudaMemcpyDeviceToHost, s));
+    HZ_CUDA(cudaStreamSynchronize(s));
+  }
+  if (!(sum[2] > 0) || !(sum[3] > 0)) { set_error("hz_eqerror: degenerate reference field"); return HZ_ERR_DOMAIN; }
+  *err = sum[0] / sum[2] + sum[1] / sum[3];
+  return HZ_OK;
+}
+
+extern "C" hz_status hz_eqerror(const hz_coeffs* c, const void* u_ref, const void* u, const long long src_xyz[3],
+                                int npml_mask, double ball_cells, double* err_out, void* stream) {
+  if (!c || !u_ref || !u || !src_xyz || !err_out || npml_mask < 0) { set_error("hz_eqerror: bad arguments"); return HZ_ERR_INVALID_ARG; }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return c->dtype == HZ_C64 ? eqerror_t<float>(c, u_ref, u, src_xyz, npml_mask, ball_cells, err_out, s)
+                            : eqerror_t<double>(c, u_ref, u, src_xyz, npml_mask, ball_cells, err_out, s);
+}
+
+extern "C" hz_status hz_table_dispersion(const hz_table* t, int nG, const double* G, int nang, const double* theta,
+                                         const double* phi, double* vtilde, void* stream) {
+  if (!t || nG < 1 || nang < 1 || !G || !theta || !phi || !vtilde) { set_error("hz_table_dispersion: bad arguments"); return HZ_ERR_INVALID_ARG; }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // class weights at each G: clamped linear interpolation of the table's free weights (A13)
+  const Table& T = t->t;
+  std::vector<double> w7(7 * (size_t)nG), gv(G, G + nG);
+  for (int i = 0; i < nG; i++) {
+    if (!(G[i] > 0) || !std::isfinite(G[i])) { set_error("hz_table_dispersion: G must be finite and > 0"); return HZ_ERR_DOMAIN; }
+    double u[5];
+    if (T.n_g == 1) {
+      for (int k = 0; k < 5; k++) u[k] = T.rows5[k];
+    } else {
+      const double gmax = T.g_min + T.dg * (T.n_g - 1);
+      const double sidx = (std::fmin(std::fmax(G[i], T.g_min), gmax) - T.g_min) / T.dg;
+      const int ii = std::min((int)std::floor(sidx), T.n_g - 2);
+      const double tau = sidx - ii;
+      for (int k = 0; k < 5; k++) u[k] = (1.0 - tau) * T.rows5[5 * ii + k] + tau * T.rows5[5 * (ii + 1) + k];
+    }
+    double* o = &w7[7 * (size_t)i];
+    o[0] = u[0];
+    o[1] = u[1];
+    o[2] = 1.0 - u[0] - u[1];
+    o[3] = u[2];
+    o[4] = 6.0 * u[3];
+    o[5] = 12.0 * u[4];
+    o[6] = 1.0 - o[3] - o[4] - o[5];
+  }
+  DBuf dw, dg, dt, dp, dout;
+  HZ_CUDA(dw.ensure(w7.size() * sizeof(double)));
+  HZ_CUDA(dg.ensure(gv.size() * sizeof(double)));
+  HZ_CUDA(dt.ensure(sizeof(double) * nang));
+  HZ_CUDA(dp.ensure(sizeof(double) * nang));
+  HZ_CUDA(dout.ensure(sizeof(double) * (size_t)nG * nang));
+  HZ_CUDA(cudaMemcpyAsync(dw.p, w7.data(), w7.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  HZ_CUDA(cudaMemcpyAsync(dg.p, gv.data(), gv.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  HZ_CUDA(cudaMemcpyAsync(dt.p, theta, sizeof(double) * nang, cudaMemcpyHostToDevice, s));
+  HZ_CUDA(cudaMemcpyAsync(dp.p, phi, sizeof(double) * nang, cudaMemcpyHostToDevice, s));
+  HZ_CUDA(launch_dispersion(dw.as<double>(), dg.as<double>(), nG, dt.as<double>(), dp.as<double>(), nang, dout.as<double>(), s));
+  count_launch();
+  HZ_CUDA(cudaMemcpyAsync(vtilde, dout.p, sizeof(double) * (size_t)nG * nang, cudaMemcpyDefault, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  return HZ_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
 // (4) batched BiCGSTAB (north star (3); reading A21)
 // ---------------------------------------------------------------------------------------------
 namespace {

@@ -673,6 +673,92 @@ cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s) {
 template cudaError_t launch_record<float>(const ApplyParams<float>&, float*, cudaStream_t);
 template cudaError_t launch_record<double>(const ApplyParams<double>&, double*, cudaStream_t);
 
+// =============================================================================================
+// eqerror (reading A20): per-block partial sums (fp64) of W|Re d|, W|Im d|, W|Re ref|,
+// W|Im ref| over the owned points at least `npml` nodes from every face and more than `ball` nodes
+// from the source, W = h · distance; a fixed-order host sum finishes the reduction.
+// =============================================================================================
+template <typename R>
+__global__ void eqerror_kernel(const typename Cx<R>::T* __restrict__ uref, const typename Cx<R>::T* __restrict__ u,
+                               int nx, int ny, int nzl, int z0, int nzg, long long xs, long long ys, long long zs,
+                               double h, int npml, double ball, double* __restrict__ partials) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const long long plane = (long long)nx * ny;
+  const long long n = (long long)nzl * plane;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long long)gridDim.x * blockDim.x) {
+    const int zl = (int)(idx / plane);
+    const int rem = (int)(idx - (long long)zl * plane);
+    const int y = rem / nx, x = rem - y * nx;
+    const int zg = z0 + zl;
+    if (x < npml || x >= nx - npml || y < npml || y >= ny - npml || zg < npml || zg >= nzg - npml) continue;
+    const double dx = (double)(x - xs), dy = (double)(y - ys), dz = (double)(zg - zs);
+    const double d = sqrt(dx * dx + dy * dy + dz * dz);
+    if (!(d > ball)) continue;
+    const double W = h * d;
+    const typename Cx<R>::T a = uref[plane + idx], b = u[plane + idx];
+    acc[0] += fabs(W * ((double)a.x - (double)b.x));
+    acc[1] += fabs(W * ((double)a.y - (double)b.y));
+    acc[2] += fabs(W * (double)a.x);
+    acc[3] += fabs(W * (double)a.y);
+  }
+  __shared__ double red[8][4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) v += red[w][threadIdx.x];
+    partials[blockIdx.x * 4 + threadIdx.x] = v;
+  }
+}
+
+template <typename R>
+cudaError_t launch_eqerror(const typename Cx<R>::T* uref, const typename Cx<R>::T* u, int nx, int ny, int nzl, int z0,
+                           int nzg, const long long* src, double h, int npml, double ball, double* partials, int nblocks,
+                           cudaStream_t s) {
+  eqerror_kernel<R><<<nblocks, 256, 0, s>>>(uref, u, nx, ny, nzl, z0, nzg, src[0], src[1], src[2], h, npml, ball, partials);
+  return cudaGetLastError();
+}
+template cudaError_t launch_eqerror<float>(const float2*, const float2*, int, int, int, int, int, const long long*, double,
+                                           int, double, double*, int, cudaStream_t);
+template cudaError_t launch_eqerror<double>(const double2*, const double2*, int, int, int, int, int, const long long*,
+                                            double, int, double, double*, int, cudaStream_t);
+
+// =============================================================================================
+// Plane-wave dispersion of the stencil: vtilde = G/(√(2J) π) √R with
+//   R = ws1(3−C) + (ws2/3)(6−C−B) + (ws3/2)(3−3A+B−C),  J = μ0 + 2μ1 C + 4μ2 B + 8μ3 A
+//   A = cos a cos b cos c, B = Σ pairwise products, C = Σ cosines; (a, b, c) = 2π/G (cosφ cosθ,
+//   cosφ sinθ, sinφ).  w7[i] = (ws1, ws2, ws3, wm0, wm1, wm2, wm3) at G[i]; fp64.
+// =============================================================================================
+__global__ void dispersion_kernel(const double* __restrict__ w7, const double* __restrict__ G, int nG,
+                                  const double* __restrict__ theta, const double* __restrict__ phi, int nang,
+                                  double* __restrict__ out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)nG * nang) return;
+  const int i = (int)(t / nang), j = (int)(t - (long long)i * nang);
+  const double g = G[i], k = 2.0 * M_PI / g;
+  const double a = k * cos(phi[j]) * cos(theta[j]), b = k * cos(phi[j]) * sin(theta[j]), c = k * sin(phi[j]);
+  const double ca = cos(a), cb = cos(b), cc = cos(c);
+  const double A = ca * cb * cc, B = ca * cb + ca * cc + cb * cc, C = ca + cb + cc;
+  const double* w = w7 + 7 * i;
+  const double Rr = w[0] * (3.0 - C) + w[1] / 3.0 * (6.0 - C - B) + 0.5 * w[2] * (3.0 - 3.0 * A + B - C);
+  const double mu0 = w[3], mu1 = w[4] / 6.0, mu2 = w[5] / 12.0, mu3 = w[6] / 8.0;
+  const double J = mu0 + 2.0 * mu1 * C + 4.0 * mu2 * B + 8.0 * mu3 * A;
+  out[t] = g / (sqrt(2.0 * J) * M_PI) * sqrt(Rr);
+}
+cudaError_t launch_dispersion(const double* w7, const double* G, int nG, const double* theta, const double* phi, int nang,
+                              double* out, cudaStream_t s) {
+  const long long n = (long long)nG * nang;
+  dispersion_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w7, G, nG, theta, phi, nang, out);
+  return cudaGetLastError();
+}
+
 template <typename R>
 cudaError_t launch_gam_field(const ApplyParams<R>& p, R* out, cudaStream_t s) {
   const size_t smem = (size_t)p.n_g * TAB_STRIDE * sizeof(R);

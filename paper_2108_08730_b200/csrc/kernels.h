@@ -58,6 +58,12 @@ template <typename R> cudaError_t launch_winv(const R* v, R* w, long long n, cud
 template <typename R> cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s);
 template <typename R> cudaError_t launch_gam_field(const ApplyParams<R>& p, R* out, cudaStream_t s);
 template <typename R>
+cudaError_t launch_eqerror(const typename Cx<R>::T* uref, const typename Cx<R>::T* u, int nx, int ny, int nzl, int z0,
+                           int nzg, const long long* src, double h, int npml, double ball, double* partials, int nblocks,
+                           cudaStream_t s);
+cudaError_t launch_dispersion(const double* w7, const double* G, int nG, const double* theta, const double* phi, int nang,
+                              double* out, cudaStream_t s);
+template <typename R>
 cudaError_t launch_sources(const ApplyParams<R>& p, int nsrc, const long long* nodes, const double* amps,
                            int consistent, R ih3, typename Cx<R>::T* b, cudaStream_t s);
 template <typename R>

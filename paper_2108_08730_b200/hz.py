@@ -86,6 +86,9 @@ _sigs = {
     "hz_solve": (ct.c_int, [_vp, _vp, _vp, ct.c_int, _P(hz_solve_opts), _P(ct.c_double),
                             _P(ct.c_int), _P(hz_solve_stats), _vp]),
     "hz_point_sources": (ct.c_int, [_vp, ct.c_int, _P(ct.c_longlong), _P(ct.c_double), ct.c_int, _vp, _vp]),
+    "hz_eqerror": (ct.c_int, [_vp, _vp, _vp, _P(ct.c_longlong), ct.c_int, ct.c_double, _P(ct.c_double), _vp]),
+    "hz_table_dispersion": (ct.c_int, [_vp, ct.c_int, _P(ct.c_double), ct.c_int, _P(ct.c_double), _P(ct.c_double),
+                                       _P(ct.c_double), _vp]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
@@ -292,3 +295,26 @@ def hz_point_sources(c: Coeffs, nodes, b, amps=None, consistent=True, stream=Non
     _check(_lib.hz_point_sources(c._h, n.shape[0], n.ctypes.data_as(_P(ct.c_longlong)),
                                  a.ctypes.data_as(_P(ct.c_double)) if a is not None else None,
                                  1 if consistent else 0, _ptr(b), _stream_ptr(stream)), "hz_point_sources")
+
+
+def hz_eqerror(c: Coeffs, u_ref, u, src_xyz, npml_mask: int, ball_cells: float = 2.0, stream=None) -> float:
+    """The paper's err (reading A20) between two slab wavefields (see include/hz.h)."""
+    src = (ct.c_longlong * 3)(*[int(t) for t in src_xyz])
+    out = ct.c_double()
+    _check(_lib.hz_eqerror(c._h, _ptr(u_ref), _ptr(u), src, npml_mask, ball_cells, ct.byref(out), _stream_ptr(stream)),
+           "hz_eqerror")
+    return out.value
+
+
+def hz_table_dispersion(table: Table, G, theta, phi, stream=None) -> np.ndarray:
+    """vtilde[len(G)][len(theta)] of the table's stencil at the given G and angles (radians), on the device."""
+    G = np.ascontiguousarray(G, dtype=np.float64).ravel()
+    th = np.ascontiguousarray(theta, dtype=np.float64).ravel()
+    ph = np.ascontiguousarray(phi, dtype=np.float64).ravel()
+    if th.shape != ph.shape:
+        raise ValueError("theta and phi must have the same length")
+    out = np.zeros((G.size, th.size))
+    _check(_lib.hz_table_dispersion(table._h, G.size, G.ctypes.data_as(_P(ct.c_double)), th.size,
+                                    th.ctypes.data_as(_P(ct.c_double)), ph.ctypes.data_as(_P(ct.c_double)),
+                                    out.ctypes.data_as(_P(ct.c_double)), _stream_ptr(stream)), "hz_table_dispersion")
+    return out

@@ -347,3 +347,37 @@ def test_gam_record_sources_and_decomposition(hz, ctx, table, ga_table):
         torch.cuda.synchronize()
         out[:, z0:z1] = aud[:, 1:-1].cpu().numpy()
     assert np.array_equal(out, full)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_eqerror_on_device(hz, ctx, table, dtype):
+    """hz_eqerror (reading A20) equals the oracle's metric on the same two fields."""
+    from oracle import metrics
+    rng = np.random.default_rng(82)
+    nz, ny, nx, h, npml = 13, 17, 21, 25.0, 3
+    v = rng.uniform(1500.0, 4500.0, (nz, ny, nx))
+    C = assemble(hz, ctx, table, v, h, 7.0, npml, dtype)
+    a = synth.random_field((1, nz, ny, nx), seed=15)[0].astype(cdt(dtype))
+    b = (a + 0.05 * synth.random_field((1, nz, ny, nx), seed=16)[0]).astype(cdt(dtype))
+    src = (10, 8, 6)
+    ua, ub = C.alloc_field(1), C.alloc_field(1)
+    ua[0, 1:-1] = torch.from_numpy(a).cuda()
+    ub[0, 1:-1] = torch.from_numpy(b).cuda()
+    got = hz.hz_eqerror(C, ua, ub, src, npml, 2.0)
+    ref = metrics.eqerror(a.astype(np.complex128), b.astype(np.complex128), metrics.distance(v.shape, src, h),
+                          metrics.interior_mask(v.shape, npml, src))
+    assert abs(got - ref) <= 1e-12 * ref, (got, ref)
+
+
+def test_table_dispersion_on_device(hz, table, ga_table):
+    """hz_table_dispersion (P:129-160) equals the oracle's vtilde of the same interpolated weights;
+    the GA table stays within 1e-4 of 1 on G ∈ [4, 40] (north-star check 3)."""
+    from oracle import dispersion, weights
+    G = np.array([4.0, 4.05, 6.3, 12.0, 25.55, 40.0])
+    th, ph = np.meshgrid(np.radians(np.arange(0, 91, 15)), np.radians(np.arange(0, 46, 15)), indexing="ij")
+    got = hz.hz_table_dispersion(table, G, th.ravel(), ph.ravel())
+    u5, _ = weights.lookup(ga_table, G)
+    w7 = weights.u5_to_w7(u5)
+    ref = np.stack([dispersion.vtilde(w7[i], G[i], th.ravel(), ph.ravel()) for i in range(len(G))])
+    assert np.allclose(got, ref, rtol=0, atol=1e-12)
+    assert np.abs(got - 1.0).max() <= 1e-4
