@@ -271,12 +271,28 @@ __global__ void bicg_s_kernel(VecParams<R> q) {
   }
   const C a = to_c<R>(alpha);
   const long long off = (long long)rhs * q.fstride + q.plane;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < q.n; i += (long long)gridDim.x * blockDim.x) {
-    const C r = q.r[off + i], v = q.v[off + i];
-    C s;
-    s.x = r.x - (a.x * v.x - a.y * v.y);
-    s.y = r.y - (a.x * v.y + a.y * v.x);
-    q.r[off + i] = s;
+  // 4 independent elements per thread and step: 8 loads in flight per thread (the kernel is HBM-bound)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < q.n; i0 += 4 * stride) {
+    C r[4], v[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const long long i = i0 + k * stride;
+      if (i < q.n) {
+        r[k] = q.r[off + i];
+        v[k] = q.v[off + i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const long long i = i0 + k * stride;
+      if (i < q.n) {
+        C s;
+        s.x = r[k].x - (a.x * v[k].x - a.y * v[k].y);
+        s.y = r[k].y - (a.x * v[k].y + a.y * v[k].x);
+        q.r[off + i] = s;
+      }
+    }
   }
 }
 
@@ -315,15 +331,34 @@ __global__ void __launch_bounds__(NT) bicg_update_kernel(VecParams<R> q) {
   const C a = to_c<R>(alpha), w = to_c<R>(omega), bt = to_c<R>(beta);
   const long long off = (long long)rhs * q.fstride + q.plane;
   double part[1] = {0.0};
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < q.n; i += (long long)gridDim.x * blockDim.x) {
-    const C s = q.r[off + i], t = q.t[off + i], pp = q.p[off + i], vv = q.v[off + i];
-    C xx = q.x[off + i];
+  // two independent elements per thread and step (12 loads in flight per thread; HBM-bound)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < q.n; i0 += 2 * stride) {
+  C S_[2], T_[2], P_[2], V_[2], X_[2], L_[2];
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    const long long i = i0 + k * stride;
+    if (i < q.n) {
+      S_[k] = q.r[off + i];
+      T_[k] = q.t[off + i];
+      P_[k] = q.p[off + i];
+      V_[k] = q.v[off + i];
+      X_[k] = q.x[off + i];
+      if (q.xlo != nullptr) L_[k] = q.xlo[off + i];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    const long long i = i0 + k * stride;
+    if (i >= q.n) continue;
+    const C s = S_[k], t = T_[k], pp = P_[k], vv = V_[k];
+    C xx = X_[k];
     // x += α p + ω s; with q.xlo the iterate is the double-word x + xlo (compensated update)
     C dx;
     dx.x = (a.x * pp.x - a.y * pp.y) + (w.x * s.x - w.y * s.y);
     dx.y = (a.x * pp.y + a.y * pp.x) + (w.x * s.y + w.y * s.x);
     if (q.xlo != nullptr) {
-      C lo = q.xlo[off + i];
+      C lo = L_[k];
       two_sum(xx.x, dx.x + lo.x, xx.x, lo.x);
       two_sum(xx.y, dx.y + lo.y, xx.y, lo.y);
       q.xlo[off + i] = lo;
@@ -346,6 +381,7 @@ __global__ void __launch_bounds__(NT) bicg_update_kernel(VecParams<R> q) {
     q.r[off + i] = r;
     q.p[off + i] = pn;
     part[0] += (double)r.x * (double)r.x + (double)r.y * (double)r.y;
+  }
   }
   const int nblocks = gridDim.x;
   block_grid_reduce<1, NT>(part, q.partials + (long long)rhs * nblocks, q.dotR + 3 * rhs, q.tickets + rhs, nblocks,
