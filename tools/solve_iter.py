@@ -17,6 +17,7 @@ ci = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 nrhs = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 300
 dt = sys.argv[4] if len(sys.argv) > 4 else "c64"
+check_every = int(sys.argv[5]) if len(sys.argv) > 5 else 10
 cfg = synth.get_config(ci)
 rd = np.float32 if dt == "c64" else np.float64
 v = torch.from_numpy(synth.velocity_model(cfg).astype(rd)).cuda()
@@ -32,7 +33,7 @@ for timing in (1, 0, 0):
     x = C.alloc_field(nrhs)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    st, rel, its, stt = hz.hz_solve(C, b, x, rtol=1e-14, max_iter=iters, timing=bool(timing))
+    st, rel, its, stt = hz.hz_solve(C, b, x, rtol=1e-14, max_iter=iters, timing=bool(timing), check_every=check_every)
     torch.cuda.synchronize()
     res.append((time.perf_counter() - t0, stt))
 wall = min(r[0] for r in res[1:])
