@@ -183,12 +183,13 @@ typedef struct {
 
 typedef struct {
   double apply_ms_total;    /* sum of operator-apply kernel durations (timing = 1)               */
-  long long apply_launches; /* number of operator-apply kernel launches                          */
+  long long apply_launches; /* number of operator applies (one kernel launch each for complex64,
+                               two for the register-path kernels: complex128, fp64 residual)      */
   long long kernel_launches;/* all libhz kernel launches during the call                         */
-  double apply_bytes_total; /* algorithmic HBM bytes of all apply launches: per launch
+  double apply_bytes_total; /* algorithmic HBM bytes of all applies: per apply
                                n_points * (sizeof(real) + n_active_rhs * k * sizeof(complex)),
                                k = fields read/written per RHS by the launch's epilogue          */
-  double apply_points_total;/* grid points x active RHS processed by all apply launches          */
+  double apply_points_total;/* grid points x active RHS processed by all applies                  */
   int replacements;         /* residual replacements performed                                   */
   int restarts;             /* breakdown restarts                                                */
   int iterations;           /* BiCGSTAB iterations of the batch (max over RHS)                   */
