@@ -381,3 +381,24 @@ def test_table_dispersion_on_device(hz, table, ga_table):
     ref = np.stack([dispersion.vtilde(w7[i], G[i], th.ravel(), ph.ravel()) for i in range(len(G))])
     assert np.allclose(got, ref, rtol=0, atol=1e-12)
     assert np.abs(got - 1.0).max() <= 1e-4
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_apply_random_shapes(hz, ctx, table, ga_table, seed):
+    """Planner / kernel edge cases: random small grids (down to 3 nodes per axis, odd and even sizes,
+    PML widths 0..3, one-node PML-free bands), 1–5 RHS (one-RHS and RHS-pair CTAs, idle pair slots),
+    both dtypes and both mass forms — full oracle comparison of every point."""
+    rng = np.random.default_rng(1000 + seed)
+    nz, ny, nx = (int(t) for t in rng.integers(3, 24, 3))
+    npml = int(rng.integers(0, 4))
+    nrhs = int(rng.integers(1, 6))
+    dtype = "c64" if seed % 2 == 0 else "c128"
+    mass = "colloc" if seed % 3 == 0 else "eq8"
+    v = rng.uniform(1500.0, 4500.0, (nz, ny, nx))
+    u = synth.random_field((nrhs, nz, ny, nx), seed=200 + seed)
+    C = assemble(hz, ctx, table, v, 25.0, 7.0, npml, dtype, mass=mass)
+    got = gpu_apply(hz, C, u)
+    ref = op.apply(op.assemble(oracle_problem(v, 25.0, 7.0, npml, ga_table, dtype, mass=mass)), u)
+    err = np.abs(got - ref) / (np.abs(ref) + 1e-3 * np.abs(ref).max())
+    assert rel(got, ref) <= TOL[dtype] and err.max() <= (1e-4 if dtype == "c64" else 1e-10), \
+        ((nz, ny, nx), npml, nrhs, rel(got, ref), np.unravel_index(err.argmax(), err.shape))
