@@ -155,3 +155,28 @@ def test_solver_edge_cases(hz, ctx, table):
     st3, rel3, its3, _ = hz.hz_solve(C, b, x3, rtol=1e-6)
     assert st2 == hz.HZ_OK and np.array_equal(its2, its3)
     assert np.array_equal(xh, x3.cpu().numpy())
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_solve_random_small(hz, ctx, table, ga_table, seed):
+    """Batched solve on random small models (RHS converging at different iterations, RHS pairs with a
+    retired member, odd RHS counts): every returned x meets rtol on the ORACLE matrix's residual."""
+    rng = np.random.default_rng(3000 + seed)
+    nz, ny, nx = (int(t) for t in rng.integers(14, 22, 3))
+    npml = 3
+    nrhs = int(rng.integers(2, 6))
+    v = rng.uniform(1500.0, 3500.0, (nz, ny, nx)).astype(np.float32)
+    C = hz.hz_assemble_coeffs(ctx, nx, ny, nz, 25.0, torch.from_numpy(v).cuda(), 5.0, table, npml=npml)
+    nodes = np.stack([rng.integers(npml + 1, n - npml - 1, nrhs) for n in (nx, ny, nz)], axis=1)
+    b = C.alloc_field(nrhs)
+    hz.hz_point_sources(C, nodes, b)
+    x = C.alloc_field(nrhs)
+    st, relres, its, _ = hz.hz_solve(C, b, x, rtol=1e-6, max_iter=20000)
+    assert st == hz.HZ_OK and np.all(relres <= 1e-6), (st, relres, its)
+    P = op.Problem(v.astype(np.float64), 25.0, 5.0, npml, ga_table)
+    A = op.assemble(P)
+    B = op.point_sources(P, nodes)
+    X = x[:, 1:-1].cpu().numpy().astype(np.complex128)
+    for r in range(nrhs):
+        br = B[r].ravel()
+        assert np.linalg.norm(br - A @ X[r].ravel()) / np.linalg.norm(br) <= 1.5e-6, r
