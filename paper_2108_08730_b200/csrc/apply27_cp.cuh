@@ -214,10 +214,12 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
   int goff[KS];        // in-plane element offset y·nx + x (0 outside the grid)
   uint32_t sdst[KS];   // byte offset of the w element in a stage (~0u: no element for this slot)
   bool gout[KS];       // element outside the grid: zero fill
+  // e / P by a float reciprocal: exact here (e < CP_HALO, P ≤ 66: the rounding error ≪ 0.5 / P)
+  const float invP = 1.0f / (float)P;
 #pragma unroll
   for (int k = 0; k < KS; k++) {
     const int e = tid + k * NT;
-    const int r = e / P, cc = e - r * P;
+    const int r = (int)(((float)e + 0.5f) * invP), cc = e - r * P;
     const int gx = X0 - 1 + cc, gy = Y0 - 1 + r;
     const bool in_tile = r < ROWS;
     const bool gin = in_tile && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
@@ -259,7 +261,7 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
   // ---- this thread's position (threads past tx·TY/NY duplicate position 0 and never store)
   const bool pos_ok = tid < tx * (TY / NY);
   const int pt = pos_ok ? tid : 0;
-  const int s_ = pt / tx, c_ = pt - s_ * tx;
+  const int s_ = (int)(((float)pt + 0.5f) / (float)tx), c_ = pt - s_ * tx;   // exact: pt < 512, tx ≤ 64
   const int x = X0 + c_;
   const int yl0 = Y0 + NY * s_;
   const bool x_ok = pos_ok && x >= X0n && x < X1n;
