@@ -222,6 +222,12 @@ hz_status hz_point_sources(const hz_coeffs* c, int nsrc, const long long* node_x
  * (theta[j], phi[j]) in radians, evaluated on the device in fp64: vtilde[i*nang + j] (host or device
  * memory; G, theta, phi are host arrays).  HZ_ERR_DOMAIN for G <= 0.
  * ------------------------------------------------------------------------------------------- */
+/* hz_export_matrix: the explicit impedance matrix rows of this rank's slab (the paper's
+ * sparse direct-solver setting): for every owned node n (C order [nz_local][ny][nx]) its 27 entries
+ * A[n, n+d] (d in C order dz, dy, dx in {-1,0,1}) in the per-axis form (A6, A8; the coeffs' mass form
+ * and weight rule), cols[n][27] = global node index (z*ny + y)*nx + x, or -1 with value 0 outside the
+ * grid (Dirichlet, A9); vals[n][27] complex of the dtype.  Host or device arrays (caller-owned). */
+hz_status hz_export_matrix(const hz_coeffs* c, long long* cols, void* vals, void* stream);
 hz_status hz_eqerror(const hz_coeffs* c, const void* u_ref, const void* u, const long long src_xyz[3],
                      int npml_mask, double ball_cells, double* err_out, void* stream);
 hz_status hz_table_dispersion(const hz_table* t, int nG, const double* G, int nang, const double* theta,

@@ -1045,6 +1045,31 @@ extern "C" hz_status hz_eqerror(const hz_coeffs* c, const void* u_ref, const voi
                             : eqerror_t<double>(c, u_ref, u, src_xyz, npml_mask, ball_cells, err_out, s);
 }
 
+template <typename R>
+static hz_status matrix_t(const hz_coeffs* c, long long* cols, void* vals, cudaStream_t s) {
+  typedef typename Cx<R>::T C;
+  const size_t n = (size_t)c->grid.nz_local * c->plane() * 27;
+  DBuf dc, dv;
+  long long* cd = cols;
+  void* vd = vals;
+  const bool cdev = is_device_ptr(cols), vdev = is_device_ptr(vals);
+  if (!cdev) { HZ_CUDA(dc.ensure(n * sizeof(long long))); cd = dc.as<long long>(); }
+  if (!vdev) { HZ_CUDA(dv.ensure(n * sizeof(C))); vd = dv.p; }
+  ApplyParams<R> p = make_params<R>(c);
+  HZ_CUDA(launch_matrix<R>(p, c->mass == HZ_MASS_COLLOC, cd, reinterpret_cast<C*>(vd), s));
+  count_launch();
+  if (!cdev) HZ_CUDA(cudaMemcpyAsync(cols, cd, n * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  if (!vdev) HZ_CUDA(cudaMemcpyAsync(vals, vd, n * sizeof(C), cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  return HZ_OK;
+}
+
+extern "C" hz_status hz_export_matrix(const hz_coeffs* c, long long* cols, void* vals, void* stream) {
+  if (!c || !cols || !vals) { set_error("hz_export_matrix: bad arguments"); return HZ_ERR_INVALID_ARG; }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return c->dtype == HZ_C64 ? matrix_t<float>(c, cols, vals, s) : matrix_t<double>(c, cols, vals, s);
+}
+
 extern "C" hz_status hz_table_dispersion(const hz_table* t, int nG, const double* G, int nang, const double* theta,
                                          const double* phi, double* vtilde, void* stream) {
   if (!t || nG < 1 || nang < 1 || !G || !theta || !phi || !vtilde) { set_error("hz_table_dispersion: bad arguments"); return HZ_ERR_INVALID_ARG; }

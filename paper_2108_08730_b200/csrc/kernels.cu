@@ -767,6 +767,85 @@ template cudaError_t launch_eqerror<double>(const double2*, const double2*, int,
                                             double, int, double, double*, int, cudaStream_t);
 
 // =============================================================================================
+// Explicit matrix export (the paper's direct-solver setting): the 27 entries of
+// every owned row in the per-axis form of the oracle (readings A6, A8; Eq. 8 / Eq. "10" mass; GA or
+// GAm weights) — ELL layout, column = global node index or -1 outside the grid (Dirichlet, A9).
+//   A[n, n+d] = ω² μ_class(d) w_{n+d}  (Eq. 8; w_n for Eq. "10")  +  Σ_a D_a(n_a, d_a) T(d⊥; t(n))
+// =============================================================================================
+template <typename R>
+__global__ void matrix_kernel(ApplyParams<R> p, bool colloc, long long* __restrict__ cols,
+                              typename Cx<R>::T* __restrict__ vals) {
+  typedef typename Cx<R>::T C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* tab = reinterpret_cast<R*>(smem_raw);
+  for (int i = threadIdx.x; i < p.n_g * TAB_STRIDE; i += blockDim.x) tab[i] = p.tab[i];
+  __syncthreads();
+  const long long n = (long long)p.nzl * p.plane;
+  const R ih2 = p.ih2;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long long)gridDim.x * blockDim.x) {
+    const int zl = (int)(idx / p.plane);
+    const int rem = (int)(idx - (long long)zl * p.plane);
+    const int y = rem / p.nx, x = rem - y * p.nx;
+    const int zg = p.z0 + zl;
+    const long long e = p.plane + idx;   // storage element of the row
+    R t1, t2, mu0, mu1, mu2;
+    if (p.gam != nullptr) {
+      t1 = p.gam[e], t2 = p.gam[p.fstride + e], mu0 = p.gam[2 * p.fstride + e];
+      mu1 = p.gam[3 * p.fstride + e], mu2 = p.gam[4 * p.fstride + e];
+    } else {
+      interp_weights<R>(p.v[e], tab, p.n_g, p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
+    }
+    const R t0 = R(1) - R(4) * (t1 + t2);
+    const R mu[4] = {mu0, mu1, mu2, (R(1) - mu0 - R(6) * mu1 - R(12) * mu2) * R(0.125)};
+    const R tw[3] = {t0, t1, t2};
+    // stretched 1-D second differences: a± = h⁻² + δ± (the device holds δ)
+    const int ia[3] = {x, y, zg};
+    C am[3], ap[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      const C dm = p.dm[a][ia[a]], dpp = p.dp[a][ia[a]];
+      am[a] = make_cx(dm.x + ih2, dm.y);
+      ap[a] = make_cx(dpp.x + ih2, dpp.y);
+    }
+    const R wn = p.w[e];
+    for (int d = 0; d < 27; d++) {
+      const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+      const long long o = idx * 27 + d;
+      const int xx = x + dx, yy = y + dy, zz = zg + dz;
+      if (xx < 0 || xx >= p.nx || yy < 0 || yy >= p.ny || zz < 0 || zz >= p.nzg) {
+        cols[o] = -1;
+        vals[o] = make_cx(R(0), R(0));
+        continue;
+      }
+      const int cls = (dx != 0) + (dy != 0) + (dz != 0);
+      const R wnb = colloc ? wn : p.w[e + (long long)dz * p.plane + (long long)dy * p.nx + dx];
+      C v = make_cx(p.w2 * mu[cls] * wnb, R(0));
+      const int dd[3] = {dx, dy, dz};
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        const int pa = dd[(a + 1) % 3], qa = dd[(a + 2) % 3];
+        const R T = tw[(pa != 0) + (qa != 0)];
+        const C D = dd[a] < 0 ? am[a] : (dd[a] > 0 ? ap[a] : make_cx(-am[a].x - ap[a].x, -am[a].y - ap[a].y));
+        v.x += D.x * T;
+        v.y += D.y * T;
+      }
+      cols[o] = ((long long)zz * p.ny + yy) * p.nx + xx;
+      vals[o] = v;
+    }
+  }
+}
+
+template <typename R>
+cudaError_t launch_matrix(const ApplyParams<R>& p, bool colloc, long long* cols, typename Cx<R>::T* vals, cudaStream_t s) {
+  const size_t smem = (size_t)p.n_g * TAB_STRIDE * sizeof(R);
+  cudaFuncSetAttribute(matrix_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  matrix_kernel<R><<<148 * 4, 256, smem, s>>>(p, colloc, cols, vals);
+  return cudaGetLastError();
+}
+template cudaError_t launch_matrix<float>(const ApplyParams<float>&, bool, long long*, float2*, cudaStream_t);
+template cudaError_t launch_matrix<double>(const ApplyParams<double>&, bool, long long*, double2*, cudaStream_t);
+
+// =============================================================================================
 // Plane-wave dispersion of the stencil: vtilde = G/(√(2J) π) √R with
 //   R = ws1(3−C) + (ws2/3)(6−C−B) + (ws3/2)(3−3A+B−C),  J = μ0 + 2μ1 C + 4μ2 B + 8μ3 A
 //   A = cos a cos b cos c, B = Σ pairwise products, C = Σ cosines; (a, b, c) = 2π/G (cosφ cosθ,

@@ -61,6 +61,8 @@ template <typename R>
 cudaError_t launch_eqerror(const typename Cx<R>::T* uref, const typename Cx<R>::T* u, int nx, int ny, int nzl, int z0,
                            int nzg, const long long* src, double h, int npml, double ball, double* partials, int nblocks,
                            cudaStream_t s);
+template <typename R>
+cudaError_t launch_matrix(const ApplyParams<R>& p, bool colloc, long long* cols, typename Cx<R>::T* vals, cudaStream_t s);
 cudaError_t launch_dispersion(const double* w7, const double* G, int nG, const double* theta, const double* phi, int nang,
                               double* out, cudaStream_t s);
 template <typename R>

@@ -86,6 +86,7 @@ _sigs = {
     "hz_solve": (ct.c_int, [_vp, _vp, _vp, ct.c_int, _P(hz_solve_opts), _P(ct.c_double),
                             _P(ct.c_int), _P(hz_solve_stats), _vp]),
     "hz_point_sources": (ct.c_int, [_vp, ct.c_int, _P(ct.c_longlong), _P(ct.c_double), ct.c_int, _vp, _vp]),
+    "hz_export_matrix": (ct.c_int, [_vp, _P(ct.c_longlong), _vp, _vp]),
     "hz_eqerror": (ct.c_int, [_vp, _vp, _vp, _P(ct.c_longlong), ct.c_int, ct.c_double, _P(ct.c_double), _vp]),
     "hz_table_dispersion": (ct.c_int, [_vp, ct.c_int, _P(ct.c_double), ct.c_int, _P(ct.c_double), _P(ct.c_double),
                                        _P(ct.c_double), _vp]),
@@ -318,3 +319,14 @@ def hz_table_dispersion(table: Table, G, theta, phi, stream=None) -> np.ndarray:
                                     th.ctypes.data_as(_P(ct.c_double)), ph.ctypes.data_as(_P(ct.c_double)),
                                     out.ctypes.data_as(_P(ct.c_double)), _stream_ptr(stream)), "hz_table_dispersion")
     return out
+
+
+def hz_export_matrix(c: Coeffs, stream=None):
+    """(cols [n][27] int64, vals [n][27] complex) of this rank's rows (see include/hz.h)."""
+    g = c.grid
+    n = g.nz_local * g.ny * g.nx
+    cols = np.empty((n, 27), dtype=np.int64)
+    vals = np.empty((n, 27), dtype=np.complex64 if c.dtype == HZ_C64 else np.complex128)
+    _check(_lib.hz_export_matrix(c._h, cols.ctypes.data_as(_P(ct.c_longlong)), vals.ctypes.data_as(_vp),
+                                 _stream_ptr(stream)), "hz_export_matrix")
+    return cols, vals
