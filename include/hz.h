@@ -59,8 +59,10 @@ typedef enum { HZ_C64 = 0, HZ_C128 = 1 } hz_dtype;
  * variant "Eq. 10". */
 typedef enum { HZ_MASS_EQ8 = 0, HZ_MASS_COLLOC = 1 } hz_mass;
 /* Weight rule of a row: GA = the weights tabulated at the row's own local G; GAm = the mean of
- * the weights tabulated at the row's 27 stencil nodes (in-grid nodes only; reading A19). */
-typedef enum { HZ_RULE_GA = 0, HZ_RULE_GAM = 1 } hz_rule;
+ * the weights tabulated at the row's 27 stencil nodes (in-grid nodes only; reading A19).
+ * GA_RECORD = GA in "record mode": the per-point weights are stored once at assemble
+ * and read by every apply instead of being recomputed from v (same values; +20 / 40 B per point). */
+typedef enum { HZ_RULE_GA = 0, HZ_RULE_GAM = 1, HZ_RULE_GA_RECORD = 2 } hz_rule;
 
 typedef struct hz_ctx hz_ctx;
 typedef struct hz_table hz_table;
@@ -113,8 +115,9 @@ void hz_table_destroy(hz_table* t);
  * PML arrays (profile A7, per-axis stretching A8) and uploads the table.  The per-point
  * coefficients (G = v/(f h), lookup + interpolation, t0..t2, mu0..mu3) are
  * NOT stored: every apply recomputes them from v (fused mode, 4 bytes/point).  rule = HZ_RULE_GAM
- * instead stores the 27-node mean weights once ([5][nz_local+2][ny][nx] in the dtype's precision) and
- * the apply reads them (+20 / 40 bytes per point and apply).
+ * (HZ_RULE_GA_RECORD) instead stores the 27-node mean (the row's own) weights once
+ * ([5][nz_local+2][ny][nx] in the dtype's precision) and the apply reads them (+20 / 40 bytes per
+ * point and apply).
  * grid: this rank's slab of the global grid.  pml->v_pml <= 0 selects max(v) over all ranks.
  * With nranks > 1 the table rows of rank 0 are broadcast so every rank uses identical weights.
  * Returns HZ_WARN_CLAMPED (outputs valid) when *n_clamped > 0.

@@ -372,7 +372,7 @@ ApplyParams<R, S> make_params(const hz_coeffs* c) {
   p.nchunks = c->nchunks;
   p.v = c->v.as<S>();
   p.w = c->w.as<S>();
-  p.gam = c->rule == HZ_RULE_GAM ? c->gam.as<S>() : nullptr;
+  p.gam = c->rule != HZ_RULE_GA ? c->gam.as<S>() : nullptr;
   p.tab = sizeof(R) == 4 ? c->tab_f.as<R>() : c->tab_d.as<R>();
   p.ctab = sizeof(R) == 4 ? c->ctab_f.as<R>() : c->ctab_d.as<R>();
   p.tab_lo = c->tab_lo;
@@ -827,11 +827,11 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
   }
   if (sizeof(R) == 4) HZ_TRY(cp_geometry(c.get()));
   // ---- GAm: the 27-node mean weights of every owned row, once (A19)
-  if (rule == HZ_RULE_GAM) {
+  if (rule != HZ_RULE_GA) {
     HZ_CUDA(c->gam.ensure(5 * (size_t)c->fstride() * sizeof(R)));
     HZ_CUDA(cudaMemsetAsync(c->gam.p, 0, 5 * (size_t)c->fstride() * sizeof(R), s));
     ApplyParams<R> gp = make_params<R>(c.get());
-    HZ_CUDA(launch_gam_field<R>(gp, c->gam.as<R>(), s));
+    HZ_CUDA(launch_gam_field<R>(gp, c->gam.as<R>(), rule == HZ_RULE_GAM ? 1 : 0, s));
     count_launch();
     HZ_CUDA(cudaStreamSynchronize(s));
   }
@@ -862,7 +862,7 @@ hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, c
   if (table->t.n_g < 1) { set_error("hz_assemble_coeffs: empty table"); return HZ_ERR_INVALID_ARG; }
   if (ctx->nranks > 1 && g.nz_local < 1) { set_error("hz_assemble_coeffs: empty slab"); return HZ_ERR_INVALID_ARG; }
   if (cudaSetDevice(ctx->device) != cudaSuccess) { set_error("hz_assemble_coeffs: cudaSetDevice failed"); return HZ_ERR_CUDA; }
-  if (rule != HZ_RULE_GA && rule != HZ_RULE_GAM) { set_error("hz_assemble_coeffs: bad rule"); return HZ_ERR_INVALID_ARG; }
+  if (rule != HZ_RULE_GA && rule != HZ_RULE_GAM && rule != HZ_RULE_GA_RECORD) { set_error("hz_assemble_coeffs: bad rule"); return HZ_ERR_INVALID_ARG; }
   if (dtype == HZ_C64) return assemble_t<float>(ctx, grid, v, freq_hz, pml, table, mass, rule, out, n_clamped);
   if (dtype == HZ_C128) return assemble_t<double>(ctx, grid, v, freq_hz, pml, table, mass, rule, out, n_clamped);
   set_error("hz_assemble_coeffs: bad dtype");

@@ -50,9 +50,10 @@ __global__ void record_kernel(ApplyParams<R> p, R w2_over_1, R* __restrict__ rec
 // GAm rule (reading A19): per owned point, the mean of the interpolated free weights
 // (t1, t2, μ0, μ1, μ2) over the in-grid nodes of its 27-point stencil (v halo planes carry the
 // neighbouring slabs).  One-time, at assemble; out: [5][nzl+2][ny][nx] (halo planes not written).
+// radius 0 stores the row's own weights: the "record mode" of the GA rule.
 // =============================================================================================
 template <typename R>
-__global__ void gam_field_kernel(ApplyParams<R> p, R* __restrict__ out) {
+__global__ void gam_field_kernel(ApplyParams<R> p, R* __restrict__ out, int radius) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* tab = reinterpret_cast<R*>(smem_raw);
   for (int i = threadIdx.x; i < p.n_g * TAB_STRIDE; i += blockDim.x) tab[i] = p.tab[i];
@@ -64,12 +65,12 @@ __global__ void gam_field_kernel(ApplyParams<R> p, R* __restrict__ out) {
     const int y = rem / p.nx, x = rem - y * p.nx;
     R a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
     int cnt = 0;
-    for (int dz = -1; dz <= 1; dz++) {
+    for (int dz = -radius; dz <= radius; dz++) {
       const int zg = p.z0 + zl + dz;
       if (zg < 0 || zg >= p.nzg) continue;
-      for (int dy = -1; dy <= 1; dy++) {
+      for (int dy = -radius; dy <= radius; dy++) {
         if (y + dy < 0 || y + dy >= p.ny) continue;
-        for (int dx = -1; dx <= 1; dx++) {
+        for (int dx = -radius; dx <= radius; dx++) {
           if (x + dx < 0 || x + dx >= p.nx) continue;
           R t1, t2, mu0, mu1, mu2;
           interp_weights<R>(p.v[(long long)(zl + 1 + dz) * p.plane + (long long)(y + dy) * p.nx + (x + dx)], tab, p.n_g,
@@ -875,14 +876,14 @@ cudaError_t launch_dispersion(const double* w7, const double* G, int nG, const d
 }
 
 template <typename R>
-cudaError_t launch_gam_field(const ApplyParams<R>& p, R* out, cudaStream_t s) {
+cudaError_t launch_gam_field(const ApplyParams<R>& p, R* out, int radius, cudaStream_t s) {
   const size_t smem = (size_t)p.n_g * TAB_STRIDE * sizeof(R);
   cudaFuncSetAttribute(gam_field_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  gam_field_kernel<R><<<148 * 8, 256, smem, s>>>(p, out);
+  gam_field_kernel<R><<<148 * 8, 256, smem, s>>>(p, out, radius);
   return cudaGetLastError();
 }
-template cudaError_t launch_gam_field<float>(const ApplyParams<float>&, float*, cudaStream_t);
-template cudaError_t launch_gam_field<double>(const ApplyParams<double>&, double*, cudaStream_t);
+template cudaError_t launch_gam_field<float>(const ApplyParams<float>&, float*, int, cudaStream_t);
+template cudaError_t launch_gam_field<double>(const ApplyParams<double>&, double*, int, cudaStream_t);
 
 template <typename R>
 cudaError_t launch_sources(const ApplyParams<R>& p, int nsrc, const long long* nodes, const double* amps,

@@ -56,7 +56,7 @@ cudaError_t launch_apply<double, float>(const ApplyParams<double, float>& p, int
                                         cudaStream_t s);
 template <typename R> cudaError_t launch_winv(const R* v, R* w, long long n, cudaStream_t s);
 template <typename R> cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s);
-template <typename R> cudaError_t launch_gam_field(const ApplyParams<R>& p, R* out, cudaStream_t s);
+template <typename R> cudaError_t launch_gam_field(const ApplyParams<R>& p, R* out, int radius, cudaStream_t s);
 template <typename R>
 cudaError_t launch_eqerror(const typename Cx<R>::T* uref, const typename Cx<R>::T* u, int nx, int ny, int nzl, int z0,
                            int nzg, const long long* src, double h, int npml, double ball, double* partials, int nblocks,

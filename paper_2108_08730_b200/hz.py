@@ -23,7 +23,7 @@ _lib = ct.CDLL(_LIBPATH)
 HZ_OK, HZ_NOT_CONVERGED, HZ_BREAKDOWN, HZ_WARN_CLAMPED = 0, 1, 2, 3
 HZ_C64, HZ_C128 = 0, 1
 HZ_MASS_EQ8, HZ_MASS_COLLOC = 0, 1
-HZ_RULE_GA, HZ_RULE_GAM = 0, 1
+HZ_RULE_GA, HZ_RULE_GAM, HZ_RULE_GA_RECORD = 0, 1, 2
 STATUS_NAMES = {0: "HZ_OK", 1: "HZ_NOT_CONVERGED", 2: "HZ_BREAKDOWN", 3: "HZ_WARN_CLAMPED",
                 -1: "HZ_ERR_INVALID_ARG", -2: "HZ_ERR_DOMAIN", -3: "HZ_ERR_RANK", -4: "HZ_ERR_OOM",
                 -5: "HZ_ERR_CUDA", -6: "HZ_ERR_NCCL", -7: "HZ_ERR_SOURCE_IN_PML"}

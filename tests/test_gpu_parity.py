@@ -423,3 +423,17 @@ def test_export_matrix_equals_oracle_csr(hz, ctx, table, ga_table, dtype, mass, 
     assert (A != 0).nnz == (R != 0).nnz and abs((A != 0) - (R != 0)).nnz == 0
     tol = 1e-12 if dtype == "c128" else 2e-6
     assert abs(A - R).max() <= tol * abs(R).max(), abs(A - R).max() / abs(R).max()
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_apply_ga_record_mode(hz, ctx, table, ga_table, dtype):
+    """GA in record mode (per-point weights stored at assemble, read by the apply)
+    gives the GA operator: oracle parity like the fused (recompute-from-v) mode."""
+    rng = np.random.default_rng(84)
+    nz, ny, nx, h, f, npml = 13, 15, 37, 25.0, 7.0, 3
+    v = rng.uniform(1500.0, 4500.0, (nz, ny, nx))
+    u = synth.random_field((2, nz, ny, nx), seed=17)
+    C = assemble(hz, ctx, table, v, h, f, npml, dtype, rule=hz.HZ_RULE_GA_RECORD)
+    got = gpu_apply(hz, C, u)
+    ref = op.apply(op.assemble(oracle_problem(v, h, f, npml, ga_table, dtype)), u)
+    assert rel(got, ref) <= TOL[dtype], rel(got, ref)
