@@ -24,7 +24,6 @@
 #include <stdint.h>
 
 #include "apply27.cuh"
-#include "apply27_tma.cuh"   // mbarrier helpers
 
 namespace hz {
 
@@ -64,17 +63,7 @@ __host__ __device__ constexpr size_t cp_stage_bytes(int nr) { return (size_t)CP_
 #endif
 __host__ __device__ constexpr int cp_stages(int epi) { return CP_STAGES + ((HZ_CP_S_SMEM && epi == 2) ? 1 : 0); }
 __host__ __device__ constexpr size_t cp_smem_bytes(int tab_n, int nr, int epi) {
-  return (((size_t)tab_n * 12 * 4 + 127) / 128) * 128 + (size_t)cp_stages(epi) * cp_stage_bytes(nr) + 128;
-}
-// stage hand-off by mbarriers instead of a CTA barrier per plane: every thread's cp.async of a stage
-// arrives on the stage's "full" barrier (cp.async.mbarrier.arrive.noinc), consumers wait on it; each
-// warp releases a stage on its "empty" barrier after its last read, producers wait on that before
-// refilling — warps drift up to a stage apart instead of meeting at every plane
-#ifndef HZ_CP_MBAR
-#define HZ_CP_MBAR 0   // measured: no gain over the per-plane barrier (config 2 solve 0.264 -> 0.278 ms, config 4 same)
-#endif
-__device__ __forceinline__ void cp_mbar_arrive(uint64_t* b) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+  return (((size_t)tab_n * 12 * 4 + 127) / 128) * 128 + (size_t)cp_stages(epi) * cp_stage_bytes(nr);
 }
 // work item {x0 | y0 << 16, tx | ty << 8 | (xs − x0) << 16 | (ys − y0) << 24, z0 | z1 << 16,
 // (xe − x0) | (ye − y0) << 8 | mode << 16}: the tile computes [x0, x0+tx) × [y0, y0+ty) and stores
@@ -185,7 +174,6 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
   constexpr bool SSM = HZ_CP_S_SMEM && EPI == EPI_DOT4;   // s operand from the ring
   constexpr int S = cp_stages(EPI);
   constexpr int L = SSM ? S - 2 : S - 1;                   // planes issued ahead
-  constexpr bool MB = HZ_CP_MBAR && !SSM;                   // mbarrier hand-off (see cp_mbar_arrive)
   const unsigned FULL = 0xffffffffu;
 
   // ---- block → (work item, RHS group)
@@ -226,12 +214,10 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
   int goff[KS];        // in-plane element offset y·nx + x (0 outside the grid)
   uint32_t sdst[KS];   // byte offset of the w element in a stage (~0u: no element for this slot)
   bool gout[KS];       // element outside the grid: zero fill
-  // e / P by a float reciprocal: exact here (e < CP_HALO, P ≤ 66: the rounding error ≪ 0.5 / P)
-  const float invP = 1.0f / (float)P;
 #pragma unroll
   for (int k = 0; k < KS; k++) {
     const int e = tid + k * NT;
-    const int r = (int)(((float)e + 0.5f) * invP), cc = e - r * P;
+    const int r = e / P, cc = e - r * P;
     const int gx = X0 - 1 + cc, gy = Y0 - 1 + r;
     const bool in_tile = r < ROWS;
     const bool gin = in_tile && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
@@ -245,13 +231,7 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
   asm("mov.b64 %0, %0;" : "+l"(ug0));   // keep the group's base in a register (not re-derived per use)
 #endif
   const float* __restrict__ wg = p.w;
-  uint64_t* fullb = reinterpret_cast<uint64_t*>(ring + (size_t)S * stage_bytes);
-  uint64_t* emptyb = fullb + S;
   auto issue = [&](int j) {
-    if (MB) {
-      if (j >= nplanes) return;
-      if (j >= S) mbar_wait(&emptyb[j % S], (uint32_t)(j / S - 1) & 1u);   // plane j-S released its slot
-    }
     if (j < nplanes) {
       const int pl = zc0 - 1 + j;
       const int zg = p.z0 + pl;
@@ -269,31 +249,17 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
           if (act[r]) cp_async8(st + wbytes + (uint32_t)r * ubytes + 2u * sdst[k], ug0 + (o + (uint32_t)r * fs), zf);
       }
     }
-    if (MB)
-      cp_mbar_arrive(&fullb[j % S]);
-    else
-      cp_commit();
+    cp_commit();
   };
-  if (MB) {
-    if (tid == 0) {
-      for (int k = 0; k < S; k++) {
-        mbar_init(&fullb[k], NT);
-        mbar_init(&emptyb[k], NT / 32);
-      }
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-  }
   for (int j = 0; j < L; j++) issue(j);
 
   // stage the coefficient table while the first planes stream in
   for (int e = tid; e < p.tab_n * CTAB_STRIDE; e += NT) stab[e] = p.ctab[(long long)p.tab_lo * CTAB_STRIDE + e];
-  if (MB) __syncthreads();   // (without MB the first plane's barrier covers it)
 
   // ---- this thread's position (threads past tx·TY/NY duplicate position 0 and never store)
   const bool pos_ok = tid < tx * (TY / NY);
   const int pt = pos_ok ? tid : 0;
-  const int s_ = (int)(((float)pt + 0.5f) / (float)tx), c_ = pt - s_ * tx;   // exact: pt < 512, tx ≤ 64
+  const int s_ = pt / tx, c_ = pt - s_ * tx;
   const int x = X0 + c_;
   const int yl0 = Y0 + NY * s_;
   const bool x_ok = pos_ok && x >= X0n && x < X1n;
@@ -391,13 +357,8 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
     // planes j and j+1 have landed (own copies), then every thread's copies; the slot of plane j+L-S
     // (j-1, or j-2 when the previous plane's centre is still read) is free — every thread is past the
     // iteration that last read it — and receives plane j+L
-    if (MB) {
-      mbar_wait(&fullb[j % S], (uint32_t)(j / S) & 1u);
-      if (j + 1 < nplanes) mbar_wait(&fullb[(j + 1) % S], (uint32_t)((j + 1) / S) & 1u);
-    } else {
-      cp_wait<L - 2>();
-      __syncthreads();
-    }
+    cp_wait<L - 2>();
+    __syncthreads();
     issue(j + L);
 
     const unsigned char* st = ring + (size_t)(j % S) * stage_bytes;
@@ -587,10 +548,6 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
         }
       }
     }
-    if (MB) {   // this warp is done with stage j (read here, and as the "next" stage in call j-1)
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(&emptyb[j % S]);
-    }
   };
 
   Coef6<R> cs0[NY], cs1[NY], cs2[NY];
@@ -612,7 +569,7 @@ __device__ __forceinline__ void cp_body(const ApplyParams<float, float>& p, int 
     if (j + 2 >= nplanes) break;
     body(cs2, cs0, cs1, ms2, ms0, ms1, as2, as0, as1, ss2, ss0, j + 2);
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  cp_wait<0>();
 
   if constexpr (K > 0) cp_reduce<NR, K, NT>(part, act, p, rhs0, item0 + blockIdx.x);
 }
