@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--dtype", choices=["c64", "c128"], default="c64")
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--max-iter", type=int, default=20000)
+    ap.add_argument("--ell", type=int, choices=[1, 2], default=1, help="1: BiCGSTAB (default), 2: BiCGStab(2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=30, help="oracle BiCGSTAB iterations in the cpu_baseline sample")
@@ -353,7 +354,7 @@ def run_hz(args):
         else:
             x_out.zero_()
         st, rel, its, stt = hz.hz_solve(C, b, x_out, rtol=args.rtol, max_iter=args.max_iter,
-                                        timing=True, stream=stream)                 # a6, a7
+                                        timing=True, ell=args.ell, stream=stream)   # a6, a7
         return st, rel, its, stt
 
     def timed(v_in, x_out, k):
@@ -425,6 +426,7 @@ def run_hz(args):
         "data": "synthetic",
         "config": {"workload": workload_name(cfg, freq, nrhs, args.dtype), "grid": [cfg.nx, cfg.ny, cfg.nz],
                    "nrhs": nrhs, "rtol": args.rtol, "parallelism": f"z-slab x{ws}",
+                   "solver": "BiCGSTAB" if args.ell == 1 else "BiCGStab(2)",
                    "l2": "flushed before every step (256 MiB write); step working set > L2"},
         "solve_s_per_rhs": ms_per_step * 1e-3 / nrhs,
         "iterations": int(stats[-1]["iterations"]),

@@ -182,6 +182,11 @@ typedef struct {
   int replace_every; /* residual replacement period, default 50                    */
   int check_every;   /* host convergence poll period, default 10                   */
   int timing;        /* 1 = time every operator-apply launch with CUDA events      */
+  int ell;           /* Krylov method: 1 (or 0) = BiCGSTAB (default); 2 = BiCGStab(2)
+                        (Sleijpen & Fokkema 1993: two BiCG steps then a 2-term minimal-
+                        residual polynomial; four applies per outer step, counted as two
+                        iterations; robust where BiCGSTAB's omega -> 0 stalls it — DESIGN.md
+                        reading A23).  Any other value: HZ_ERR_INVALID_ARG.            */
 } hz_solve_opts;
 
 typedef struct {

@@ -178,8 +178,9 @@ struct hz_table {
 struct SolverWork {
   int nrhs = 0;
   DBuf rhat, p, v, t, r;        // fields [nrhs][nzl+2][ny][nx]
+  DBuf r1, r2;                  // BiCGStab(2) only
   DBuf xlo;                     // compensation term of the c64 iterate (double-float x)
-  DBuf dotA, dotB, dotR, dotN;  // fp64 dot buffers
+  DBuf dotA, dotB, dotR, dotN, dotG;  // fp64 dot buffers
   DBuf state, active;
   DBuf partials, tickets;
   DBuf hb, hx;                  // staging for host b / x
@@ -1160,6 +1161,12 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   HZ_CUDA(w.v.ensure(fb));
   HZ_CUDA(w.t.ensure(fb));
   HZ_CUDA(w.r.ensure(fb));
+  const bool ell2 = o.ell == 2;
+  if (ell2) {
+    HZ_CUDA(w.r1.ensure(fb));
+    HZ_CUDA(w.r2.ensure(fb));
+    HZ_CUDA(w.dotG.ensure(sizeof(double) * nrhs));
+  }
   if (sizeof(R) == 4) {
     HZ_CUDA(w.xlo.ensure(fb));
     HZ_CUDA(cudaMemsetAsync(w.xlo.p, 0, fb, s));
@@ -1174,7 +1181,7 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->ctx->device);
   const int vblocks = (int)std::max(1LL, std::min((n + 1023) / 1024, (long long)(8 * sms + nrhs - 1) / nrhs));
-  HZ_CUDA(w.partials.ensure(sizeof(double) * (size_t)vblocks * nrhs));
+  HZ_CUDA(w.partials.ensure(sizeof(double) * (size_t)vblocks * nrhs * 3));   // ≤ 3 dots per vector kernel
   HZ_CUDA(w.tickets.ensure(sizeof(unsigned) * nrhs));
   HZ_CUDA(cudaMemsetAsync(w.tickets.p, 0, sizeof(unsigned) * nrhs, s));
   HZ_CUDA(cudaMemsetAsync(w.state.p, 0, sizeof(SolverState) * nrhs, s));
@@ -1226,6 +1233,9 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   q.v = w.v.as<C>();
   q.t = w.t.as<C>();
   q.xlo = sizeof(R) == 4 ? w.xlo.as<C>() : nullptr;
+  q.r1 = ell2 ? w.r1.as<C>() : nullptr;
+  q.r2 = ell2 ? w.r2.as<C>() : nullptr;
+  q.dotG = ell2 ? w.dotG.as<double>() : nullptr;
   q.dotA = w.dotA.as<double>();
   q.dotB = w.dotB.as<double>();
   q.dotR = w.dotR.as<double>();
@@ -1290,8 +1300,14 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   // despite its own rounding floor (~eps32·‖|A||x|‖/‖b‖, 2–5e-7 on configs 1–3; reading A21)
   const double rtol_it = sizeof(R) == 4 ? 0.5 * o.rtol : o.rtol;
   const double rtol2 = rtol_it * rtol_it;
+  auto init = [&]() -> hz_status {
+    if (!ell2) return vec(BICG_INIT);
+    HZ_CUDA(launch_bicgl<R>(BCL_INIT, q, nrhs, s));
+    count_launch();
+    return HZ_OK;
+  };
   HZ_TRY(resid(false));
-  HZ_TRY(vec(BICG_INIT));
+  HZ_TRY(init());
 
   int restarts = 0, replacements = 0;
   int it = 0;
@@ -1332,48 +1348,63 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
     return HZ_OK;
   };
 
+  // one operator apply with a dot epilogue (+ the ranks' sum of its dots)
+  auto apply_dots = [&](DBuf& in, DBuf& out, int epi, const C* rh, DBuf& dots, int ndots) -> hz_status {
+    HZ_TRY(halo_exchange(c, in.p, nrhs, sizeof(C), s));
+    ApplyParams<R> p = base;
+    p.u = in.as<C>();
+    p.au = out.as<C>();
+    p.rhat = rh;
+    p.dots = dots.as<double>();
+    timer.mark(s);
+    HZ_TRY(apply_launch<R, R>(c, p, nrhs, epi, s));
+    timer.mark(s);
+    account(3);
+    HZ_TRY(allreduce_sum(c, dots.as<double>(), (size_t)ndots * nrhs, s));
+    return HZ_OK;
+  };
+  auto vecl = [&](int which) -> hz_status {
+    HZ_CUDA(launch_bicgl<R>(which, q, nrhs, s));
+    count_launch();
+    return HZ_OK;
+  };
+  // after a residual replacement: BiCGSTAB re-reads ρ = (r̂0, r) from dotR; BiCGStab(2) always does
+  auto rho_reset = [&]() -> hz_status { return ell2 ? HZ_OK : vec(BICG_RHO_RESET); };
+  const C* rh = w.rhat.as<C>();
+
   while (n_active() > 0 && it < o.max_iter) {
-    // v = A p, (r̂0, v)
-    HZ_TRY(halo_exchange(c, w.p.p, nrhs, sizeof(C), s));
-    {
-      ApplyParams<R> p = base;
-      p.u = w.p.as<C>();
-      p.au = w.v.as<C>();
-      p.rhat = w.rhat.as<C>();
-      p.dots = w.dotA.as<double>();
-      timer.mark(s);
-      HZ_TRY(apply_launch<R, R>(c, p, nrhs, EPI_DOT1, s));
-      timer.mark(s);
-      account(3);
-      HZ_TRY(allreduce_sum(c, w.dotA.as<double>(), 2 * (size_t)nrhs, s));
+    int inc = 1;
+    if (!ell2) {
+      HZ_TRY(apply_dots(w.p, w.v, EPI_DOT1, rh, w.dotA, 2));   // v = A p, (r̂0, v)
+      HZ_TRY(vec(BICG_S));                                      // s = r − α v (in r)
+      HZ_TRY(apply_dots(w.r, w.t, EPI_DOT4, rh, w.dotB, 7));   // t = A s, (t,s), (t,t), (r̂0,s), (r̂0,t)
+      HZ_TRY(vec(BICG_UPDATE));                                 // x, r, p; ‖r‖²
+      HZ_TRY(allreduce_sum(c, w.dotR.as<double>(), 3 * (size_t)nrhs, s));
+    } else {   // one BiCGStab(2) outer step (kernels.cu K3'): four applies = two BiCGSTAB iterations
+      inc = 2;
+      HZ_TRY(vecl(BCL_A));
+      HZ_TRY(apply_dots(w.p, w.v, EPI_DOT1, rh, w.dotA, 2));   // u1 = A u0
+      HZ_TRY(vecl(BCL_B));
+      HZ_TRY(apply_dots(w.r, w.r1, EPI_DOT1, rh, w.dotA, 2));  // r1 = A r0
+      HZ_TRY(vecl(BCL_C));
+      HZ_TRY(apply_dots(w.v, w.t, EPI_DOT1, rh, w.dotA, 2));   // u2 = A u1
+      HZ_TRY(vecl(BCL_D));
+      HZ_TRY(allreduce_sum(c, w.dotG.as<double>(), (size_t)nrhs, s));
+      HZ_TRY(apply_dots(w.r1, w.r2, EPI_DOT4, w.r.as<C>(), w.dotB, 7));   // r2 = A r1 (r̂ := r0)
+      HZ_TRY(vecl(BCL_E));
+      HZ_TRY(allreduce_sum(c, w.dotR.as<double>(), 3 * (size_t)nrhs, s));
     }
-    HZ_TRY(vec(BICG_S));  // s = r − α v (in r)
-    // t = A s, (t,s), (t,t), (r̂0,s), (r̂0,t)
-    HZ_TRY(halo_exchange(c, w.r.p, nrhs, sizeof(C), s));
-    {
-      ApplyParams<R> p = base;
-      p.u = w.r.as<C>();
-      p.au = w.t.as<C>();
-      p.rhat = w.rhat.as<C>();
-      p.dots = w.dotB.as<double>();
-      timer.mark(s);
-      HZ_TRY(apply_launch<R, R>(c, p, nrhs, EPI_DOT4, s));
-      timer.mark(s);
-      account(3);
-      HZ_TRY(allreduce_sum(c, w.dotB.as<double>(), 7 * (size_t)nrhs, s));
-    }
-    HZ_TRY(vec(BICG_UPDATE));  // x, r, p; ‖r‖²
-    HZ_TRY(allreduce_sum(c, w.dotR.as<double>(), 3 * (size_t)nrhs, s));
-    ++it;
+    it += inc;
     for (int r = 0; r < nrhs; r++)
-      if (active[r]) iters[r]++;
-    const bool replaced = o.replace_every > 0 && it % o.replace_every == 0;
+      if (active[r]) iters[r] += inc;
+    auto crossed = [&](int period) { return period > 0 && it / period > (it - inc) / period; };
+    const bool replaced = crossed(o.replace_every);
     if (replaced) {
       HZ_TRY(resid(true));
-      HZ_TRY(vec(BICG_RHO_RESET));
+      HZ_TRY(rho_reset());
       replacements++;
     }
-    if (replaced || it % std::max(1, o.check_every) == 0 || it >= o.max_iter) {
+    if (replaced || crossed(std::max(1, o.check_every)) || it >= o.max_iter) {
       HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
       HZ_CUDA(cudaMemcpyAsync(hst.data(), w.state.p, sizeof(SolverState) * nrhs, cudaMemcpyDeviceToHost, s));
       HZ_CUDA(cudaStreamSynchronize(s));
@@ -1385,7 +1416,7 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
       }
       if (brk) {  // restart broken RHS with r̂0 = r = b − A x (all active RHS restart together)
         HZ_TRY(resid(false));
-        HZ_TRY(vec(BICG_INIT));
+        HZ_TRY(init());
         restarts++;
         if (restarts > 50) break;
         continue;
@@ -1394,7 +1425,7 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
         HZ_TRY(retire(true));           // hdot holds the recomputed true residuals
       } else if (cand) {                // verify on the recomputed TRUE residual (A21)
         HZ_TRY(resid(true));
-        HZ_TRY(vec(BICG_RHO_RESET));
+        HZ_TRY(rho_reset());
         replacements++;
         HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
         HZ_CUDA(cudaStreamSynchronize(s));
@@ -1441,9 +1472,11 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
 extern "C" hz_status hz_solve(const hz_coeffs* c, const void* b, void* x, int nrhs, const hz_solve_opts* opts,
                               double* relres_out, int* iters_out, hz_solve_stats* stats, void* stream) {
   if (!c || !b || !x || nrhs < 1) { set_error("hz_solve: bad arguments"); return HZ_ERR_INVALID_ARG; }
-  hz_solve_opts o = {1e-6, 20000, 50, 10, 0};
+  hz_solve_opts o = {1e-6, 20000, 50, 10, 0, 1};
   if (opts) o = *opts;
   if (!(o.rtol > 0) || o.max_iter < 1) { set_error("hz_solve: need rtol > 0, max_iter >= 1"); return HZ_ERR_INVALID_ARG; }
+  if (o.ell == 0) o.ell = 1;
+  if (o.ell != 1 && o.ell != 2) { set_error("hz_solve: ell must be 1 (BiCGSTAB) or 2 (BiCGStab(2))"); return HZ_ERR_INVALID_ARG; }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return c->dtype == HZ_C64 ? solve_t<float>(c, b, x, nrhs, o, relres_out, iters_out, stats, s)
                             : solve_t<double>(c, b, x, nrhs, o, relres_out, iters_out, stats, s);

@@ -405,6 +405,157 @@ __global__ void __launch_bounds__(NT) norm2_kernel(const typename Cx<R>::T* __re
 }
 
 // =============================================================================================
+// K3': BiCGStab(2) vector steps (Sleijpen & Fokkema 1993, ℓ = 2, reading A23) — a
+// solver option for the models where BiCGSTAB stagnates (its ω → 0 on strongly indefinite
+// Helmholtz systems).  One outer step = two BiCGSTAB iterations' worth of applies (four):
+//   A: ρ0 ← −ω ρ0; ρ1 = (r̂0, r0); β = α ρ1/ρ0; ρ0 ← ρ1;            u0 = r0 − β u0
+//      u1 = A u0, σ = (r̂0, u1)                                          [apply, DOT1]
+//   B: α = ρ0/σ;                                                        r0 −= α u1; x += α u0
+//      r1 = A r0, ρ1 = (r̂0, r1)                                         [apply, DOT1]
+//   C: β = α ρ1/ρ0; ρ0 ← ρ1;                                u0 = r0 − β u0; u1 = r1 − β u1
+//      u2 = A u1, σ = (r̂0, u2)                                          [apply, DOT1]
+//   D: α = ρ0/σ;                        r0 −= α u1; r1 −= α u2; x += α u0; ‖r1‖² → dotG
+//      r2 = A r1; (r2,r1), ‖r2‖², (r0,r1), (r0,r2)                      [apply, DOT4, r̂ := r0]
+//   E: (γ1, γ2) = argmin ‖r0 − γ1 r1 − γ2 r2‖ (2×2 normal equations in fp64); ω = γ2;
+//      x += γ1 r0 + γ2 r1; r0 −= γ1 r1 + γ2 r2; u0 −= γ1 u1 + γ2 u2;   ‖r0‖², (r̂0, r0) → dotR
+// (a, b) = Σ conj(a) b.  Fields: r0 = q.r, r1 = q.r1, r2 = q.r2, u0 = q.p, u1 = q.v, u2 = q.t.
+// State: rho_used = ρ0 after A (read by B, C), rho_next = ρ0 after C (read by D, next A), alpha
+// (B, D), omega (E); no kernel reads a field it writes (every CTA derives the scalars itself).
+// =============================================================================================
+template <typename R>
+__device__ __forceinline__ void x_add(const VecParams<R>& q, long long e, typename Cx<R>::T dx) {
+  typename Cx<R>::T xx = q.x[e];
+  if (q.xlo != nullptr) {   // double-word iterate (complex64): compensated update, as bicg_update_kernel
+    typename Cx<R>::T lo = q.xlo[e];
+    two_sum(xx.x, dx.x + lo.x, xx.x, lo.x);
+    two_sum(xx.y, dx.y + lo.y, xx.y, lo.y);
+    q.xlo[e] = lo;
+  } else {
+    xx.x += dx.x;
+    xx.y += dx.y;
+  }
+  q.x[e] = xx;
+}
+
+template <typename R, int NT, int STEP>
+__global__ void __launch_bounds__(NT) bicgl_kernel(VecParams<R> q) {
+  typedef typename Cx<R>::T C;
+  const int rhs = blockIdx.y;
+  if (q.active[rhs] == 0) return;
+  SolverState& st = q.state[rhs];
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  bool brk = STEP != BCL_INIT && (st.flags & 1) != 0;
+  double2 s1 = make_double2(0.0, 0.0), s2 = s1;   // the step's two complex scalars
+  if constexpr (STEP == BCL_INIT) {
+    if (lead) {   // ρ0 = α = ω = 1... (α = 0 so that the first β vanishes); (r̂0, r0) = ‖r0‖² as r̂0 = r0
+      st.rho_next[0] = 1.0;
+      st.rho_next[1] = 0.0;
+      st.alpha[0] = st.alpha[1] = 0.0;
+      st.omega[0] = 1.0;
+      st.omega[1] = 0.0;
+      st.flags = 0;
+      q.dotR[3 * rhs + 1] = q.dotR[3 * rhs + 0];
+      q.dotR[3 * rhs + 2] = 0.0;
+    }
+  } else if constexpr (STEP == BCL_A) {
+    const double2 om = make_double2(st.omega[0], st.omega[1]);
+    const double2 r0p = zmul(make_double2(-om.x, -om.y), make_double2(st.rho_next[0], st.rho_next[1]));
+    const double2 rho1 = make_double2(q.dotR[3 * rhs + 1], q.dotR[3 * rhs + 2]);
+    if (tiny(r0p, 1.0) || tiny(rho1, 1.0)) brk = true;
+    else s1 = zdiv(zmul(make_double2(st.alpha[0], st.alpha[1]), rho1), r0p);   // β
+    if (lead) {
+      st.rho_used[0] = rho1.x;
+      st.rho_used[1] = rho1.y;
+    }
+  } else if constexpr (STEP == BCL_B || STEP == BCL_D) {
+    const double2 rho = STEP == BCL_B ? make_double2(st.rho_used[0], st.rho_used[1])
+                                      : make_double2(st.rho_next[0], st.rho_next[1]);
+    const double2 sig = make_double2(q.dotA[2 * rhs], q.dotA[2 * rhs + 1]);
+    if (brk || tiny(sig, 1.0) || tiny(rho, 1.0)) brk = true;
+    else s1 = zdiv(rho, sig);   // α
+    if (lead) {
+      st.alpha[0] = s1.x;
+      st.alpha[1] = s1.y;
+    }
+  } else if constexpr (STEP == BCL_C) {
+    const double2 rho0 = make_double2(st.rho_used[0], st.rho_used[1]);
+    const double2 rho1 = make_double2(q.dotA[2 * rhs], q.dotA[2 * rhs + 1]);
+    if (brk || tiny(rho0, 1.0)) brk = true;
+    else s1 = zdiv(zmul(make_double2(st.alpha[0], st.alpha[1]), rho1), rho0);   // β
+    if (lead) {
+      st.rho_next[0] = rho1.x;
+      st.rho_next[1] = rho1.y;
+    }
+  } else {   // BCL_E: normal equations [a11 a12; a21 a22] γ = c of the 2-term minimal residual
+    const double* dB = q.dotB + 7 * rhs;
+    const double a11 = q.dotG[rhs], a22 = dB[2];
+    const double2 a21 = make_double2(dB[0], dB[1]);          // (r2, r1)
+    const double2 a12 = make_double2(a21.x, -a21.y);         // (r1, r2)
+    const double2 c1 = make_double2(dB[3], -dB[4]);          // (r1, r0) = conj((r0, r1))
+    const double2 c2 = make_double2(dB[5], -dB[6]);          // (r2, r0)
+    const double det = a11 * a22 - (a21.x * a21.x + a21.y * a21.y);
+    if (brk || !(det > 1e-14 * a11 * a22) || !isfinite(det)) {
+      brk = true;
+    } else {
+      const double2 n1 = csub(cscale(a22, c1), cmul(a12, c2));
+      const double2 n2 = csub(cscale(a11, c2), cmul(a21, c1));
+      s1 = cscale(1.0 / det, n1);   // γ1
+      s2 = cscale(1.0 / det, n2);   // γ2 = ω
+    }
+    if (lead) {
+      st.omega[0] = s2.x;
+      st.omega[1] = s2.y;
+    }
+  }
+  if (brk) s1 = s2 = make_double2(0.0, 0.0);
+  if (lead && brk) st.flags |= 1;
+  const C a = to_c<R>(s1), b = to_c<R>(s2);
+  const long long off = (long long)rhs * q.fstride + q.plane;
+  constexpr int K = STEP == BCL_E ? 3 : (STEP == BCL_D ? 1 : 0);
+  double part[K > 0 ? K : 1];
+#pragma unroll
+  for (int k = 0; k < (K > 0 ? K : 1); k++) part[k] = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < q.n; i += stride) {
+    const long long e = off + i;
+    if constexpr (STEP == BCL_INIT) {
+      q.rhat[e] = q.r[e];
+      q.p[e] = czero(R(0));
+    } else if constexpr (STEP == BCL_A) {   // u0 = r0 − β u0
+      q.p[e] = csub(q.r[e], cmul(a, q.p[e]));
+    } else if constexpr (STEP == BCL_B) {   // r0 −= α u1; x += α u0
+      q.r[e] = csub(q.r[e], cmul(a, q.v[e]));
+      x_add<R>(q, e, cmul(a, q.p[e]));
+    } else if constexpr (STEP == BCL_C) {   // u0 = r0 − β u0; u1 = r1 − β u1
+      q.p[e] = csub(q.r[e], cmul(a, q.p[e]));
+      q.v[e] = csub(q.r1[e], cmul(a, q.v[e]));
+    } else if constexpr (STEP == BCL_D) {   // r0 −= α u1; r1 −= α u2; x += α u0
+      const C u1 = q.v[e];
+      q.r[e] = csub(q.r[e], cmul(a, u1));
+      const C r1 = csub(q.r1[e], cmul(a, q.t[e]));
+      q.r1[e] = r1;
+      x_add<R>(q, e, cmul(a, q.p[e]));
+      part[0] += (double)r1.x * (double)r1.x + (double)r1.y * (double)r1.y;
+    } else {                      // E: x += γ1 r0 + γ2 r1; r0 −= γ1 r1 + γ2 r2; u0 −= γ1 u1 + γ2 u2
+      const C r0 = q.r[e], r1 = q.r1[e];
+      x_add<R>(q, e, cadd(cmul(a, r0), cmul(b, r1)));
+      const C rn = csub(r0, cadd(cmul(a, r1), cmul(b, q.r2[e])));
+      q.r[e] = rn;
+      q.p[e] = csub(q.p[e], cadd(cmul(a, q.v[e]), cmul(b, q.t[e])));
+      const C rh = q.rhat[e];
+      part[0] += (double)rn.x * (double)rn.x + (double)rn.y * (double)rn.y;
+      acc_cdot(part[1], part[2], rh, rn);
+    }
+  }
+  if constexpr (K > 0) {
+    const int nblocks = gridDim.x;
+    double* out = STEP == BCL_E ? q.dotR + 3 * rhs : q.dotG + rhs;
+    block_grid_reduce<K, NT>(part, q.partials + (long long)rhs * nblocks * K, out, q.tickets + rhs, nblocks,
+                             blockIdx.x);
+  }
+}
+
+// =============================================================================================
 // host-side launchers (kernels.h)
 // =============================================================================================
 template <typename R> struct ApplyCfg;
@@ -924,6 +1075,23 @@ cudaError_t launch_bicg(int which, const VecParams<R>& q, int nrhs, cudaStream_t
 }
 template cudaError_t launch_bicg<float>(int, const VecParams<float>&, int, cudaStream_t);
 template cudaError_t launch_bicg<double>(int, const VecParams<double>&, int, cudaStream_t);
+
+template <typename R>
+cudaError_t launch_bicgl(int which, const VecParams<R>& q, int nrhs, cudaStream_t s) {
+  dim3 grid((unsigned)q.nblocks, (unsigned)nrhs);
+  switch (which) {
+    case BCL_INIT: bicgl_kernel<R, VEC_NT, BCL_INIT><<<grid, VEC_NT, 0, s>>>(q); break;
+    case BCL_A: bicgl_kernel<R, VEC_NT, BCL_A><<<grid, VEC_NT, 0, s>>>(q); break;
+    case BCL_B: bicgl_kernel<R, VEC_NT, BCL_B><<<grid, VEC_NT, 0, s>>>(q); break;
+    case BCL_C: bicgl_kernel<R, VEC_NT, BCL_C><<<grid, VEC_NT, 0, s>>>(q); break;
+    case BCL_D: bicgl_kernel<R, VEC_NT, BCL_D><<<grid, VEC_NT, 0, s>>>(q); break;
+    case BCL_E: bicgl_kernel<R, VEC_NT, BCL_E><<<grid, VEC_NT, 0, s>>>(q); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+template cudaError_t launch_bicgl<float>(int, const VecParams<float>&, int, cudaStream_t);
+template cudaError_t launch_bicgl<double>(int, const VecParams<double>&, int, cudaStream_t);
 
 template <typename R>
 cudaError_t launch_norm2(const typename Cx<R>::T* f, long long fstride, long long plane, long long n, int nrhs,

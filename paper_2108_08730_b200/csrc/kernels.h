@@ -27,9 +27,11 @@ struct VecParams {
   int nblocks;        // CTAs per RHS
   C *x, *r, *rhat, *p, *v, *t;
   C* xlo;              // compensation term of the iterate (complex64 solver) or null
+  C *r1, *r2;          // BiCGStab(2) only: A-images of r0 (= r) within one outer step
   const double* dotA;  // [nrhs][2]
   const double* dotB;  // [nrhs][7]
   double* dotR;        // [nrhs][3]
+  double* dotG;        // BiCGStab(2) only: [nrhs] ‖r1‖²
   double* partials;
   unsigned int* tickets;
   SolverState* state;
@@ -37,6 +39,9 @@ struct VecParams {
 };
 
 enum { BICG_INIT = 0, BICG_S = 1, BICG_UPDATE = 2, BICG_RHO_RESET = 3 };
+// BiCGStab(2) vector steps (bicgl_kernel): one outer step = BCL_A, apply, BCL_B, apply, BCL_C, apply,
+// BCL_D, apply (DOT4), BCL_E
+enum { BCL_INIT = 0, BCL_A = 1, BCL_B = 2, BCL_C = 3, BCL_D = 4, BCL_E = 5 };
 
 template <typename R> int apply_ny();
 template <typename R> int apply_warps();
@@ -71,6 +76,7 @@ cudaError_t launch_sources(const ApplyParams<R>& p, int nsrc, const long long* n
 template <typename R>
 cudaError_t launch_vstats(const R* v, long long n, R inv_fh, R g_min, R g_max, unsigned long long* out, cudaStream_t s);
 template <typename R> cudaError_t launch_bicg(int which, const VecParams<R>& q, int nrhs, cudaStream_t s);
+template <typename R> cudaError_t launch_bicgl(int which, const VecParams<R>& q, int nrhs, cudaStream_t s);
 template <typename R>
 cudaError_t launch_norm2(const typename Cx<R>::T* f, long long fstride, long long plane, long long n, int nrhs,
                          int nblocks, double* partials, double* out, unsigned int* tickets, cudaStream_t s);

@@ -46,11 +46,11 @@ def setup(hz, ctx, table, cfg, dtype):
     return v.astype(rd).astype(np.float64), C
 
 
-def gpu_solve(hz, C, nodes, rtol=1e-6):
+def gpu_solve(hz, C, nodes, rtol=1e-6, ell=1):
     b = C.alloc_field(len(nodes))
     hz.hz_point_sources(C, nodes, b)
     x = C.alloc_field(len(nodes))
-    st, rel, its, stats = hz.hz_solve(C, b, x, rtol=rtol, max_iter=20000)
+    st, rel, its, stats = hz.hz_solve(C, b, x, rtol=rtol, max_iter=20000, ell=ell)
     torch.cuda.synchronize()
     return st, rel, its, x[:, 1:-1].cpu().numpy().astype(np.complex128)
 
@@ -66,12 +66,13 @@ def rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
+@pytest.mark.parametrize("ell", [1, 2])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
-def test_config1_solve_vs_oracle_and_analytic(hz, ctx, table, ga_table, dtype):
+def test_config1_solve_vs_oracle_and_analytic(hz, ctx, table, ga_table, dtype, ell):
     cfg = synth.get_config(1)
     v, C = setup(hz, ctx, table, cfg, dtype)
     nodes = synth.source_nodes(cfg)
-    st, relres, its, x = gpu_solve(hz, C, nodes)
+    st, relres, its, x = gpu_solve(hz, C, nodes, ell=ell)
     assert st == hz.HZ_OK and relres[0] <= 1e-6, (st, relres)
     P = op.Problem(v, cfg.h, cfg.freq, cfg.npml, ga_table)
     A = op.assemble(P)
@@ -91,14 +92,14 @@ def test_config1_solve_vs_oracle_and_analytic(hz, ctx, table, ga_table, dtype):
     assert metrics.eqerror(ref, x[0], D, m) <= 5e-3
 
 
-@pytest.mark.parametrize("dtype", ["c64", "c128"])
-def test_config2_batched_solve(hz, ctx, table, ga_table, dtype):
+@pytest.mark.parametrize("dtype,ell", [("c64", 1), ("c128", 1), ("c64", 2)])
+def test_config2_batched_solve(hz, ctx, table, ga_table, dtype, ell):
     """4 RHS solved together: every wavefield against the stored oracle wavefield (1e-4) and by its
-    residual with the oracle matrix."""
+    residual with the oracle matrix (BiCGSTAB, and BiCGStab(2) for complex64)."""
     cfg = synth.get_config(2)
     v, C = setup(hz, ctx, table, cfg, dtype)
     nodes = synth.source_nodes(cfg)
-    st, relres, its, x = gpu_solve(hz, C, nodes)
+    st, relres, its, x = gpu_solve(hz, C, nodes, ell=ell)
     assert st == hz.HZ_OK and np.all(relres <= 1e-6), (st, relres, its)
     P = op.Problem(v, cfg.h, cfg.freq, cfg.npml, ga_table)
     A = op.assemble(P)
@@ -157,8 +158,8 @@ def test_solver_edge_cases(hz, ctx, table):
     assert np.array_equal(xh, x3.cpu().numpy())
 
 
-@pytest.mark.parametrize("seed", range(4))
-def test_solve_random_small(hz, ctx, table, ga_table, seed):
+@pytest.mark.parametrize("seed,ell", [(0, 1), (1, 1), (2, 1), (3, 1), (0, 2), (1, 2), (2, 2)])
+def test_solve_random_small(hz, ctx, table, ga_table, seed, ell):
     """Batched solve on random small models (RHS converging at different iterations, RHS pairs with a
     retired member, odd RHS counts): every returned x meets rtol on the ORACLE matrix's residual."""
     rng = np.random.default_rng(3000 + seed)
@@ -171,7 +172,7 @@ def test_solve_random_small(hz, ctx, table, ga_table, seed):
     b = C.alloc_field(nrhs)
     hz.hz_point_sources(C, nodes, b)
     x = C.alloc_field(nrhs)
-    st, relres, its, _ = hz.hz_solve(C, b, x, rtol=1e-6, max_iter=20000)
+    st, relres, its, _ = hz.hz_solve(C, b, x, rtol=1e-6, max_iter=20000, ell=ell)
     assert st == hz.HZ_OK and np.all(relres <= 1e-6), (st, relres, its)
     P = op.Problem(v.astype(np.float64), 25.0, 5.0, npml, ga_table)
     A = op.assemble(P)
@@ -180,3 +181,32 @@ def test_solve_random_small(hz, ctx, table, ga_table, seed):
     for r in range(nrhs):
         br = B[r].ravel()
         assert np.linalg.norm(br - A @ X[r].ravel()) / np.linalg.norm(br) <= 1.5e-6, r
+
+
+def test_bicgstab2_edge_cases(hz, ctx, table):
+    """BiCGStab(2): b = 0 retires at iteration 0, a non-zero initial guess, an iteration cap (counted in
+    BiCGSTAB-equivalent steps of 2), host buffers equal to device buffers bit for bit, and a bad ell."""
+    cfg = synth.get_config(1)
+    v, C = setup(hz, ctx, table, cfg, "c64")
+    b = C.alloc_field(3)
+    hz.hz_point_sources(C, np.repeat(synth.source_nodes(cfg), 3, 0), b)
+    b[1].zero_()
+    x = C.alloc_field(3)
+    x[2].normal_()
+    st, relres, its, stats = hz.hz_solve(C, b, x, rtol=1e-6, ell=2)
+    assert st == hz.HZ_OK and its[1] == 0 and float(x[1].abs().max()) == 0.0
+    assert np.all(relres <= 1e-6) and its[0] % 2 == 0
+    x2 = C.alloc_field(3)
+    st, relres, its, stats = hz.hz_solve(C, b, x2, rtol=1e-12, max_iter=7, ell=2)
+    assert st == hz.HZ_NOT_CONVERGED and its[0] == 8 and stats["iterations"] == 8
+    # 4 applies per outer step (+ the initial and final residuals)
+    assert stats["apply_launches"] >= 4 * 4
+    bh = b.cpu().numpy()
+    xh = np.zeros_like(bh)
+    st2, rel2, its2, _ = hz.hz_solve(C, bh, xh, rtol=1e-6, ell=2)
+    x3 = C.alloc_field(3)
+    st3, rel3, its3, _ = hz.hz_solve(C, b, x3, rtol=1e-6, ell=2)
+    assert st2 == hz.HZ_OK and np.array_equal(its2, its3)
+    assert np.array_equal(xh, x3.cpu().numpy())
+    with pytest.raises(Exception):
+        hz.hz_solve(C, b, x3, rtol=1e-6, ell=3)

@@ -106,3 +106,32 @@ def test_gradient_ordering_ga_gm(ga_table):
     """Paper's Linear row ordering GA < Gm (Table 2) on the reduced analog."""
     gm = weights.WeightTable(4.0, 0.1, np.array([4.0]), weights.gm_weights()[None], 0)
     assert _gradient_case(61, ga_table) < _gradient_case(61, gm)
+
+
+def _small_helmholtz(ga_table, seed=5, n=(12, 11, 10)):
+    rng = np.random.default_rng(seed)
+    v = rng.uniform(1500.0, 3500.0, n)
+    P = op.Problem(v, 25.0, 5.0, 3, ga_table)
+    A = op.assemble(P)
+    b = op.point_sources(P, np.array([[5, 5, 4]]))[0].ravel()
+    return A, b
+
+
+def test_bicgstab_l1_is_bicgstab(ga_table):
+    """BiCGStab(1) is BiCGSTAB (Sleijpen & Fokkema 1993, §3): the oracle's two independently written
+    recurrences give the same iterates after 8 iterations (no residual replacement)."""
+    A, b = _small_helmholtz(ga_table)
+    x1, _, it1 = solvers.bicgstab(A, b, rtol=0.0, max_iter=8, replace_every=10 ** 9)
+    xl, _, itl = solvers.bicgstab_l(A, b, ell=1, rtol=0.0, max_iter=8)
+    assert it1 == itl == 8
+    assert np.linalg.norm(x1 - xl) <= 1e-9 * np.linalg.norm(x1)
+
+
+def test_bicgstab_l2_reaches_the_direct_solution(ga_table):
+    """BiCGStab(2) converges to the sparse direct (LU) solution of a complex-symmetric, indefinite
+    Helmholtz system with PML (random velocities)."""
+    A, b = _small_helmholtz(ga_table)
+    xd = solvers.solve_splu(A, b)
+    x2, rel, it = solvers.bicgstab_l(A, b, ell=2, rtol=1e-10)
+    assert rel <= 1e-10 and it % 2 == 0
+    assert np.linalg.norm(x2 - xd) <= 1e-7 * np.linalg.norm(xd)
