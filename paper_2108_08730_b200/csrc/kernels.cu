@@ -410,31 +410,32 @@ __global__ void __launch_bounds__(NT) norm2_kernel(const typename Cx<R>::T* __re
 // Helmholtz systems).  One outer step = two BiCGSTAB iterations' worth of applies (four):
 //   A: ρ0 ← −ω ρ0; ρ1 = (r̂0, r0); β = α ρ1/ρ0; ρ0 ← ρ1;            u0 = r0 − β u0
 //      u1 = A u0, σ = (r̂0, u1)                                          [apply, DOT1]
-//   B: α = ρ0/σ;                                                        r0 −= α u1; x += α u0
+//   B: α = ρ0/σ;                                                        r0 −= α u1
 //      r1 = A r0, ρ1 = (r̂0, r1)                                         [apply, DOT1]
-//   C: β = α ρ1/ρ0; ρ0 ← ρ1;                                u0 = r0 − β u0; u1 = r1 − β u1
+//   C: β = α ρ1/ρ0; ρ0 ← ρ1;                  x += α u0; u0 = r0 − β u0; u1 = r1 − β u1
 //      u2 = A u1, σ = (r̂0, u2)                                          [apply, DOT1]
-//   D: α = ρ0/σ;                        r0 −= α u1; r1 −= α u2; x += α u0; ‖r1‖² → dotG
+//   D: α = ρ0/σ;                                   r0 −= α u1; r1 −= α u2; ‖r1‖² → dotG
 //      r2 = A r1; (r2,r1), ‖r2‖², (r0,r1), (r0,r2)                      [apply, DOT4, r̂ := r0]
 //   E: (γ1, γ2) = argmin ‖r0 − γ1 r1 − γ2 r2‖ (2×2 normal equations in fp64); ω = γ2;
-//      x += γ1 r0 + γ2 r1; r0 −= γ1 r1 + γ2 r2; u0 −= γ1 u1 + γ2 u2;   ‖r0‖², (r̂0, r0) → dotR
+//      x += α u0 + γ1 r0 + γ2 r1; r0 −= γ1 r1 + γ2 r2; u0 −= γ1 u1 + γ2 u2;  ‖r0‖², (r̂0, r0) → dotR
 // (a, b) = Σ conj(a) b.  Fields: r0 = q.r, r1 = q.r1, r2 = q.r2, u0 = q.p, u1 = q.v, u2 = q.t.
+// The BiCG part's x += α u0 is deferred from B to C and from D to E, the next kernels that read u0
+// before changing it: 40 fewer B/pt per outer step (x and its compensation word are read and
+// written twice instead of three times), same arithmetic.
 // State: rho_used = ρ0 after A (read by B, C), rho_next = ρ0 after C (read by D, next A), alpha
 // (B, D), omega (E); no kernel reads a field it writes (every CTA derives the scalars itself).
 // =============================================================================================
+// x += dx in registers; with comp the iterate is the double-word x + lo (compensated update, as
+// bicg_update_kernel)
 template <typename R>
-__device__ __forceinline__ void x_add(const VecParams<R>& q, long long e, typename Cx<R>::T dx) {
-  typename Cx<R>::T xx = q.x[e];
-  if (q.xlo != nullptr) {   // double-word iterate (complex64): compensated update, as bicg_update_kernel
-    typename Cx<R>::T lo = q.xlo[e];
+__device__ __forceinline__ void x_upd(typename Cx<R>::T& xx, typename Cx<R>::T& lo, typename Cx<R>::T dx, bool comp) {
+  if (comp) {
     two_sum(xx.x, dx.x + lo.x, xx.x, lo.x);
     two_sum(xx.y, dx.y + lo.y, xx.y, lo.y);
-    q.xlo[e] = lo;
   } else {
     xx.x += dx.x;
     xx.y += dx.y;
   }
-  q.x[e] = xx;
 }
 
 template <typename R, int NT, int STEP>
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(NT) bicgl_kernel(VecParams<R> q) {
   SolverState& st = q.state[rhs];
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   bool brk = STEP != BCL_INIT && (st.flags & 1) != 0;
-  double2 s1 = make_double2(0.0, 0.0), s2 = s1;   // the step's two complex scalars
+  double2 s1 = make_double2(0.0, 0.0), s2 = s1, s3 = s1;   // the step's complex scalars
   if constexpr (STEP == BCL_INIT) {
     if (lead) {   // ρ0 = α = ω = 1... (α = 0 so that the first β vanishes); (r̂0, r0) = ‖r0‖² as r̂0 = r0
       st.rho_next[0] = 1.0;
@@ -480,8 +481,9 @@ __global__ void __launch_bounds__(NT) bicgl_kernel(VecParams<R> q) {
   } else if constexpr (STEP == BCL_C) {
     const double2 rho0 = make_double2(st.rho_used[0], st.rho_used[1]);
     const double2 rho1 = make_double2(q.dotA[2 * rhs], q.dotA[2 * rhs + 1]);
+    s2 = make_double2(st.alpha[0], st.alpha[1]);                                  // α of B
     if (brk || tiny(rho0, 1.0)) brk = true;
-    else s1 = zdiv(zmul(make_double2(st.alpha[0], st.alpha[1]), rho1), rho0);   // β
+    else s1 = zdiv(zmul(s2, rho1), rho0);                                         // β
     if (lead) {
       st.rho_next[0] = rho1.x;
       st.rho_next[1] = rho1.y;
@@ -494,6 +496,7 @@ __global__ void __launch_bounds__(NT) bicgl_kernel(VecParams<R> q) {
     const double2 c1 = make_double2(dB[3], -dB[4]);          // (r1, r0) = conj((r0, r1))
     const double2 c2 = make_double2(dB[5], -dB[6]);          // (r2, r0)
     const double det = a11 * a22 - (a21.x * a21.x + a21.y * a21.y);
+    s3 = make_double2(st.alpha[0], st.alpha[1]);   // α of D
     if (brk || !(det > 1e-14 * a11 * a22) || !isfinite(det)) {
       brk = true;
     } else {
@@ -507,44 +510,98 @@ __global__ void __launch_bounds__(NT) bicgl_kernel(VecParams<R> q) {
       st.omega[1] = s2.y;
     }
   }
-  if (brk) s1 = s2 = make_double2(0.0, 0.0);
+  // on breakdown the step's own scalars vanish; the deferred α u0 (C: s2, E: s3) is still applied
+  // (its α was stored as 0 if its own step broke down), keeping x consistent with r
+  if (brk) {
+    s1 = make_double2(0.0, 0.0);
+    if (STEP != BCL_C) s2 = s1;
+  }
   if (lead && brk) st.flags |= 1;
-  const C a = to_c<R>(s1), b = to_c<R>(s2);
+  const C a = to_c<R>(s1), b = to_c<R>(s2), g = to_c<R>(s3);
   const long long off = (long long)rhs * q.fstride + q.plane;
   constexpr int K = STEP == BCL_E ? 3 : (STEP == BCL_D ? 1 : 0);
   double part[K > 0 ? K : 1];
 #pragma unroll
   for (int k = 0; k < (K > 0 ? K : 1); k++) part[k] = 0.0;
+  // U elements per thread and pass: every operand of the U elements is loaded before the first store
+  // (the fields may alias as far as the compiler knows), so 2U..9U loads are in flight (HBM-bound)
+  constexpr int U = sizeof(R) == 4 ? 4 : 2;
+  const bool comp = q.xlo != nullptr;
+  C f0[U], f1[U], f2[U], f3[U], f4[U], f5[U], f6[U], f7[U], f8[U];
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < q.n; i += stride) {
-    const long long e = off + i;
-    if constexpr (STEP == BCL_INIT) {
-      q.rhat[e] = q.r[e];
-      q.p[e] = czero(R(0));
-    } else if constexpr (STEP == BCL_A) {   // u0 = r0 − β u0
-      q.p[e] = csub(q.r[e], cmul(a, q.p[e]));
-    } else if constexpr (STEP == BCL_B) {   // r0 −= α u1; x += α u0
-      q.r[e] = csub(q.r[e], cmul(a, q.v[e]));
-      x_add<R>(q, e, cmul(a, q.p[e]));
-    } else if constexpr (STEP == BCL_C) {   // u0 = r0 − β u0; u1 = r1 − β u1
-      q.p[e] = csub(q.r[e], cmul(a, q.p[e]));
-      q.v[e] = csub(q.r1[e], cmul(a, q.v[e]));
-    } else if constexpr (STEP == BCL_D) {   // r0 −= α u1; r1 −= α u2; x += α u0
-      const C u1 = q.v[e];
-      q.r[e] = csub(q.r[e], cmul(a, u1));
-      const C r1 = csub(q.r1[e], cmul(a, q.t[e]));
-      q.r1[e] = r1;
-      x_add<R>(q, e, cmul(a, q.p[e]));
-      part[0] += (double)r1.x * (double)r1.x + (double)r1.y * (double)r1.y;
-    } else {                      // E: x += γ1 r0 + γ2 r1; r0 −= γ1 r1 + γ2 r2; u0 −= γ1 u1 + γ2 u2
-      const C r0 = q.r[e], r1 = q.r1[e];
-      x_add<R>(q, e, cadd(cmul(a, r0), cmul(b, r1)));
-      const C rn = csub(r0, cadd(cmul(a, r1), cmul(b, q.r2[e])));
-      q.r[e] = rn;
-      q.p[e] = csub(q.p[e], cadd(cmul(a, q.v[e]), cmul(b, q.t[e])));
-      const C rh = q.rhat[e];
-      part[0] += (double)rn.x * (double)rn.x + (double)rn.y * (double)rn.y;
-      acc_cdot(part[1], part[2], rh, rn);
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < q.n; i0 += U * stride) {
+#pragma unroll
+    for (int k = 0; k < U; k++) {
+      const long long i = i0 + k * stride;
+      if (i >= q.n) continue;
+      const long long e = off + i;
+      if constexpr (STEP == BCL_INIT) {
+        f0[k] = q.r[e];
+      } else if constexpr (STEP == BCL_A) {
+        f0[k] = q.r[e];
+        f1[k] = q.p[e];
+      } else if constexpr (STEP == BCL_B) {
+        f0[k] = q.r[e];
+        f1[k] = q.v[e];
+      } else if constexpr (STEP == BCL_C) {
+        f0[k] = q.p[e];
+        f1[k] = q.x[e];
+        if (comp) f2[k] = q.xlo[e];
+        f3[k] = q.r[e];
+        f4[k] = q.r1[e];
+        f5[k] = q.v[e];
+      } else if constexpr (STEP == BCL_D) {
+        f0[k] = q.r[e];
+        f1[k] = q.v[e];
+        f2[k] = q.r1[e];
+        f3[k] = q.t[e];
+      } else {
+        f0[k] = q.r[e];
+        f1[k] = q.r1[e];
+        f2[k] = q.p[e];
+        f3[k] = q.x[e];
+        if (comp) f4[k] = q.xlo[e];
+        f5[k] = q.r2[e];
+        f6[k] = q.v[e];
+        f7[k] = q.t[e];
+        f8[k] = q.rhat[e];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; k++) {
+      const long long i = i0 + k * stride;
+      if (i >= q.n) continue;
+      const long long e = off + i;
+      if constexpr (STEP == BCL_INIT) {
+        q.rhat[e] = f0[k];
+        q.p[e] = czero(R(0));
+      } else if constexpr (STEP == BCL_A) {   // u0 = r0 − β u0
+        q.p[e] = csub(f0[k], cmul(a, f1[k]));
+      } else if constexpr (STEP == BCL_B) {   // r0 −= α u1
+        q.r[e] = csub(f0[k], cmul(a, f1[k]));
+      } else if constexpr (STEP == BCL_C) {   // x += α u0 (of B); u0 = r0 − β u0; u1 = r1 − β u1
+        const C u0 = f0[k];
+        x_upd<R>(f1[k], f2[k], cmul(b, u0), comp);
+        q.x[e] = f1[k];
+        if (comp) q.xlo[e] = f2[k];
+        q.p[e] = csub(f3[k], cmul(a, u0));
+        q.v[e] = csub(f4[k], cmul(a, f5[k]));
+      } else if constexpr (STEP == BCL_D) {   // r0 −= α u1; r1 −= α u2
+        q.r[e] = csub(f0[k], cmul(a, f1[k]));
+        const C r1 = csub(f2[k], cmul(a, f3[k]));
+        q.r1[e] = r1;
+        part[0] += (double)r1.x * (double)r1.x + (double)r1.y * (double)r1.y;
+      } else {   // E: x += α u0 (of D) + γ1 r0 + γ2 r1; r0 −= γ1 r1 + γ2 r2; u0 −= γ1 u1 + γ2 u2
+        const C r0 = f0[k], r1 = f1[k], u0 = f2[k];
+        x_upd<R>(f3[k], f4[k], cadd(cmul(g, u0), cadd(cmul(a, r0), cmul(b, r1))), comp);
+        q.x[e] = f3[k];
+        if (comp) q.xlo[e] = f4[k];
+        const C rn = csub(r0, cadd(cmul(a, r1), cmul(b, f5[k])));
+        q.r[e] = rn;
+        q.p[e] = csub(u0, cadd(cmul(a, f6[k]), cmul(b, f7[k])));
+        part[0] += (double)rn.x * (double)rn.x + (double)rn.y * (double)rn.y;
+        acc_cdot(part[1], part[2], f8[k], rn);
+      }
     }
   }
   if constexpr (K > 0) {
