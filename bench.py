@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--max-iter", type=int, default=20000)
     ap.add_argument("--ell", type=int, choices=[1, 2], default=1, help="1: BiCGSTAB (default), 2: BiCGStab(2)")
+    ap.add_argument("--replace-every", type=int, default=50,
+                    help="residual replacement period (the stagnation window is max(20x this, 1000) iterations)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=30, help="oracle BiCGSTAB iterations in the cpu_baseline sample")
@@ -354,7 +356,8 @@ def run_hz(args):
         else:
             x_out.zero_()
         st, rel, its, stt = hz.hz_solve(C, b, x_out, rtol=args.rtol, max_iter=args.max_iter,
-                                        timing=True, ell=args.ell, stream=stream)   # a6, a7
+                                        replace_every=args.replace_every, timing=True, ell=args.ell,
+                                        stream=stream)                              # a6, a7
         return st, rel, its, stt
 
     def timed(v_in, x_out, k):
