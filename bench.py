@@ -64,7 +64,9 @@ def parse():
     ap.add_argument("--max-iter", type=int, default=20000)
     ap.add_argument("--ell", type=int, choices=[1, 2], default=1, help="1: BiCGSTAB (default), 2: BiCGStab(2)")
     ap.add_argument("--replace-every", type=int, default=50,
-                    help="residual replacement period (the stagnation window is max(20x this, 1000) iterations)")
+                    help="residual replacement period")
+    ap.add_argument("--stall-window", type=int, default=0,
+                    help="iterations without a 10%% residual drop before a RHS is retired (0: max(20 x replace-every, 1000))")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=30, help="oracle BiCGSTAB iterations in the cpu_baseline sample")
@@ -357,6 +359,7 @@ def run_hz(args):
             x_out.zero_()
         st, rel, its, stt = hz.hz_solve(C, b, x_out, rtol=args.rtol, max_iter=args.max_iter,
                                         replace_every=args.replace_every, timing=True, ell=args.ell,
+                                        stall_window=args.stall_window,
                                         stream=stream)                              # a6, a7
         return st, rel, its, stt
 

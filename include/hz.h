@@ -172,7 +172,7 @@ hz_status hz_apply_impedance(const hz_coeffs* c, void* u, void* au, int nrhs, vo
  * the x update, device-resident, folded into x on exit), so the true residual can reach 1e-6 and
  * below (a plain complex64 iteration floors near 1e-6 on the configs of BASELINE.json); the
  * iteration itself runs to rtol/2 so the fp64-recomputed residual lands below rtol.  A RHS whose
- * true residual stagnates (stats.stagnated) is retired with HZ_NOT_CONVERGED and its best x.
+ * true residual stagnates (stats.stagnated) is retired with HZ_NOT_CONVERGED and its last iterate.
  * Host pointers for b / x are accepted: the call stages them (pinned) through device buffers.
  * Returns HZ_OK, HZ_NOT_CONVERGED or HZ_BREAKDOWN (outputs valid), or an error.
  * ------------------------------------------------------------------------------------------- */
@@ -187,6 +187,9 @@ typedef struct {
                         residual polynomial; four applies per outer step, counted as two
                         iterations; robust where BiCGSTAB's omega -> 0 stalls it — DESIGN.md
                         reading A23).  Any other value: HZ_ERR_INVALID_ARG.            */
+  int stall_window;  /* a RHS whose true residual has not dropped 10% within this many
+                        iterations is retired (HZ_NOT_CONVERGED, stats.stagnated = 1);
+                        0 = default max(20*replace_every, 1000); < 0 = never            */
 } hz_solve_opts;
 
 typedef struct {
@@ -202,7 +205,7 @@ typedef struct {
   int restarts;             /* breakdown restarts                                                */
   int iterations;           /* BiCGSTAB iterations of the batch (max over RHS)                   */
   int stagnated;            /* 1 if some RHS was retired because its true residual stagnated
-                               (no 10% reduction in max(20*replace_every, 1000) iterations)      */
+                               (no 10% reduction in stall_window iterations)      */
 } hz_solve_stats;
 
 hz_status hz_solve(const hz_coeffs* c, const void* b, void* x, int nrhs, const hz_solve_opts* opts,

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <atomic>
+#include <climits>
 #include <map>
 #include <mutex>
 #include <cmath>
@@ -1317,7 +1318,9 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   std::vector<double> best(nrhs, HUGE_VAL);
   std::vector<int> best_it(nrhs, 0);
   bool stagnated_any = false;
-  const int stall_iters = std::max(20 * std::max(1, o.replace_every), 1000);
+  const int stall_iters = o.stall_window > 0   ? o.stall_window
+                          : o.stall_window < 0 ? INT_MAX
+                                               : std::max(20 * std::max(1, o.replace_every), 1000);
   // initial convergence check (x0 may already solve the system)
   HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
   HZ_CUDA(cudaStreamSynchronize(s));
@@ -1472,7 +1475,7 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
 extern "C" hz_status hz_solve(const hz_coeffs* c, const void* b, void* x, int nrhs, const hz_solve_opts* opts,
                               double* relres_out, int* iters_out, hz_solve_stats* stats, void* stream) {
   if (!c || !b || !x || nrhs < 1) { set_error("hz_solve: bad arguments"); return HZ_ERR_INVALID_ARG; }
-  hz_solve_opts o = {1e-6, 20000, 50, 10, 0, 1};
+  hz_solve_opts o = {1e-6, 20000, 50, 10, 0, 1, 0};
   if (opts) o = *opts;
   if (!(o.rtol > 0) || o.max_iter < 1) { set_error("hz_solve: need rtol > 0, max_iter >= 1"); return HZ_ERR_INVALID_ARG; }
   if (o.ell == 0) o.ell = 1;

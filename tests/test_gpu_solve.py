@@ -210,3 +210,21 @@ def test_bicgstab2_edge_cases(hz, ctx, table):
     assert np.array_equal(xh, x3.cpu().numpy())
     with pytest.raises(Exception):
         hz.hz_solve(C, b, x3, rtol=1e-6, ell=3)
+
+
+@pytest.mark.parametrize("ell", [1, 2])
+def test_stall_window(hz, ctx, table, ell):
+    """stall_window < 0 never retires (the iteration cap ends the solve); a short window retires a
+    RHS whose true residual has reached the complex64 floor (rtol 1e-14 is unreachable)."""
+    cfg = synth.get_config(1)
+    v, C = setup(hz, ctx, table, cfg, "c64")
+    b = C.alloc_field(1)
+    hz.hz_point_sources(C, synth.source_nodes(cfg), b)
+    x = C.alloc_field(1)
+    st, rel, its, stats = hz.hz_solve(C, b, x, rtol=1e-14, max_iter=400, stall_window=-1, ell=ell)
+    assert st == hz.HZ_NOT_CONVERGED and stats["stagnated"] == 0 and its[0] == 400, (st, its, stats)
+    assert rel[0] <= 1e-6
+    x = C.alloc_field(1)
+    st, rel, its, stats = hz.hz_solve(C, b, x, rtol=1e-14, max_iter=20000, stall_window=100, ell=ell)
+    assert st == hz.HZ_NOT_CONVERGED and stats["stagnated"] == 1 and its[0] < 20000, (st, its, stats)
+    assert rel[0] <= 1e-6
