@@ -1419,6 +1419,11 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
       }
       if (brk) {  // restart broken RHS with r̂0 = r = b − A x (all active RHS restart together)
         HZ_TRY(resid(false));
+        // the recomputed true residuals also feed the convergence / stagnation test, so a RHS at its
+        // rounding floor (where breakdowns recur) is retired by the stall window, not the restart cap
+        HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
+        HZ_CUDA(cudaStreamSynchronize(s));
+        HZ_TRY(retire(true));
         HZ_TRY(init());
         restarts++;
         if (restarts > 50) break;
