@@ -145,6 +145,25 @@ def test_apply_full_size_sampled(hz, ctx, table, ga_table, cfg_i):
     assert np.all(np.isfinite(got))
 
 
+def test_apply_config5_whole_grid_sampled(hz, ctx, table, ga_table):
+    """Maximum size: config 5's whole 1201×1201×401 grid (5.8·10⁸ points, 4.6 GB per complex64
+    field, 32-bit in-field offsets near their limit) on one GPU, 2 RHS, bench launch configuration;
+    sampled rows (4000 random + boundary corners, both RHS) against the oracle."""
+    cfg = synth.get_config(5)
+    v = synth.velocity_slab(cfg, 0, cfg.nz, device="cuda").astype(np.float32)
+    C = assemble(hz, ctx, table, v, cfg.h, cfg.freq, cfg.npml, "c64")
+    u = synth.random_field((2,) + cfg.shape, seed=15)
+    got = gpu_apply(hz, C, u)
+    del C
+    nodes = sample_nodes(cfg, 4000, 5)
+    P = op.Problem(v.astype(np.float64), cfg.h, cfg.freq, cfg.npml, ga_table)
+    for r in range(2):
+        ref = op.apply_rows(P, u[r], nodes)
+        g = got[r, nodes[:, 2], nodes[:, 1], nodes[:, 0]]
+        assert rel(g, ref) <= TOL["c64"], r
+    assert np.all(np.isfinite(got[:, ::7]))
+
+
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 def test_record_and_pml_export(hz, ctx, table, ga_table, dtype):
     rng = np.random.default_rng(21)
