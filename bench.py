@@ -14,6 +14,9 @@ Reported (one JSON line, rank 0):
           polls are inside that time; `apply_kernel_gpts_s` is the same count over the apply
           kernels' own CUDA-event time)
   solve_s_per_rhs, iterations, relres       BiCGSTAB part of the metric
+  solver_alt  the same step solved with the other Krylov method (BiCGStab(2) beside the default
+          BiCGSTAB; `--ell 2` swaps them): ms/step, s/RHS, iterations, relres (min(K, 3) timed
+          steps after one warm-up, same timing rules; `--no-alt` skips it)
   roofline  dominant kernel = the fused coefficient + 27-point apply (apply27_kernel): algorithmic
           bytes of every apply launch (v once + fields per active RHS) ÷ its CUDA-event
           time measured inside the timed steps, against MEASURED_PEAKS.json hbm_gbs
@@ -68,6 +71,7 @@ def parse():
     ap.add_argument("--stall-window", type=int, default=0,
                     help="iterations without a 10%% residual drop before a RHS is retired (0: max(20 x replace-every, 1000))")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the other Krylov method's timing (solver_alt)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=30, help="oracle BiCGSTAB iterations in the cpu_baseline sample")
     ap.add_argument("--ref-iters", type=int, default=4, help="oracle BiCGSTAB iterations per --impl reference step")
@@ -348,7 +352,7 @@ def run_hz(args):
         if ws > 1:
             dist.barrier()
 
-    def one_step(v_in, x_out):
+    def one_step(v_in, x_out, ell=None):
         T = hz.hz_build_weight_table(*TABLE_ARGS)                                  # a1
         C = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, v_in, freq, T, npml=cfg.npml,
                                   z0=z0, nz_local=nzl, dtype=dt_code)               # a2–a5
@@ -358,12 +362,13 @@ def run_hz(args):
         else:
             x_out.zero_()
         st, rel, its, stt = hz.hz_solve(C, b, x_out, rtol=args.rtol, max_iter=args.max_iter,
-                                        replace_every=args.replace_every, timing=True, ell=args.ell,
+                                        replace_every=args.replace_every, timing=True,
+                                        ell=args.ell if ell is None else ell,
                                         stall_window=args.stall_window,
                                         stream=stream)                              # a6, a7
         return st, rel, its, stt
 
-    def timed(v_in, x_out, k):
+    def timed(v_in, x_out, k, ell=None):
         tot_ms, stats, last = 0.0, [], None
         l0 = hz.hz_kernel_launch_count()
         for _ in range(k):
@@ -373,7 +378,7 @@ def run_hz(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            last = one_step(v_in, x_out)
+            last = one_step(v_in, x_out, ell)
             e1.record(stream)
             torch.cuda.synchronize(dev)
             barrier()
@@ -415,6 +420,18 @@ def run_hz(args):
         e2e = {"value": pts_e_all / (tmax_e * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d) * ws,
                "d2h_bytes_per_step": int(d2h) * ws, "ms_per_step": tmax_e / args.steps}
 
+    # ---------------- the other Krylov method on the same step (time to solution beside it) ----------------
+    alt = None
+    if not args.no_alt:
+        ell_alt = 3 - args.ell
+        one_step(v_dev, x, ell_alt)
+        tot_a, _, last_a, _ = timed(v_dev, x, min(args.steps, 3), ell_alt)
+        (tmax_a,) = parallel.rank_max([tot_a], dev)
+        ka = min(args.steps, 3)
+        alt = {"solver": "BiCGSTAB" if ell_alt == 1 else "BiCGStab(2)", "ms_per_step": tmax_a / ka,
+               "solve_s_per_rhs": tmax_a / ka * 1e-3 / nrhs, "iterations": int(last_a[3]["iterations"]),
+               "relres_max": float(np.max(last_a[1])), "status": int(last_a[0]), "steps": ka}
+
     if rank != 0:
         if ws > 1:
             dist.barrier()
@@ -435,6 +452,7 @@ def run_hz(args):
                    "solver": "BiCGSTAB" if args.ell == 1 else "BiCGStab(2)",
                    "l2": "flushed before every step (256 MiB write); step working set > L2"},
         "solve_s_per_rhs": ms_per_step * 1e-3 / nrhs,
+        "solver_alt": alt,
         "iterations": int(stats[-1]["iterations"]),
         "relres_max": float(np.max(rel)),
         "status": int(st),
