@@ -186,7 +186,8 @@ typedef struct {
                         (Sleijpen & Fokkema 1993: two BiCG steps then a 2-term minimal-
                         residual polynomial; four applies per outer step, counted as two
                         iterations; robust where BiCGSTAB's omega -> 0 stalls it — DESIGN.md
-                        reading A23).  Any other value: HZ_ERR_INVALID_ARG.            */
+                        reading A23; max_iter is tested per outer step, so the count can
+                        end at max_iter + 1).  Any other value: HZ_ERR_INVALID_ARG.     */
   int stall_window;  /* a RHS whose true residual has not dropped 10% within this many
                         iterations is retired (HZ_NOT_CONVERGED, stats.stagnated = 1);
                         0 = default max(20*replace_every, 1000); < 0 = never            */
