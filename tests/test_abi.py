@@ -95,3 +95,26 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(hz.HzError) as e:
         hz.hz_ctx_create(0)
     assert e.value.status in (-5, -1)
+
+
+def test_c99_consumer(tmp_path, ga_table):
+    """include/hz.h compiles as strict C99 and libhz links from C: tests/c/abi_consumer.c builds the
+    default table through the ABI (host-only calls) and its row at G = 12 matches the oracle's."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    libdir = os.path.dirname(hz._LIBPATH)
+    exe = str(tmp_path / "abi_consumer")
+    subprocess.run([gcc, "-std=c99", "-pedantic", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c", "abi_consumer.c"), "-L", libdir, "-lhz",
+                    f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.splitlines()
+    fields = {ln.split()[0]: ln.split()[1:] for ln in out}
+    assert int(fields["n_g"][0]) == 361
+    row = np.array([float(t) for t in fields["row80"]])
+    assert np.max(np.abs(row - ga_table.u5[80])) <= 1e-8 * np.max(np.abs(ga_table.u5))
+    w7 = np.array([float(t) for t in fields["w7_80"]])
+    assert abs(w7[0] + w7[1] + w7[2] - 1.0) <= 1e-14 and abs(w7[3:].sum() - 1.0) <= 1e-14
+    assert "import" in fields and int(fields["invalid"][0]) == -1
