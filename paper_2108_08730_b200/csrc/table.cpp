@@ -12,9 +12,11 @@
 // block Gaussian elimination (block Thomas) in 80-bit long double, followed by two steps of
 // iterative refinement.  cond(normal) ~ 1.5e10 at lambda = 1e-2, so long double keeps the weights
 // accurate to ~1e-9 relative (the oracle uses numpy lstsq on the stacked matrix).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "hz_internal.h"
@@ -23,11 +25,14 @@ namespace hz {
 
 typedef long double ld;
 
-void h_row(ld G, ld theta, ld phi, ld H[5], ld* g) {
+namespace {
+// One row from the direction cosines' factors (cos φ, sin φ, cos θ, sin θ), evaluated in the same
+// order as h_row so that both give bit-identical rows.
+void h_row_cs(ld G, ld cphi, ld sphi, ld cth, ld sth, ld H[5], ld* g) {
   const ld pi = 3.141592653589793238462643383279502884L;
-  ld a = 2 * pi * cosl(phi) * cosl(theta) / G;
-  ld b = 2 * pi * cosl(phi) * sinl(theta) / G;
-  ld c = 2 * pi * sinl(phi) / G;
+  ld a = 2 * pi * cphi * cth / G;
+  ld b = 2 * pi * cphi * sth / G;
+  ld c = 2 * pi * sphi / G;
   ld ca = cosl(a), cb = cosl(b), cc = cosl(c);
   ld A = ca * cb * cc;
   ld B = ca * cb + ca * cc + cb * cc;
@@ -40,6 +45,9 @@ void h_row(ld G, ld theta, ld phi, ld H[5], ld* g) {
   H[4] = k * (12 * A - 4 * B);                            // H5
   *g = 0.5L * ((4 * pi * pi / (G * G) + 3) * A - B + C - 3);  // g
 }
+}  // namespace
+
+void h_row(ld G, ld theta, ld phi, ld H[5], ld* g) { h_row_cs(G, cosl(phi), sinl(phi), cosl(theta), sinl(theta), H, g); }
 
 namespace {
 
@@ -79,35 +87,47 @@ struct BlockSystem {
   std::vector<ld> rhs; // [n][5]
 };
 
-// Block Thomas: solve D_i w_i + off (w_{i-1} + w_{i+1}) = r_i.
-bool solve_block_tridiag(const BlockSystem& S, const std::vector<ld>& r, std::vector<ld>& w) {
+// Block Thomas for D_i w_i + off (w_{i-1} + w_{i+1}) = r_i.  factor(): the inverses of the eliminated
+// diagonal blocks D'_0 = D_0, D'_i = D_i - off^2 D'_{i-1}^{-1} (they do not depend on r, so the
+// iterative-refinement solves reuse them); solve(): r'_i = r_i - off D'_{i-1}^{-1} r'_{i-1}, then
+// back substitution.
+bool factor_block_tridiag(const BlockSystem& S, std::vector<ld>& invs) {
   const int n = S.n;
-  std::vector<ld> Dp(25 * n), rp(5 * n);
-  // forward elimination: D'_0 = D_0; D'_i = D_i - off^2 D'_{i-1}^{-1}; r'_i = r_i - off D'_{i-1}^{-1} r'_{i-1}
-  std::vector<ld> invs(25 * n);
+  invs.assign(25 * (size_t)n, 0.0L);
   for (int i = 0; i < n; i++) {
     ld Di[5][5];
     for (int a = 0; a < 5; a++)
       for (int b = 0; b < 5; b++) Di[a][b] = S.D[25 * i + 5 * a + b];
-    ld ri[5];
-    for (int a = 0; a < 5; a++) ri[a] = r[5 * i + a];
     if (i > 0) {
       const ld* Ip = &invs[25 * (i - 1)];
-      for (int a = 0; a < 5; a++) {
+      for (int a = 0; a < 5; a++)
         for (int b = 0; b < 5; b++) Di[a][b] -= S.off * S.off * Ip[5 * a + b];
-        ld s = 0;
-        for (int b = 0; b < 5; b++) s += Ip[5 * a + b] * rp[5 * (i - 1) + b];
-        ri[a] -= S.off * s;
-      }
     }
     ld Inv[5][5];
     if (!inv5(Di, Inv)) return false;
-    for (int a = 0; a < 5; a++) {
-      rp[5 * i + a] = ri[a];
+    for (int a = 0; a < 5; a++)
       for (int b = 0; b < 5; b++) invs[25 * i + 5 * a + b] = Inv[a][b];
+  }
+  return true;
+}
+
+void solve_block_tridiag(const BlockSystem& S, const std::vector<ld>& invs, const std::vector<ld>& r,
+                         std::vector<ld>& w) {
+  const int n = S.n;
+  std::vector<ld> rp(5 * (size_t)n);
+  for (int i = 0; i < n; i++) {
+    for (int a = 0; a < 5; a++) {
+      ld ri = r[5 * i + a];
+      if (i > 0) {
+        const ld* Ip = &invs[25 * (i - 1)];
+        ld s = 0;
+        for (int b = 0; b < 5; b++) s += Ip[5 * a + b] * rp[5 * (i - 1) + b];
+        ri -= S.off * s;
+      }
+      rp[5 * i + a] = ri;
     }
   }
-  w.assign(5 * n, 0.0L);
+  w.assign(5 * (size_t)n, 0.0L);
   for (int i = n - 1; i >= 0; i--) {
     ld t[5];
     for (int a = 0; a < 5; a++) t[a] = rp[5 * i + a] - (i + 1 < n ? S.off * w[5 * (i + 1) + a] : 0.0L);
@@ -117,7 +137,6 @@ bool solve_block_tridiag(const BlockSystem& S, const std::vector<ld>& r, std::ve
       w[5 * i + a] = s;
     }
   }
-  return true;
 }
 
 }  // namespace
@@ -138,25 +157,44 @@ hz_status build_table(double g_min, double g_max, double dg, double lambda,
   S.D.assign(25 * (size_t)n, 0.0L);
   S.rhs.assign(5 * (size_t)n, 0.0L);
   S.off = -(ld)lambda;
-  for (int i = 0; i < n; i++) {
-    ld G = (ld)g_min + (ld)dg * i;
-    for (size_t kp = 0; kp < phi.size(); kp++)        // phi outer
-      for (size_t jt = 0; jt < theta.size(); jt++) {  // theta inner
-        ld H[5], g;
-        h_row(G, (ld)theta[jt], (ld)phi[kp], H, &g);
-        for (int a = 0; a < 5; a++) {
-          for (int b = 0; b < 5; b++) S.D[25 * i + 5 * a + b] += H[a] * H[b];
-          S.rhs[5 * i + a] += H[a] * g;
+  // the angles' sines and cosines once (the G loop only needs cos of the scaled direction cosines)
+  std::vector<ld> cph(phi.size()), sph(phi.size()), cth(theta.size()), sth(theta.size());
+  for (size_t k = 0; k < phi.size(); k++) { cph[k] = cosl((ld)phi[k]); sph[k] = sinl((ld)phi[k]); }
+  for (size_t k = 0; k < theta.size(); k++) { cth[k] = cosl((ld)theta[k]); sth[k] = sinl((ld)theta[k]); }
+  // the per-G blocks are independent: threads own contiguous ranges of G, each block is summed in
+  // the same (phi outer, theta inner) order as a serial loop, so the table is bitwise thread-count
+  // independent
+  auto assemble = [&](int i0, int i1) {
+    for (int i = i0; i < i1; i++) {
+      ld G = (ld)g_min + (ld)dg * i;
+      for (size_t kp = 0; kp < phi.size(); kp++)        // phi outer
+        for (size_t jt = 0; jt < theta.size(); jt++) {  // theta inner
+          ld H[5], g;
+          h_row_cs(G, cph[kp], sph[kp], cth[jt], sth[jt], H, &g);
+          for (int a = 0; a < 5; a++) {
+            for (int b = 0; b < 5; b++) S.D[25 * i + 5 * a + b] += H[a] * H[b];
+            S.rhs[5 * i + a] += H[a] * g;
+          }
         }
-      }
-    ld d = (i == 0 || i == n - 1) ? 1.0L : 2.0L;  // D^T D of first differences (no boundary rows)
-    for (int a = 0; a < 5; a++) S.D[25 * i + 5 * a + a] += (ld)lambda * d;
+      ld d = (i == 0 || i == n - 1) ? 1.0L : 2.0L;  // D^T D of first differences (no boundary rows)
+      for (int a = 0; a < 5; a++) S.D[25 * i + 5 * a + a] += (ld)lambda * d;
+    }
+  };
+  const long long rows = (long long)n * (long long)(phi.size() * theta.size());
+  const int nthr = rows < 4000 ? 1 : (int)std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency()));
+  if (nthr == 1) {
+    assemble(0, n);
+  } else {
+    std::vector<std::thread> pool;
+    for (int k = 0; k < nthr; k++) pool.emplace_back(assemble, (int)((long long)n * k / nthr), (int)((long long)n * (k + 1) / nthr));
+    for (auto& t : pool) t.join();
   }
-  std::vector<ld> w;
-  if (!solve_block_tridiag(S, S.rhs, w)) {
+  std::vector<ld> w, invs;
+  if (!factor_block_tridiag(S, invs)) {
     set_error("hz_build_weight_table: singular normal equations (lambda = 0 with rank-3 blocks? A14)");
     return HZ_ERR_RANK;
   }
+  solve_block_tridiag(S, invs, S.rhs, w);
   // iterative refinement on the normal equations
   for (int it = 0; it < 2; it++) {
     std::vector<ld> r(5 * (size_t)n);
@@ -169,7 +207,7 @@ hz_status build_table(double g_min, double g_max, double dg, double lambda,
         r[5 * i + a] = s;
       }
     std::vector<ld> dw;
-    if (!solve_block_tridiag(S, r, dw)) break;
+    solve_block_tridiag(S, invs, r, dw);
     for (size_t k = 0; k < w.size(); k++) w[k] += dw[k];
   }
   out->g_min = g_min;
