@@ -16,7 +16,7 @@ Reported (one JSON line, rank 0):
   solve_s_per_rhs, iterations, relres       BiCGSTAB part of the metric
   solver_alt  the same step solved with the other Krylov method (BiCGStab(2) beside the default
           BiCGSTAB; `--ell 2` swaps them): ms/step, s/RHS, iterations, relres (min(K, 3) timed
-          steps after one warm-up, same timing rules; `--no-alt` skips it)
+          steps after one warm-up, same timing rules; N = 1 only; `--no-alt` skips it)
   roofline  dominant kernel = the fused coefficient + 27-point apply (apply27_kernel): algorithmic
           bytes of every apply launch (v once + fields per active RHS) ÷ its CUDA-event
           time measured inside the timed steps, against MEASURED_PEAKS.json hbm_gbs
@@ -422,7 +422,7 @@ def run_hz(args):
 
     # ---------------- the other Krylov method on the same step (time to solution beside it) ----------------
     alt = None
-    if not args.no_alt:
+    if not args.no_alt and ws == 1:
         ell_alt = 3 - args.ell
         one_step(v_dev, x, ell_alt)
         tot_a, _, last_a, _ = timed(v_dev, x, min(args.steps, 3), ell_alt)
