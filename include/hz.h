@@ -161,7 +161,9 @@ void hz_coeffs_destroy(hz_coeffs* c);
 hz_status hz_apply_impedance(const hz_coeffs* c, void* u, void* au, int nrhs, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
- * (4) solve — batched BiCGSTAB for A x_r = b_r, r = 0..nrhs-1 (north star (3)); blocking.
+ * (4) solve — batched BiCGSTAB (or BiCGStab(2), opts.ell) for A x_r = b_r, r = 0..nrhs-1 (north
+ * star (3)); blocking.  opts == NULL: the defaults below; zero-initialise the struct before setting
+ * fields so that ell = 0 and stall_window = 0 select their defaults.
  * b, x: [nrhs][nz_local+2][ny][nx]; x holds the initial guess on entry (zeros OK) and the final
  * iterate on exit.  Each RHS iterates independently (per-RHS scalars on the device, fp64 dot
  * accumulation, residual replacement every replace_every iterations) and stops when its
@@ -204,7 +206,7 @@ typedef struct {
   double apply_points_total;/* grid points x active RHS processed by all applies                  */
   int replacements;         /* residual replacements performed                                   */
   int restarts;             /* breakdown restarts                                                */
-  int iterations;           /* BiCGSTAB iterations of the batch (max over RHS)                   */
+  int iterations;           /* BiCGSTAB(-equivalent) iterations of the batch (max over RHS)       */
   int stagnated;            /* 1 if some RHS was retired because its true residual stagnated
                                (no 10% reduction in stall_window iterations)      */
 } hz_solve_stats;
