@@ -1,34 +1,32 @@
 #!/usr/bin/env python
 """bench.py — B200 benchmark of the wavelength-adaptive 27-point Helmholtz hot path
-(arXiv 2108.08730; BASELINE.json `metric`).
+(arXiv 2108.08730; BASELINE.json `metric`: adaptive 27-pt apply Gpts/s & HBM % of peak; BiCGSTAB
+s/RHS at 1/2/4/8 GPU).
 
-One STEP is one pass of the whole north-star hot path (SURVEY.md §8(a) rows a1–a8) over the
-N=1 workload, BASELINE configs[1] (config 2: 101³ linear-gradient model, 5 Hz, 4 point sources,
-complex64):
-    hz_build_weight_table (a1, host C++)  →  hz_assemble_coeffs (a2–a5)  →
-    hz_point_sources (a8)  →  hz_solve: batched BiCGSTAB to ‖b−Ax‖/‖b‖ ≤ 1e-6 (a6, a7).
+Headline workload: BASELINE configs[3] = config 4, the 801×801×187 thrust-belt model (the overthrust
+stand-in, Table 1), complex64, f = 10 Hz, z-slab split over the N GPUs (total work
+fixed → "scaling": "strong").  One timed STEP = one hz_apply_impedance of a batch of `--nrhs` (8)
+fields: the fused per-point coefficient build (G = v/(f h), table lookup + interpolation, PML
+stretching; §8(a) a2–a5) and the matrix-free 27-point apply (a6), halo planes over NCCL for N > 1.
+  value      Gpts/s = grid points × nrhs ÷ the step's device time (max over ranks)
+  roofline   that launch: algorithmic bytes (4 + 16·nrhs per point) ÷ its CUDA-event
+             time, against MEASURED_PEAKS.json hbm_gbs; `traffic` = ncu DRAM bytes per launch from
+             profiles/ncu_traffic.json (the committed capture of this workload)
+  solve      the rest of the hot path on the same workload: weight table (a1) + assemble + point
+             sources (a8) + batched solve (a7) of `--solve-nrhs` (2) sources to ‖b−Ax‖/‖b‖ ≤ 1e-6,
+             BiCGSTAB (the north star's method) and BiCGStab(2) beside it, each bounded by
+             --solve-max-iter; s/RHS, iterations, relres and status reported as they come out
+  e2e        the same metric through the C ABI with HOST (pinned) u and Au buffers: the H2D copy of
+             the batch and the D2H copy of the result are inside the timed region
+  cpu_baseline / --impl reference   the CPU oracle (scipy CSR SpMV, complex128, 1 core) on a
+             z-chunk of the same model
+  apply_nrhs1, fixed_weights, record_mode, gam_rule, config2_solve   extra measurements (N = 1)
+`--weak`: the config-5 weak-scaling series 1201×1201×(50N+1): value = apply
+Gpts/s of 1 RHS per GPU's slab, plus the time per BiCGSTAB iteration; "scaling": "weak".
 
-Reported (one JSON line, rank 0):
-  value   apply Gpts/s of the whole step = Σ over the step's operator applies of
-          (grid points × active RHS) ÷ step time  (the solve's vector kernels, reductions and host
-          polls are inside that time; `apply_kernel_gpts_s` is the same count over the apply
-          kernels' own CUDA-event time)
-  solve_s_per_rhs, iterations, relres       BiCGSTAB part of the metric
-  solver_alt  the same step solved with the other Krylov method (BiCGStab(2) beside the default
-          BiCGSTAB; `--ell 2` swaps them): ms/step, s/RHS, iterations, relres (min(K, 3) timed
-          steps after one warm-up, same timing rules; N = 1 only; `--no-alt` skips it)
-  roofline  dominant kernel = the fused coefficient + 27-point apply (apply27_kernel): algorithmic
-          bytes of every apply launch (v once + fields per active RHS) ÷ its CUDA-event
-          time measured inside the timed steps, against MEASURED_PEAKS.json hbm_gbs
-  e2e     same metric through the C ABI with HOST buffers: v (pinned) in, x0 in, x out — the copies
-          are inside the timed region
-  cpu_baseline  the CPU oracle (scipy CSR BiCGSTAB, complex128, 1 core) on a bounded sample
-`--impl reference` times that oracle as the reference arm.
-
-Multi-GPU (torchrun, one rank per GPU): the grid is split in z-slabs (halo planes and dot products
-over NCCL inside libhz); total work is fixed → "scaling": "strong".  Timing: W warm-up steps, then
-K steps each bracketed by barrier + synchronize, L2 flushed (256 MiB write) before every step, CUDA
-events on the launching stream, max over ranks.
+Timing: W warm-up steps, then K steps each bracketed by barrier + synchronize, L2 flushed (256 MiB
+write) before every step (the step's working set, ≥ 16 GB, exceeds L2 anyway), CUDA events on the
+launching stream, max over ranks; nvidia-smi clocks sampled during the timed steps.
 """
 from __future__ import annotations
 
@@ -56,28 +54,22 @@ TABLE_ARGS = (4.0, 40.0, 0.1, 1e-2)       # G range, ΔG, λ (BASELINE configs[0
 def parse():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["hz", "reference"], default="hz")
-    ap.add_argument("--config", type=int, default=2, help="BASELINE config index 1..5 (default 2 = configs[1])")
-    ap.add_argument("--freq", type=float, default=None, help="frequency override (config 4: 5 or 10 Hz)")
-    ap.add_argument("--nrhs", type=int, default=None, help="number of sources (default: the config's)")
-    ap.add_argument("--dtype", choices=["c64", "c128"], default="c64")
+    ap.add_argument("--config", type=int, default=4, help="BASELINE config index 1..5 (default 4 = configs[3])")
+    ap.add_argument("--freq", type=float, default=None, help="frequency (default: the config's highest)")
+    ap.add_argument("--nrhs", type=int, default=8, help="fields per apply batch (headline)")
+    ap.add_argument("--weak", action="store_true", help="config-5 weak-scaling slab series 1201x1201x(50N+1)")
+    ap.add_argument("--solve-nrhs", type=int, default=2, help="sources in the timed solve leg")
+    ap.add_argument("--solve-max-iter", type=int, default=8000, help="iteration bound of each solve leg")
     ap.add_argument("--rtol", type=float, default=1e-6)
-    ap.add_argument("--max-iter", type=int, default=20000)
-    ap.add_argument("--ell", type=int, choices=[1, 2], default=1, help="1: BiCGSTAB (default), 2: BiCGStab(2)")
-    ap.add_argument("--replace-every", type=int, default=50,
-                    help="residual replacement period")
-    ap.add_argument("--stall-window", type=int, default=0,
-                    help="iterations without a 10%% residual drop before a RHS is retired (0: max(20 x replace-every, 1000))")
+    ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-alt", action="store_true", help="skip the other Krylov method's timing (solver_alt)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the extra measurements (N = 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=30, help="oracle BiCGSTAB iterations in the cpu_baseline sample")
-    ap.add_argument("--ref-iters", type=int, default=4, help="oracle BiCGSTAB iterations per --impl reference step")
-    ap.add_argument("--no-large", action="store_true",
-                    help="skip the apply-only roofline measurement on the large config (N=1 only)")
-    ap.add_argument("--large-config", type=int, default=4, help="config of the apply-only roofline measurement")
+    ap.add_argument("--cpu-planes", type=int, default=4, help="z-planes of the oracle's CSR sample")
+    ap.add_argument("--cpu-spmv", type=int, default=10, help="oracle SpMVs timed in the cpu_baseline sample")
     return ap.parse_args()
 
 
@@ -89,38 +81,32 @@ def dist_env():
     return ws, rank, local
 
 
-def workload(args):
+def workload(args, ws):
+    """(cfg, freq): the headline model, or the weak-scaling slab series of config 5."""
+    if args.weak:
+        cfg = synth.get_config(5, nz=50 * ws + 1)
+        return cfg, cfg.freq
     cfg = synth.get_config(args.config)
-    freq = args.freq if args.freq is not None else cfg.freqs[-1] if args.config == 4 else cfg.freq
-    nodes = synth.source_nodes(cfg)
-    if args.nrhs is not None:
-        reps = int(np.ceil(args.nrhs / len(nodes)))
-        nodes = np.concatenate([nodes] * reps)[: args.nrhs]
-    return cfg, freq, nodes
-
-
-def workload_name(cfg, freq, nrhs, dtype):
-    return (f"config{cfg.index} {cfg.name} {cfg.nx}x{cfg.ny}x{cfg.nz} h={cfg.h:g}m f={freq:g}Hz "
-            f"npml={cfg.npml} nrhs={nrhs} {dtype}: table+assemble+sources+BiCGSTAB(rtol)")
+    freq = args.freq if args.freq is not None else cfg.freqs[-1]
+    return cfg, freq
 
 
 def read_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(path) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def read_traffic(workload_key):
-    """dram bytes per apply launch from a committed ncu --set full capture (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def read_traffic(key):
+    """ncu DRAM bytes per launch for a workload key from the committed capture (profiles/), or None."""
     try:
-        with open(path) as f:
-            d = json.load(f)
-        e = d.get(workload_key)
-        return None if e is None else float(e["dram_bytes_per_launch"])
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            e = json.load(f).get(key)
+        return None if e is None else {"dram_bytes_per_launch": float(e["dram_bytes_per_launch"]),
+                                       "source": e.get("source")}
     except Exception:
         return None
 
@@ -168,7 +154,6 @@ class ClockSampler:
             for n, v in zip(names, parts[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        # "under load": samples within the top half of the observed range
         load = [x for x in sm if sm and x >= 0.5 * max(sm)] or sm
         return {"sm_mhz": statistics.median(load) if load else None,
                 "sm_max_mhz": max(smax) if smax else None,
@@ -176,154 +161,74 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------------
-def oracle_sample(cfg, freq, nodes, iters, v=None):
-    """The CPU oracle as it stands (test infrastructure; bench.py's cpu_baseline / reference leg):
-    explicit CSR impedance matrix + scipy-SpMV BiCGSTAB in complex128 on one core."""
+# CPU oracle (test infrastructure: bench.py's cpu_baseline leg and --impl reference only)
+def oracle_chunk(cfg, freq, planes):
+    """The oracle's explicit CSR impedance matrix of a `planes`-plane z-chunk of the model (the oracle's
+    z-chunked SpMV of SURVEY §8(d)), on one core."""
     from threadpoolctl import threadpool_limits
 
     from oracle import operator as op
-    from oracle import solvers, weights
+    from oracle import weights
     with threadpool_limits(1):
+        z0 = max(0, cfg.nz // 2 - planes // 2)
+        v = synth.velocity_slab(cfg, z0, planes).astype(np.float32).astype(np.float64)
         t0 = time.perf_counter()
         tab = weights.build_adaptive_table(*TABLE_ARGS)
+        A = op.assemble(op.Problem(v, cfg.h, freq, cfg.npml, tab))
         t1 = time.perf_counter()
-        if v is None:
-            v = synth.velocity_model(cfg).astype(np.float32).astype(np.float64)
-        P = op.Problem(v, cfg.h, freq, cfg.npml, tab)
-        A = op.assemble(P)
-        b = op.point_sources(P, nodes[:1])[0].ravel()
-        t2 = time.perf_counter()
-    return {"A": A, "b": b, "t_table": t1 - t0, "t_assemble": t2 - t1, "npts": A.shape[0]}
+    u = synth.random_field((A.shape[0],), seed=99).astype(np.complex128)
+    return {"A": A, "u": u, "t_assemble": t1 - t0, "npts": A.shape[0], "planes": planes, "z0": z0}
 
 
-def oracle_iters(S, iters):
+def oracle_spmv(S, n):
     from threadpoolctl import threadpool_limits
-
-    from oracle import solvers
     with threadpool_limits(1):
         t0 = time.perf_counter()
-        _, rel, it = solvers.bicgstab(S["A"], S["b"], rtol=1e-30, max_iter=iters)
-        dt = time.perf_counter() - t0
-    return dt, it
+        for _ in range(n):
+            S["u"] = S["A"] @ S["u"] * 1e-3
+        return time.perf_counter() - t0
+
+
+def oracle_sample_text(cfg, S, n, dt):
+    return (f"oracle scipy CSR SpMV (complex128, 1 of {os.cpu_count()} cores) of a {cfg.nx}x{cfg.ny}x{S['planes']} "
+            f"z-chunk (planes {S['z0']}..{S['z0'] + S['planes'] - 1}) of config {cfg.index}, {n} SpMVs in {dt:.2f}s "
+            f"(1 RHS); CSR assembly {S['t_assemble']:.1f}s outside the timed region")
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    cfg, freq, nodes = workload(args)
-    S = oracle_sample(cfg, freq, nodes, args.ref_iters)
+    cfg, freq = workload(args, 1)
+    S = oracle_chunk(cfg, freq, args.cpu_planes)
     for _ in range(args.warmup):
-        oracle_iters(S, args.ref_iters)
-    tot, its = 0.0, 0
+        oracle_spmv(S, 1)
+    per = []
     for _ in range(args.steps):
-        dt, it = oracle_iters(S, args.ref_iters)
-        tot += dt
-        its += it
-    value = S["npts"] * 2 * its / tot / 1e9
-    sample = (f"oracle scipy-CSR BiCGSTAB (complex128, 1 thread), {args.ref_iters} iterations (2 SpMV each) of "
-              f"RHS 0 per step on the full config-{cfg.index} grid; CSR assembly {S['t_assemble']:.1f}s and "
-              f"oracle table {S['t_table']:.1f}s done once outside the timed steps")
+        per.append(oracle_spmv(S, 1))
+    tot = sum(per)
+    value = S["npts"] * args.steps / tot / 1e9
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
-            "dtype": "c128", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, freq, len(nodes), args.dtype), "parallelism": "1 CPU core"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic",
+            "config": {"workload": f"config{cfg.index} {cfg.name} {cfg.nx}x{cfg.ny}x{cfg.nz} f={freq:g}Hz: "
+                                   f"27-point impedance apply (oracle CSR SpMV on a {args.cpu_planes}-plane z-chunk)",
+                       "parallelism": "1 CPU core"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": oracle_sample_text(cfg, S, args.steps, tot)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ------------------------------------------------------------------------------------------------
-def apply_large(args, hz, ctx, dev, stream, peak):
-    """Apply-only roofline on a large BASELINE config (default config 4, 801x801x187, c64, 1 RHS): the
-    hot kernel where HBM — not launch latency or the PML share of a small grid — bounds it.  CUDA events
-    on the launching stream around each apply, L2 flushed between applies, median of `reps`."""
-    import torch
-    cfg = synth.get_config(args.large_config)
-    freq = cfg.freqs[-1]
-    v = synth.velocity_slab(cfg, 0, cfg.nz, device=dev if cfg.index == 5 else None)
-    T = hz.hz_build_weight_table(*TABLE_ARGS)
-    C = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, torch.from_numpy(v).to(dev, torch.float32),
-                              freq, T, npml=cfg.npml, dtype=hz.HZ_C64)
-    del v
-    u = C.alloc_field(1)
-    u.real.uniform_(-1, 1)
-    u.imag.uniform_(-1, 1)
-    au = C.alloc_field(1)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-
-    def time_apply(Cx, reps=10):
-        for _ in range(3):
-            hz.hz_apply_impedance(Cx, u, au, stream=stream)
-        out = []
-        nonlocal_l0[0] = hz.hz_kernel_launch_count()
-        for _ in range(reps):
-            flush.fill_(1)
-            torch.cuda.synchronize(dev)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            hz.hz_apply_impedance(Cx, u, au, stream=stream)
-            e1.record(stream)
-            torch.cuda.synchronize(dev)
-            out.append(e0.elapsed_time(e1))
-        return out
-
-    nonlocal_l0 = [0]
-    ts = time_apply(C)
-    l0 = nonlocal_l0[0]
-    launches = hz.hz_kernel_launch_count() - l0
-    ms = statistics.median(ts)
-    npts = cfg.nx * cfg.ny * cfg.nz
-    # the same apply with non-adaptive weights (a one-row table: the same weights at every point, like the
-    # paper's G4 / Gm comparison stencils, P:167-170, P:273) — the adaptive lookup costs no bytes and
-    # little time (P:52, P:446 "no overhead")
-    v = synth.velocity_slab(cfg, 0, cfg.nz, device=dev if cfg.index == 5 else None)
-    Tm = hz.hz_table_import(12.0, 0.1, T.rows5()[80][None])   # the GA row at G = 12, everywhere
-    Cm = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, torch.from_numpy(v).to(dev, torch.float32),
-                               freq, Tm, npml=cfg.npml, dtype=hz.HZ_C64)
-    del v
-    ms_m = statistics.median(time_apply(Cm))
-    del Cm
-    # the GAm rule (27-node mean weights stored once, +20 B/pt read per apply; P:273, reading A19)
-    v = synth.velocity_slab(cfg, 0, cfg.nz, device=dev if cfg.index == 5 else None)
-    Cg = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, torch.from_numpy(v).to(dev, torch.float32),
-                               freq, T, npml=cfg.npml, dtype=hz.HZ_C64, rule=hz.HZ_RULE_GAM)
-    del v
-    ms_g = statistics.median(time_apply(Cg))
-    del Cg
-    # GA in record mode (per-point weights stored once, +20 B/pt read per apply; SURVEY §8(a) a5)
-    v = synth.velocity_slab(cfg, 0, cfg.nz, device=dev if cfg.index == 5 else None)
-    Cr = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, torch.from_numpy(v).to(dev, torch.float32),
-                               freq, T, npml=cfg.npml, dtype=hz.HZ_C64, rule=hz.HZ_RULE_GA_RECORD)
-    del v
-    ms_r = statistics.median(time_apply(Cr))
-    del Cr
-    byts = npts * (4 + 16)            # w in, u in, Au out (complex64, 1 RHS): DESIGN.md §5
-    achieved = byts / (ms * 1e-3) / 1e9
-    return {"workload": f"config{cfg.index} {cfg.name} {cfg.nx}x{cfg.ny}x{cfg.nz} f={freq:g}Hz c64 nrhs=1, "
-                        "hz_apply_impedance only", "gpts_s": npts / (ms * 1e-3) / 1e9, "ms": ms,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "algorithmic_bytes_per_launch": byts},
-            "gpu_launches": launches, "l2": "flushed before every apply (256 MiB write)",
-            "fixed_weights": {"table": "one row (GA weights at G = 12) at every point",
-                              "gpts_s": npts / (ms_m * 1e-3) / 1e9, "ms": ms_m, "adaptive_over_fixed_time": ms / ms_m},
-            "record_mode": {"gpts_s": npts / (ms_r * 1e-3) / 1e9, "ms": ms_r,
-                            "hbm_frac": npts * (4 + 16 + 20) / (ms_r * 1e-3) / 1e9 / peak,
-                            "note": "GA weights stored per point, read by the apply (+20 B/pt)"},
-            "gam_rule": {"gpts_s": npts / (ms_g * 1e-3) / 1e9, "ms": ms_g,
-                         "hbm_frac": npts * (4 + 16 + 20) / (ms_g * 1e-3) / 1e9 / peak,
-                         "note": "27-node mean weights read per point (+20 B/pt)"}}
-
-
 def run_hz(args):
     import torch
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
-    if ws != args.gpus:
-        args.gpus = ws
+    args.gpus = ws
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
@@ -331,106 +236,124 @@ def run_hz(args):
     from paper_2108_08730_b200 import hz, parallel
 
     ctx = parallel.make_context(local)      # NCCL communicator over all ranks (uid via torch.distributed)
-
-    cfg, freq, nodes = workload(args)
-    nrhs = len(nodes)
+    cfg, freq = workload(args, ws)
+    nrhs = 1 if args.weak else args.nrhs
     z0, nzl = parallel.slab_partition(cfg.nz, ws, rank)
-    rd = torch.float32 if args.dtype == "c64" else torch.float64
-    dt_code = hz.HZ_C64 if args.dtype == "c64" else hz.HZ_C128
     v_np = synth.velocity_slab(cfg, z0, nzl, device=dev if cfg.index == 5 else None)
-    v_dev = torch.from_numpy(v_np).to(dev, rd).contiguous()
-    v_host = torch.from_numpy(v_np).to(rd).contiguous().pin_memory()
-    fshape = (nrhs, nzl + 2, cfg.ny, cfg.nx)
-    cdt = torch.complex64 if args.dtype == "c64" else torch.complex128
-    b = torch.zeros(fshape, dtype=cdt, device=dev)
-    x = torch.zeros(fshape, dtype=cdt, device=dev)
-    x_host = torch.zeros(fshape, dtype=cdt).pin_memory()
+    v_dev = torch.from_numpy(v_np).to(dev, torch.float32).contiguous()
+    del v_np
+    T = hz.hz_build_weight_table(*TABLE_ARGS)
+    C = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, v_dev, freq, T, npml=cfg.npml, z0=z0,
+                              nz_local=nzl, dtype=hz.HZ_C64)
+    u = C.alloc_field(nrhs)
+    u.real.uniform_(-1, 1)
+    u.imag.uniform_(-1, 1)
+    au = C.alloc_field(nrhs)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    peak, peak_src = read_peak()
 
     def barrier():
         if ws > 1:
             dist.barrier()
 
-    def one_step(v_in, x_out, ell=None):
-        T = hz.hz_build_weight_table(*TABLE_ARGS)                                  # a1
-        C = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, v_in, freq, T, npml=cfg.npml,
-                                  z0=z0, nz_local=nzl, dtype=dt_code)               # a2–a5
-        hz.hz_point_sources(C, nodes, b, stream=stream)                             # a8
-        if x_out.is_cuda:
-            x_out.zero_()
-        else:
-            x_out.zero_()
-        st, rel, its, stt = hz.hz_solve(C, b, x_out, rtol=args.rtol, max_iter=args.max_iter,
-                                        replace_every=args.replace_every, timing=True,
-                                        ell=args.ell if ell is None else ell,
-                                        stall_window=args.stall_window,
-                                        stream=stream)                              # a6, a7
-        return st, rel, its, stt
-
-    def timed(v_in, x_out, k, ell=None):
-        tot_ms, stats, last = 0.0, [], None
+    def time_applies(Cx, uu, aa, k, warm):
+        for _ in range(warm):
+            hz.hz_apply_impedance(Cx, uu, aa, stream=stream)
+        torch.cuda.synchronize(dev)
+        out = []
         l0 = hz.hz_kernel_launch_count()
         for _ in range(k):
             flush.fill_(1)
             torch.cuda.synchronize(dev)
             barrier()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            last = one_step(v_in, x_out, ell)
+            hz.hz_apply_impedance(Cx, uu, aa, stream=stream)
             e1.record(stream)
             torch.cuda.synchronize(dev)
             barrier()
-            tot_ms += e0.elapsed_time(e1)
-            stats.append(last[3])
-        return tot_ms, stats, last, hz.hz_kernel_launch_count() - l0
+            out.append(e0.elapsed_time(e1))
+        return out, hz.hz_kernel_launch_count() - l0
 
-    # ---------------- device-resident arm ----------------
-    for _ in range(args.warmup):
-        one_step(v_dev, x)
+    # ---------------- headline: device-resident batched apply ----------------
     torch.cuda.synchronize(dev)
     clocks = ClockSampler(local)
     clocks.start()
-    tot_ms, stats, last, launches = timed(v_dev, x, args.steps)
+    ts, launches = time_applies(C, u, au, args.steps, args.warmup)
     clk = clocks.stop()
-    st, rel, its, _ = last
+    (tot_max,) = parallel.rank_max([sum(ts)], dev)
+    npts = cfg.nx * cfg.ny * cfg.nz
+    ms_per_step = tot_max / args.steps
+    value = npts * nrhs / (ms_per_step * 1e-3) / 1e9
+    # dominant kernel = the apply launch itself: rank-0 launch durations (CUDA events on its stream)
+    ms_launch = statistics.median(ts)
+    pts_local = cfg.nx * cfg.ny * nzl
+    byts = pts_local * (4 + 16 * nrhs)
+    achieved = byts / (ms_launch * 1e-3) / 1e9
+    wkey = f"config{cfg.index}_c64_nrhs{nrhs}_apply_{cfg.nx}x{cfg.ny}x{nzl}"
+    traffic = read_traffic(wkey) if ws == 1 else None
 
-    pts = sum(s["apply_points_total"] for s in stats)
-    abytes = sum(s["apply_bytes_total"] for s in stats)
-    ams = sum(s["apply_ms_total"] for s in stats)
-    alaunch = sum(s["apply_launches"] for s in stats)
-    (tmax,) = parallel.rank_max([tot_ms], dev)              # the job takes as long as its slowest rank
-    pts_all, bytes_all = parallel.rank_sum([pts, abytes], dev)
-    (ams_max,) = parallel.rank_max([ams], dev)
-    ms_per_step = tmax / args.steps
-    value = pts_all / (tmax * 1e-3) / 1e9
-
-    # ---------------- end-to-end arm (host buffers through the C ABI) ----------------
+    # ---------------- e2e: host (pinned) buffers through the C ABI ----------------
     e2e = None
     if not args.no_e2e:
-        for _ in range(max(1, args.warmup)):
-            one_step(v_host, x_host)
-        tot_e, stats_e, _, _ = timed(v_host, x_host, args.steps)
-        pts_e = sum(s["apply_points_total"] for s in stats_e)
-        (tmax_e,) = parallel.rank_max([tot_e], dev)
-        (pts_e_all,) = parallel.rank_sum([pts_e], dev)
-        h2d = v_host.numel() * v_host.element_size() + x_host.numel() * x_host.element_size() + nodes.nbytes
-        d2h = x_host.numel() * x_host.element_size()
-        e2e = {"value": pts_e_all / (tmax_e * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d) * ws,
-               "d2h_bytes_per_step": int(d2h) * ws, "ms_per_step": tmax_e / args.steps}
+        uh = C.alloc_field(nrhs, device="cpu", pin_memory=True)
+        uh.copy_(u.cpu())
+        ah = C.alloc_field(nrhs, device="cpu", pin_memory=True)
+        te, _ = time_applies(C, uh, ah, max(2, min(args.steps, 4)), 1)
+        (te_max,) = parallel.rank_max([sum(te)], dev)
+        ke = max(2, min(args.steps, 4))
+        fb = (nzl + 2) * cfg.ny * C.ldx * 8 * nrhs
+        e2e = {"value": npts * nrhs / (te_max / ke * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(fb) * ws,
+               "d2h_bytes_per_step": int(fb) * ws, "ms_per_step": te_max / ke, "steps": ke,
+               "path": "hz_apply_impedance with pinned host u / Au: the library stages them through device buffers"}
+        del uh, ah
 
-    # ---------------- the other Krylov method on the same step (time to solution beside it) ----------------
-    alt = None
-    if not args.no_alt and ws == 1:
-        ell_alt = 3 - args.ell
-        one_step(v_dev, x, ell_alt)
-        tot_a, _, last_a, _ = timed(v_dev, x, min(args.steps, 3), ell_alt)
-        (tmax_a,) = parallel.rank_max([tot_a], dev)
-        ka = min(args.steps, 3)
-        alt = {"solver": "BiCGSTAB" if ell_alt == 1 else "BiCGStab(2)", "ms_per_step": tmax_a / ka,
-               "solve_s_per_rhs": tmax_a / ka * 1e-3 / nrhs, "iterations": int(last_a[3]["iterations"]),
-               "relres_max": float(np.max(last_a[1])), "status": int(last_a[0]), "steps": ka}
+    # ---------------- the solve leg: table + assemble + sources + batched solve ----------------
+    solve = None
+    if not args.no_solve:
+        snodes = synth.source_nodes(cfg)
+        sn = np.resize(snodes, (min(args.solve_nrhs, len(snodes)) if not args.weak else 1, 3))
+        b = None
+        solve = {"nrhs": int(len(sn)), "rtol": args.rtol, "max_iter": args.solve_max_iter}
+        for ell, name in ((1, "bicgstab"), (2, "bicgstab2")):
+            if args.weak and ell == 2:
+                break
+            torch.cuda.synchronize(dev)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            Ts = hz.hz_build_weight_table(*TABLE_ARGS)                                       # a1
+            Cs = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, v_dev, freq, Ts, npml=cfg.npml,
+                                       z0=z0, nz_local=nzl, dtype=hz.HZ_C64)                 # a2-a5 setup
+            if b is None:
+                b = Cs.alloc_field(len(sn))
+                x = Cs.alloc_field(len(sn))
+            hz.hz_point_sources(Cs, sn, b, stream=stream)                                   # a8
+            x.zero_()
+            mi = 100 if args.weak else args.solve_max_iter
+            st, rel, its, stt = hz.hz_solve(Cs, b, x, rtol=1e-30 if args.weak else args.rtol, max_iter=mi,
+                                            ell=ell, timing=True, stall_window=-1 if args.weak else 0,
+                                            stream=stream)                                  # a6, a7
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+            (tmax,) = parallel.rank_max([e0.elapsed_time(e1)], dev)
+            it = int(stt["iterations"])
+            solve[name] = {"solver": "BiCGSTAB" if ell == 1 else "BiCGStab(2)", "status": hz.STATUS_NAMES.get(st, st),
+                           "converged": bool(st == hz.HZ_OK), "iterations": it, "relres_max": float(np.max(rel)),
+                           "s": tmax * 1e-3, "s_per_rhs": tmax * 1e-3 / len(sn),
+                           "ms_per_iteration": tmax / max(1, it),
+                           "apply_ms_share": stt["apply_ms_total"] / tmax if tmax > 0 else None,
+                           "stagnated": int(stt["stagnated"])}
+            del Cs
+        if args.weak:
+            solve["note"] = "100 BiCGSTAB iterations (rtol 0): t_iter for the weak-scaling efficiency"
+
+    # ---------------- extra measurements (N = 1) ----------------
+    extra = {}
+    if ws == 1 and not args.no_extra and not args.weak:
+        extra = extras(args, hz, ctx, cfg, freq, v_dev, T, C, u, au, time_applies, peak)
 
     if rank != 0:
         if ws > 1:
@@ -438,52 +361,101 @@ def run_hz(args):
             dist.destroy_process_group()
         return 0
 
-    peak, peak_src = read_peak()
-    achieved = abytes / (ams * 1e-3) / 1e9 if ams > 0 else None
-    wkey = f"config{cfg.index}_{args.dtype}_nrhs{nrhs}_f{freq:g}"
-    traffic = read_traffic(wkey)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": args.dtype,
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "c64",
         "data": "synthetic",
-        "config": {"workload": workload_name(cfg, freq, nrhs, args.dtype), "grid": [cfg.nx, cfg.ny, cfg.nz],
-                   "nrhs": nrhs, "rtol": args.rtol, "parallelism": f"z-slab x{ws}",
-                   "solver": "BiCGSTAB" if args.ell == 1 else "BiCGStab(2)",
-                   "l2": "flushed before every step (256 MiB write); step working set > L2"},
-        "solve_s_per_rhs": ms_per_step * 1e-3 / nrhs,
-        "solver_alt": alt,
-        "iterations": int(stats[-1]["iterations"]),
-        "relres_max": float(np.max(rel)),
-        "status": int(st),
-        "apply_kernel_gpts_s": pts_all / (ams_max * 1e-3) / 1e9 if ams_max > 0 else None,
-        "apply_share_of_step": ams / tot_ms if tot_ms > 0 else None,
-        "roofline": {"bound": "hbm", "kernel": "apply27_cp (RHS-fused coefficient build + 27-point apply + BiCGSTAB dot epilogues, a2-a6)",
+        "config": {"workload": (f"config{cfg.index} {cfg.name} {cfg.nx}x{cfg.ny}x{cfg.nz} h={cfg.h:g}m f={freq:g}Hz "
+                                f"npml={cfg.npml} c64: hz_apply_impedance of {nrhs} field(s) (fused coefficient build "
+                                f"+ 27-point apply, a2-a6)" + (" — weak-scaling slab series 1201x1201x(50N+1)"
+                                                              if args.weak else "")),
+                   "grid": [cfg.nx, cfg.ny, cfg.nz], "nrhs": nrhs, "parallelism": f"z-slab x{ws}",
+                   "l2": "flushed before every step (256 MiB write); the step's working set exceeds L2"},
+        "roofline": {"bound": "hbm", "kernel": "apply27_tm (tensor-map TMA tiles: coefficient build + 27-point apply, a2-a6)",
                      "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None,
-                     "traffic": (traffic if traffic is not None else None),
-                     "algorithmic_bytes_per_launch": abytes / alaunch if alaunch else None,
-                     "avg_launch_ms": ams / alaunch if alaunch else None},
+                     "frac": achieved / peak, "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                     "traffic_source": traffic["source"] if traffic else None,
+                     "algorithmic_bytes_per_launch": byts, "bytes_per_point": 4 + 16 * nrhs,
+                     "launch_ms_median": ms_launch},
         "clocks": clk,
         "gpu_launches": int(launches),
         "e2e": e2e,
+        "solve": solve,
     }
-    if ws == 1 and not args.no_large:
-        line["apply_large"] = apply_large(args, hz, ctx, dev, stream, peak)
+    if solve and "bicgstab" in solve:
+        line["solve_s_per_rhs"] = solve["bicgstab"]["s_per_rhs"]
+    line.update(extra)
     if ws == 1 and not args.no_cpu_baseline:
-        S = oracle_sample(cfg, freq, nodes, args.cpu_iters)
-        dt, it = oracle_iters(S, args.cpu_iters)
-        cv = S["npts"] * 2 * it / dt / 1e9
-        line["cpu_baseline"] = {
-            "value": cv, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": (f"oracle scipy-CSR BiCGSTAB (complex128, 1 of {os.cpu_count()} cores), {it} iterations "
-                       f"(2 SpMV each) of RHS 0 on the full config-{cfg.index} grid in {dt:.1f}s; CSR assembly "
-                       f"{S['t_assemble']:.1f}s excluded")}
+        S = oracle_chunk(cfg, freq, args.cpu_planes)
+        dt = oracle_spmv(S, args.cpu_spmv)
+        line["cpu_baseline"] = {"value": S["npts"] * args.cpu_spmv / dt / 1e9, "unit": UNIT, "cores": 1,
+                                "kind": "oracle", "sample": oracle_sample_text(cfg, S, args.cpu_spmv, dt)}
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def extras(args, hz, ctx, cfg, freq, v_dev, T, C, u, au, time_applies, peak):
+    """N = 1 extra measurements beside the headline: the 1-RHS apply, non-adaptive weights, the GA
+    record mode and the GAm rule on the same model, and the config-2 solve step."""
+    import torch
+    npts = cfg.nx * cfg.ny * cfg.nz
+    out = {}
+    u1, a1 = u[:1], au[:1]
+
+    def one(Cx, label, extra_bytes=0):
+        ts, _ = time_applies(Cx, u1, a1, 5, 2)
+        ms = statistics.median(ts)
+        byts = npts * (4 + 16 + extra_bytes)
+        return {"gpts_s": npts / (ms * 1e-3) / 1e9, "ms": ms, "hbm_frac": byts / (ms * 1e-3) / 1e9 / peak,
+                "note": label}
+
+    out["apply_nrhs1"] = one(C, "the same apply, 1 RHS (20 B/pt)")
+    Tm = hz.hz_table_import(12.0, 0.1, T.rows5()[80][None])    # the GA row at G = 12 everywhere
+    Cm = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, v_dev, freq, Tm, npml=cfg.npml, dtype=hz.HZ_C64)
+    out["fixed_weights"] = one(Cm, "non-adaptive weights (one-row table: GA at G = 12 everywhere, like the "
+                                   "paper's G4/Gm stencils, P:167-170): the adaptive lookup's cost (P:52, P:446)")
+    out["fixed_weights"]["adaptive_over_fixed_time"] = out["apply_nrhs1"]["ms"] / out["fixed_weights"]["ms"]
+    del Cm
+    Cr = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, v_dev, freq, T, npml=cfg.npml, dtype=hz.HZ_C64,
+                               rule=hz.HZ_RULE_GA_RECORD)
+    out["record_mode"] = one(Cr, "GA weights stored per point and read by the apply (+20 B/pt)", 20)
+    del Cr
+    Cg = hz.hz_assemble_coeffs(ctx, cfg.nx, cfg.ny, cfg.nz, cfg.h, v_dev, freq, T, npml=cfg.npml, dtype=hz.HZ_C64,
+                               rule=hz.HZ_RULE_GAM)
+    out["gam_rule"] = one(Cg, "GAm: 27-node mean weights read per point (+20 B/pt)", 20)
+    del Cg
+    torch.cuda.empty_cache()
+    # config 2 (BASELINE configs[1]): the whole step table + assemble + sources + solve, 4 RHS
+    c2 = synth.get_config(2)
+    v2 = torch.from_numpy(synth.velocity_model(c2)).cuda().float()
+    nodes = synth.source_nodes(c2)
+    res = {}
+    for ell, name in ((1, "bicgstab"), (2, "bicgstab2")):
+        tms = []
+        for rep in range(3):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            T2 = hz.hz_build_weight_table(*TABLE_ARGS)
+            C2 = hz.hz_assemble_coeffs(ctx, c2.nx, c2.ny, c2.nz, c2.h, v2, c2.freq, T2, npml=c2.npml, dtype=hz.HZ_C64)
+            b = C2.alloc_field(len(nodes))
+            x = C2.alloc_field(len(nodes))
+            hz.hz_point_sources(C2, nodes, b)
+            st, rel, its, stt = hz.hz_solve(C2, b, x, rtol=args.rtol, ell=ell)
+            e1.record()
+            torch.cuda.synchronize()
+            if rep > 0:
+                tms.append(e0.elapsed_time(e1))
+        res[name] = {"ms_per_step": statistics.median(tms), "s_per_rhs": statistics.median(tms) * 1e-3 / len(nodes),
+                     "iterations": int(stt["iterations"]), "relres_max": float(np.max(rel)),
+                     "status": hz.STATUS_NAMES.get(st, st)}
+    out["config2_solve"] = {"workload": "config2 gradient 101^3 5 Hz c64, 4 RHS: table + assemble + sources + solve "
+                                        "(rtol 1e-6), warm", **res}
+    return out
 
 
 def main():

@@ -16,9 +16,13 @@
  *   - Grids are C-ordered [z][y][x] (x fastest).  A rank owns the z-slab [z0, z0+nz_local) of a
  *     global nx*ny*nz_global grid whose dimensions INCLUDE the PML pad (A18).
  *   - Complex fields are interleaved (re, im): complex64 = 2 x float, complex128 = 2 x double.
- *     Field buffers have one halo plane at each end: [nrhs][nz_local+2][ny][nx]; local plane k
- *     lives at index k+1.  The halo planes are owned by the library during a call (see each
- *     function); the caller allocates them.
+ *     Field buffers have one halo plane at each end and a padded row pitch:
+ *     [nrhs][nz_local+2][ny][ldx] with ldx = hz_field_ldx(nx) = nx rounded up to a multiple of 4
+ *     (32-byte rows for complex64: the apply moves its plane tiles with tensor-map TMA copies, which
+ *     need 16-byte row strides, and every row starts on a DRAM sector).  Local plane k lives at index
+ *     k+1; column x < nx of row y at [y][x].  The halo planes are owned by the library during a call
+ *     (see each function); the caller allocates them.  Pad columns [nx, ldx) are never read as
+ *     field values; outputs of the apply (au) get zeros there, the solver leaves x's pads as given.
  *   - Real model arrays (velocity) are float for HZ_C64 and double for HZ_C128, [nz_local][ny][nx].
  *   - Pointers may be device or host memory: the library inspects each pointer
  *     (cudaPointerGetAttributes) and stages host buffers through device memory itself.  The
@@ -70,6 +74,8 @@ typedef struct hz_coeffs hz_coeffs;
 
 const char* hz_last_error(void);
 const char* hz_version(void);
+/* Row pitch (elements) of every field buffer for a grid nx wide: nx rounded up to a multiple of 4. */
+int hz_field_ldx(int nx);
 
 /* ---------------------------------------------------------------------------------------------
  * Context: one per rank (process).  nranks > 1 creates an NCCL communicator from `id` (obtained
@@ -78,6 +84,12 @@ const char* hz_version(void);
  * ------------------------------------------------------------------------------------------- */
 hz_status hz_get_unique_id(unsigned char id[128]);
 hz_status hz_ctx_create(int cuda_device, int nranks, int rank, const unsigned char* id, hz_ctx** out);
+/* Loopback group: nranks (1..16) contexts of ONE process on ONE device, out[0..nranks-1], one per z-slab
+ * rank.  Each rank's calls must come from its own host thread (the ranks meet in host barriers inside
+ * every collective call); halo planes move with one cudaMemcpyAsync per plane and dot products are
+ * summed over the ranks by a device kernel in rank order — the same call sites as the NCCL path.  For
+ * testing the multi-slab data path without several GPUs.  Destroy every context with hz_ctx_destroy. */
+hz_status hz_ctx_create_loopback(int cuda_device, int nranks, hz_ctx** out);
 void hz_ctx_destroy(hz_ctx* ctx);
 
 /* ---------------------------------------------------------------------------------------------
@@ -151,9 +163,10 @@ void hz_coeffs_destroy(hz_coeffs* c);
 
 /* ---------------------------------------------------------------------------------------------
  * (3) apply_impedance — Au = [M + S] u for nrhs fields, matrix-free, asynchronous on
- * `stream`.  u and au: [nrhs][nz_local+2][ny][nx] complex of the coeffs' dtype.  u's halo planes
+ * `stream`.  u and au: [nrhs][nz_local+2][ny][ldx] complex of the coeffs' dtype.  u's halo planes
  * are overwritten with the neighbouring ranks' boundary planes (nranks > 1); planes outside the
- * global grid are treated as zero (Dirichlet, A9) and never read.  au's halo planes are not written.
+ * global grid are treated as zero (Dirichlet, A9) and never read.  au's halo planes are not written;
+ * its pad columns are written as zeros (complex64) or left untouched (complex128).
  * Row n of the operator (interior class-sum form; PML rows add the stretched per-axis terms):
  *   (Au)_n = omega^2 sum_d mu_{|d|}(w_n) u_{n+d} / v_{n+d}^2                 (Eq. 8)
  *          + sum_a sum_e D_a(n_a, e) sum_{p,q} T(p,q; w_n) u_{n + e e_a + p e_b + q e_c}   (A6, A8)
@@ -162,9 +175,9 @@ hz_status hz_apply_impedance(const hz_coeffs* c, void* u, void* au, int nrhs, vo
 
 /* ---------------------------------------------------------------------------------------------
  * (4) solve — batched BiCGSTAB (or BiCGStab(2), opts.ell) for A x_r = b_r, r = 0..nrhs-1 (north
- * star (3)); blocking.  opts == NULL: the defaults below; zero-initialise the struct before setting
- * fields so that ell = 0 and stall_window = 0 select their defaults.
- * b, x: [nrhs][nz_local+2][ny][nx]; x holds the initial guess on entry (zeros OK) and the final
+ * star (3)); blocking.  opts == NULL or hz_solve_opts_default(): the defaults below; in a caller's
+ * struct every field left 0 selects its default (a zero-initialised struct is the default setting).
+ * b, x: [nrhs][nz_local+2][ny][ldx]; x holds the initial guess on entry (zeros OK) and the final
  * iterate on exit.  Each RHS iterates independently (per-RHS scalars on the device, fp64 dot
  * accumulation, residual replacement every replace_every iterations) and stops when its
  * recomputed TRUE residual ||b - A x|| / ||b|| <= rtol (A21).  relres_out[nrhs] receives the true
@@ -179,10 +192,10 @@ hz_status hz_apply_impedance(const hz_coeffs* c, void* u, void* au, int nrhs, vo
  * Returns HZ_OK, HZ_NOT_CONVERGED or HZ_BREAKDOWN (outputs valid), or an error.
  * ------------------------------------------------------------------------------------------- */
 typedef struct {
-  double rtol;       /* default 1e-6                                               */
-  int max_iter;      /* default 20000                                              */
-  int replace_every; /* residual replacement period, default 50                    */
-  int check_every;   /* host convergence poll period, default 10                   */
+  double rtol;       /* default 1e-6 (0 = default)                                 */
+  int max_iter;      /* default 20000 (0 = default)                                */
+  int replace_every; /* residual replacement period, default 50 (0 = default, < 0 = never) */
+  int check_every;   /* host convergence poll period, default 10 (0 = default)     */
   int timing;        /* 1 = time every operator-apply launch with CUDA events      */
   int ell;           /* Krylov method: 1 (or 0) = BiCGSTAB (default); 2 = BiCGStab(2)
                         (Sleijpen & Fokkema 1993: two BiCG steps then a 2-term minimal-
@@ -211,12 +224,17 @@ typedef struct {
                                (no 10% reduction in stall_window iterations)      */
 } hz_solve_stats;
 
+/* The default options: rtol 1e-6, max_iter 20000, replace_every 50, check_every 10, ell 1. */
+hz_solve_opts hz_solve_opts_default(void);
+/* A RHS whose BiCGSTAB breaks down (rho, omega or (r0^, v) ~ 0) is restarted from its recomputed true
+ * residual; one that breaks down more than max(50, stall_window/check_every + 1) times is retired on
+ * its own and the call returns HZ_BREAKDOWN (the other RHS continue). */
 hz_status hz_solve(const hz_coeffs* c, const void* b, void* x, int nrhs, const hz_solve_opts* opts,
                    double* relres_out, int* iters_out, hz_solve_stats* stats, void* stream);
 
 /* Point-source RHS (reading A15).  node_xyz: GLOBAL node indices [nsrc][3] (x, y, z);
  * amp_re_im: [nsrc][2] (NULL = unit amplitudes).  consistent = 1: b_n = amp mu_{|n-s|}(w_n)/h^3 on
- * the 27 nodes around s (row n's own weights); 0: nodal amp/h^3.  b: [nsrc][nz_local+2][ny][nx],
+ * the 27 nodes around s (row n's own weights); 0: nodal amp/h^3.  b: [nsrc][nz_local+2][ny][ldx],
  * zero-filled by the call, entries outside this rank's slab skipped.  HZ_ERR_SOURCE_IN_PML if a
  * source lies inside the PML. */
 hz_status hz_point_sources(const hz_coeffs* c, int nsrc, const long long* node_xyz,
@@ -225,7 +243,7 @@ hz_status hz_point_sources(const hz_coeffs* c, int nsrc, const long long* node_x
 /* ---------------------------------------------------------------------------------------------
  * Evaluation (not on the hot path)
  * hz_eqerror: the paper's accuracy metric (Eq. eqerror; reading A20) between two
- * wavefields of this rank's slab, [nz_local+2][ny][nx] complex of the coeffs' dtype (host or device;
+ * wavefields of this rank's slab, [nz_local+2][ny][ldx] complex of the coeffs' dtype (host or device;
  * the owned planes are read):
  *   err = sum W |Re(u_ref - u)| / sum W |Re u_ref|  +  sum W |Im(u_ref - u)| / sum W |Im u_ref|
  * with W = h * distance to the source node src_xyz (global x, y, z), over the nodes at least

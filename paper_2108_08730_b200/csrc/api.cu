@@ -1,11 +1,14 @@
 // libhz C ABI (include/hz.h): contexts, tables, coefficient assembly, apply, batched BiCGSTAB,
 // point sources; z-slab halo exchange and dot-product allreduce over NCCL for nranks > 1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <atomic>
 #include <climits>
+#include <condition_variable>
 #include <map>
 #include <mutex>
 #include <cmath>
@@ -100,21 +103,26 @@ bool is_device_ptr(const void* p) {
 // Caching device allocator: blocks released by DBuf go to a free list and are reused by later
 // requests of a similar size (assemble/solve per step would otherwise cudaMalloc/cudaFree ~8 fields
 // per call, and cudaFree synchronises the device).  hz_trim_memory() returns the cache to CUDA.
+// Blocks are keyed by (device, size): a block is only handed to a request on the device it was
+// allocated on (the current device at the request, which every entry point sets from its context).
 struct BlockCache {
   std::mutex m;
-  std::multimap<size_t, void*> free;   // size -> block
-  std::map<void*, size_t> size_of;
+  std::multimap<std::pair<int, size_t>, void*> free;   // (device, size) -> block
+  std::map<void*, std::pair<int, size_t>> info;          // block -> (device, size)
   cudaError_t acquire(size_t bytes, void** out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
     {
       std::lock_guard<std::mutex> g(m);
-      auto it = free.lower_bound(bytes);
-      if (it != free.end() && it->first <= 2 * bytes + (1u << 20)) {
+      auto it = free.lower_bound({dev, bytes});
+      if (it != free.end() && it->first.first == dev && it->first.second <= 2 * bytes + (1u << 20)) {
         *out = it->second;
         free.erase(it);
         return cudaSuccess;
       }
     }
-    cudaError_t e = cudaMalloc(out, bytes);
+    e = cudaMalloc(out, bytes);
     if (e == cudaErrorMemoryAllocation) {   // give the cache back and retry once
       cudaGetLastError();
       trim();
@@ -122,23 +130,27 @@ struct BlockCache {
     }
     if (e == cudaSuccess) {
       std::lock_guard<std::mutex> g(m);
-      size_of[*out] = bytes;
+      info[*out] = {dev, bytes};
     }
     return e;
   }
   void release(void* p) {
     std::lock_guard<std::mutex> g(m);
-    auto it = size_of.find(p);
-    if (it == size_of.end()) return;
+    auto it = info.find(p);
+    if (it == info.end()) return;
     free.emplace(it->second, p);
   }
   void trim() {
     std::lock_guard<std::mutex> g(m);
+    int cur = 0;
+    cudaGetDevice(&cur);
     for (auto& kv : free) {
+      cudaSetDevice(kv.first.first);
       cudaFree(kv.second);
-      size_of.erase(kv.second);
+      info.erase(kv.second);
     }
     free.clear();
+    cudaSetDevice(cur);
   }
 };
 BlockCache& cache() {
@@ -167,9 +179,38 @@ struct DBuf {
 // ---------------------------------------------------------------------------------------------
 // objects
 // ---------------------------------------------------------------------------------------------
+// Loopback communicator: P ranks of one process on one device (one host thread per rank), moving halo
+// planes with one cudaMemcpyAsync per plane and summing the dots with a device kernel, behind the same
+// call sites as NCCL.  Host barriers order the ranks' calls; GPU-side ordering goes through CUDA events
+// (no kernel ever waits on another rank's kernel).
+struct LoopGroup {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<void*> ptr;            // per rank: the buffer / field published for the current op
+  std::vector<long long> nzl, fstride;
+  std::vector<cudaEvent_t> ev, ev2;  // per rank: "published data ready", "done reading the others"
+  std::vector<DBuf> tmp;             // per rank: reduction output before it overwrites the rank's buffer
+  int refs = 0;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      gen++;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
 struct hz_ctx {
   int device = 0, nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
+  LoopGroup* loop = nullptr;   // loopback group (nranks > 1 without NCCL)
 };
 
 struct hz_table {
@@ -178,7 +219,7 @@ struct hz_table {
 
 struct SolverWork {
   int nrhs = 0;
-  DBuf rhat, p, v, t, r;        // fields [nrhs][nzl+2][ny][nx]
+  DBuf rhat, p, v, t, r;        // fields [nrhs][nzl+2][ny][ldx]
   DBuf r1, r2;                  // BiCGStab(2) only
   DBuf xlo;                     // compensation term of the c64 iterate (double-float x)
   DBuf dotA, dotB, dotR, dotN, dotG;  // fp64 dot buffers
@@ -191,17 +232,18 @@ struct hz_coeffs {
   hz_ctx* ctx = nullptr;
   hz_dtype dtype = HZ_C64;
   hz_grid grid{};
+  int ldx = 0;                 // row pitch of fields and model arrays (nx rounded up to 4)
   hz_mass mass = HZ_MASS_EQ8;
   hz_rule rule = HZ_RULE_GA;
-  DBuf gam;                    // GAm: [5][nzl+2][ny][nx] 27-node mean weights (t1, t2, mu0, mu1, mu2)
+  DBuf gam;                    // GAm: [5][nzl+2][ny][ldx] 27-node mean weights (t1, t2, mu0, mu1, mu2)
   double freq = 0, omega = 0, h = 0;
   double v_pml = 0;
   hz_pml pml{};
   Table table;                 // host copy actually used (rank 0's on all ranks)
   int n_g_dev = 0;             // rows uploaded (>= 2)
   double g_min = 0, g_max = 0, dg = 0;
-  DBuf v;                      // [nzl+2][ny][nx] R
-  DBuf w;                      // [nzl+2][ny][nx] R: 1/v² (the apply's model input)
+  DBuf v;                      // [nzl+2][ny][ldx] R
+  DBuf w;                      // [nzl+2][ny][ldx] R: 1/v² (the apply's model input)
   DBuf tab_f, tab_d;           // [n_g_dev][TAB_STRIDE] float / double rows (float only for C64)
   DBuf ctab_f, ctab_d;         // [n_g_dev][CTAB_STRIDE] pre-scaled class coefficients (apply)
   DBuf pml_f[6], pml_d[6];     // dm x,y,z ; dp x,y,z (complex float / complex double)
@@ -210,24 +252,28 @@ struct hz_coeffs {
   std::vector<std::complex<double>> am_h[3], ap_h[3];  // host copies for export
   DBuf partials, tickets;      // apply epilogue scratch
   int zc = 1, nchunks = 1;
-  // complex64 RHS-fused apply: per (RHS groups, RHS per CTA) a work list of cp_items (x/y-PML tiles
-  // first), built on first use
-  struct CpPlan {
+  // complex64 tensor-map apply (apply27_tm): tile geometry, the map of w, cached maps of the fields
+  // applied so far (keyed by pointer and RHS count), and per (RHS groups, RHS per CTA) a work list
+  int tm_tx = 0, tm_ty = 0, tm_org = 0, tm_nval = 0;
+  CUtensorMap tmap_w;
+  std::map<std::pair<const void*, int>, CUtensorMap> tmap_u;
+  struct TmPlan {
     DBuf work;
-    int n_xy = 0, n_in = 0;
+    int n_items = 0;
   };
-  bool cp_on = false;
-  std::map<int, std::unique_ptr<CpPlan>> cp_plans;
+  std::map<int, std::unique_ptr<TmPlan>> tm_plans;
   std::unique_ptr<SolverWork> work;
   size_t esz() const { return dtype == HZ_C64 ? 4 : 8; }   // real element size
-  long long plane() const { return (long long)grid.nx * grid.ny; }
+  long long plane() const { return (long long)ldx * grid.ny; }
   long long fstride() const { return (long long)(grid.nz_local + 2) * plane(); }
+  long long npoints() const { return (long long)grid.nx * grid.ny * grid.nz_local; }   // owned points
 };
 
 extern "C" {
 
 const char* hz_last_error(void) { return g_err.c_str(); }
-const char* hz_version(void) { return "libhz 0.1 (sm_100a)"; }
+const char* hz_version(void) { return "libhz 0.2 (sm_100a)"; }
+int hz_field_ldx(int nx) { return nx < 1 ? 0 : (nx + 3) & ~3; }
 long long hz_kernel_launch_count(void) { return g_launches.load(); }
 void hz_trim_memory(void) { cache().trim(); }
 
@@ -262,9 +308,53 @@ hz_status hz_ctx_create(int cuda_device, int nranks, int rank, const unsigned ch
   return HZ_OK;
 }
 
+hz_status hz_ctx_create_loopback(int cuda_device, int nranks, hz_ctx** out) {
+  if (!out || nranks < 1 || nranks > LOOP_MAX_RANKS) { set_error("hz_ctx_create_loopback: bad arguments (1..16 ranks)"); return HZ_ERR_INVALID_ARG; }
+  int ndev = 0;
+  HZ_CUDA(cudaGetDeviceCount(&ndev));
+  if (cuda_device < 0 || cuda_device >= ndev) { set_error("hz_ctx_create_loopback: bad device"); return HZ_ERR_INVALID_ARG; }
+  HZ_CUDA(cudaSetDevice(cuda_device));
+  LoopGroup* g = new LoopGroup;
+  g->n = nranks;
+  g->ptr.assign(nranks, nullptr);
+  g->nzl.assign(nranks, 0);
+  g->fstride.assign(nranks, 0);
+  g->ev.resize(nranks);
+  g->ev2.resize(nranks);
+  g->tmp.resize(nranks);
+  for (int r = 0; r < nranks; r++) {
+    HZ_CUDA(cudaEventCreateWithFlags(&g->ev[r], cudaEventDisableTiming));
+    HZ_CUDA(cudaEventCreateWithFlags(&g->ev2[r], cudaEventDisableTiming));
+  }
+  g->refs = nranks;
+  for (int r = 0; r < nranks; r++) {
+    hz_ctx* c = new hz_ctx;
+    c->device = cuda_device;
+    c->nranks = nranks;
+    c->rank = r;
+    c->loop = nranks > 1 ? g : nullptr;
+    out[r] = c;
+  }
+  if (nranks == 1) delete g;
+  return HZ_OK;
+}
+
 void hz_ctx_destroy(hz_ctx* c) {
   if (!c) return;
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->loop) {
+    LoopGroup* g = c->loop;
+    bool last;
+    {
+      std::lock_guard<std::mutex> lk(g->m);
+      last = --g->refs == 0;
+    }
+    if (last) {
+      for (auto e : g->ev) cudaEventDestroy(e);
+      for (auto e : g->ev2) cudaEventDestroy(e);
+      delete g;
+    }
+  }
   delete c;
 }
 
@@ -357,6 +447,16 @@ void pml_axis(int n, int npml, double h, double omega, double v_pml, double R,
   }
 }
 
+// every entry point that launches work runs on its context's device
+hz_status set_device(const hz_ctx* ctx) {
+  if (cudaSetDevice(ctx->device) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("cudaSetDevice failed");
+    return HZ_ERR_CUDA;
+  }
+  return HZ_OK;
+}
+
 // R: arithmetic type, S: storage type (= the coeffs' dtype)
 template <typename R, typename S = R>
 ApplyParams<R, S> make_params(const hz_coeffs* c) {
@@ -365,6 +465,7 @@ ApplyParams<R, S> make_params(const hz_coeffs* c) {
   memset(&p, 0, sizeof(p));
   p.nx = c->grid.nx;
   p.ny = c->grid.ny;
+  p.ldx = c->ldx;
   p.nzl = c->grid.nz_local;
   p.z0 = c->grid.z0;
   p.nzg = c->grid.nz_global;
@@ -372,6 +473,9 @@ ApplyParams<R, S> make_params(const hz_coeffs* c) {
   p.fstride = c->fstride();
   p.zc = c->zc;
   p.nchunks = c->nchunks;
+  p.tm_tx = c->tm_tx;
+  p.tm_ty = c->tm_ty;
+  p.tm_org = c->tm_org;
   p.v = c->v.as<S>();
   p.w = c->w.as<S>();
   p.gam = c->rule != HZ_RULE_GA ? c->gam.as<S>() : nullptr;
@@ -398,13 +502,41 @@ ApplyParams<R, S> make_params(const hz_coeffs* c) {
   return p;
 }
 
-// Exchange the boundary planes of `field` ([nrhs][nzl+2][ny][nx] complex) with the z neighbours.
+// ---- communication: NCCL (one process per GPU) or the loopback group; no-ops for one rank ----
+// Exchange the boundary planes of `field` ([nrhs][nzl+2][ny][ldx] complex) with the z neighbours.
 hz_status halo_exchange(const hz_coeffs* c, void* field, int nrhs, size_t elem_bytes, cudaStream_t s) {
   const hz_ctx* ctx = c->ctx;
   if (ctx->nranks == 1) return HZ_OK;
   const size_t pb = (size_t)c->plane() * elem_bytes;
   const int nzl = c->grid.nz_local;
   char* base = reinterpret_cast<char*>(field);
+  if (ctx->loop) {
+    LoopGroup* g = ctx->loop;
+    const int r = ctx->rank;
+    g->ptr[r] = field;
+    g->nzl[r] = nzl;
+    g->fstride[r] = c->fstride();
+    HZ_CUDA(cudaEventRecord(g->ev[r], s));
+    g->barrier();
+    for (int q : {r - 1, r + 1})
+      if (q >= 0 && q < g->n) HZ_CUDA(cudaStreamWaitEvent(s, g->ev[q], 0));
+    for (int k = 0; k < nrhs; k++) {
+      char* f = base + (size_t)k * (size_t)c->fstride() * elem_bytes;
+      if (r > 0) {   // halo plane 0 ← the lower neighbour's last owned plane
+        const char* src = reinterpret_cast<const char*>(g->ptr[r - 1]) + (size_t)k * (size_t)g->fstride[r - 1] * elem_bytes;
+        HZ_CUDA(cudaMemcpyAsync(f, src + (size_t)g->nzl[r - 1] * pb, pb, cudaMemcpyDeviceToDevice, s));
+      }
+      if (r < g->n - 1) {   // halo plane nzl+1 ← the upper neighbour's first owned plane
+        const char* src = reinterpret_cast<const char*>(g->ptr[r + 1]) + (size_t)k * (size_t)g->fstride[r + 1] * elem_bytes;
+        HZ_CUDA(cudaMemcpyAsync(f + (size_t)(nzl + 1) * pb, src + pb, pb, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    HZ_CUDA(cudaEventRecord(g->ev2[r], s));
+    g->barrier();
+    for (int q : {r - 1, r + 1})   // the neighbours have read my boundary planes before I change them
+      if (q >= 0 && q < g->n) HZ_CUDA(cudaStreamWaitEvent(s, g->ev2[q], 0));
+    return HZ_OK;
+  }
   HZ_TRY(nccl_check(g_nccl.GroupStart(), "ncclGroupStart"));
   for (int r = 0; r < nrhs; r++) {
     char* f = base + (size_t)r * (size_t)c->fstride() * elem_bytes;
@@ -421,189 +553,262 @@ hz_status halo_exchange(const hz_coeffs* c, void* field, int nrhs, size_t elem_b
   return HZ_OK;
 }
 
-hz_status allreduce_sum(const hz_coeffs* c, double* buf, size_t n, cudaStream_t s) {
-  if (c->ctx->nranks == 1) return HZ_OK;
-  return nccl_check(g_nccl.AllReduce(buf, buf, n, ncclDouble, ncclSum, c->ctx->comm, s), "ncclAllReduce");
+// in-place allreduce of n doubles (op 0 = sum, 1 = max) over the ranks
+hz_status comm_allreduce(const hz_ctx* ctx, double* buf, size_t n, int op, cudaStream_t s) {
+  if (ctx->nranks == 1) return HZ_OK;
+  if (ctx->loop) {
+    LoopGroup* g = ctx->loop;
+    const int r = ctx->rank;
+    g->ptr[r] = buf;
+    HZ_CUDA(g->tmp[r].ensure(n * sizeof(double)));
+    HZ_CUDA(cudaEventRecord(g->ev[r], s));
+    g->barrier();
+    LoopPtrs lp;
+    for (int q = 0; q < g->n; q++) {
+      if (q != r) HZ_CUDA(cudaStreamWaitEvent(s, g->ev[q], 0));
+      lp.p[q] = reinterpret_cast<const double*>(g->ptr[q]);
+    }
+    HZ_CUDA(launch_loop_reduce(lp, g->n, g->tmp[r].as<double>(), (long long)n, op, s));
+    count_launch();
+    HZ_CUDA(cudaEventRecord(g->ev2[r], s));
+    g->barrier();
+    for (int q = 0; q < g->n; q++)   // every rank has read my buffer before it is overwritten
+      if (q != r) HZ_CUDA(cudaStreamWaitEvent(s, g->ev2[q], 0));
+    HZ_CUDA(cudaMemcpyAsync(buf, g->tmp[r].p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return HZ_OK;
+  }
+  return nccl_check(g_nccl.AllReduce(buf, buf, n, ncclDouble, op == 0 ? ncclSum : ncclMax, ctx->comm, s), "ncclAllReduce");
 }
 
-template <typename R, typename S>
-hz_status cp_attach(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs);
+hz_status allreduce_sum(const hz_coeffs* c, double* buf, size_t n, cudaStream_t s) {
+  return comm_allreduce(c->ctx, buf, n, 0, s);
+}
 
-template <typename R, typename S>
-hz_status apply_launch(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs, int epi, cudaStream_t s) {
-  const int K = epi_k(epi);
-  if (epi != EPI_RESID) HZ_TRY(cp_attach(c, p, nrhs));
-  if (K > 0) {
-    auto* cc = const_cast<hz_coeffs*>(c);
-    ApplyParams<R, S> pp = p;
-    const long long nb = apply_slots<R, S>(pp);
-    HZ_CUDA(cc->partials.ensure(sizeof(double) * (size_t)nb * K * nrhs));
-    if (cc->tickets.n < sizeof(unsigned) * (size_t)nrhs) {
-      HZ_CUDA(cc->tickets.ensure(sizeof(unsigned) * (size_t)nrhs));
-      HZ_CUDA(cudaMemsetAsync(cc->tickets.p, 0, cc->tickets.n, s));
+// broadcast n doubles of rank 0's buffer to every rank
+hz_status comm_bcast(const hz_ctx* ctx, double* buf, size_t n, cudaStream_t s) {
+  if (ctx->nranks == 1) return HZ_OK;
+  if (ctx->loop) {
+    LoopGroup* g = ctx->loop;
+    const int r = ctx->rank;
+    g->ptr[r] = buf;
+    HZ_CUDA(cudaEventRecord(g->ev[r], s));
+    g->barrier();
+    if (r != 0) {
+      HZ_CUDA(cudaStreamWaitEvent(s, g->ev[0], 0));
+      HZ_CUDA(cudaMemcpyAsync(buf, g->ptr[0], n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     }
-    p.partials = cc->partials.as<double>();
-    p.tickets = cc->tickets.as<unsigned>();
+    HZ_CUDA(cudaEventRecord(g->ev2[r], s));
+    g->barrier();
+    if (r == 0)
+      for (int q = 1; q < g->n; q++) HZ_CUDA(cudaStreamWaitEvent(s, g->ev2[q], 0));
+    return HZ_OK;
   }
-  HZ_CUDA(launch_apply<R, S>(p, nrhs, c->mass == HZ_MASS_COLLOC, epi, s));
-  count_launch(apply_last_launches());
+  return nccl_check(g_nccl.Broadcast(buf, buf, n, ncclDouble, 0, ctx->comm, s), "ncclBroadcast");
+}
+
+// ---------------------------------------------------------------------------------------------
+// complex64 tensor-map apply (apply27_tm): tile geometry, tensor maps, work lists
+// ---------------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+hz_status tm_encoder() {
+  if (g_encode) return HZ_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || fn == nullptr) {
+    cudaGetLastError();
+    set_error("cuTensorMapEncodeTiled is not available from the CUDA driver");
+    return HZ_ERR_CUDA;
+  }
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   return HZ_OK;
 }
 
-// Work lists of the complex64 RHS-fused apply (apply27_cp).  Each axis is cut into bands — the PML
-// slab below, the interior [lo, hi], the PML slab above — and each x/y band rectangle is tiled on its
-// own (tx ≤ 64, tx·ty ≤ 256·NY, (tx+2)(ty+2) ≤ CP_HALO, ty even; the last tile of a band overlaps
-// its neighbour and stores only its own points), so a tile is either wholly in the x/y-PML or wholly
-// outside it (its body then only carries the plane-uniform z-PML corrections).  Tiles march the
-// slab in z-chunks whose count balances the launch over whole waves of resident CTAs (SMs × CTAs/SM)
-// against the 2 extra halo planes a chunk reads (env HZ_CP_ZC forces a chunk length).
-struct CpBand { int a, b; bool pml; };
-static std::vector<CpBand> cp_bands(int n, int lo, int hi) {
-  std::vector<CpBand> v;
-  if (hi < lo) return {{0, n, true}};
-  if (lo > 0) v.push_back({0, lo, true});
-  v.push_back({lo, hi + 1, false});
-  if (hi + 1 < n) v.push_back({hi + 1, n, true});
-  return v;
+// Tile geometry: tile i computes the columns [i·tx − 1, (i+1)·tx − 1) (apply27_tm.cuh); ntx tiles of
+// tx ∈ {16, 32, 64} columns cover the pitched row (the pad columns too, which the apply writes as
+// zeros): the width with the fewest box columns ntx·(tx + 4) (halo included), the wider on a tie;
+// rows ty = 512/tx; the maps start at the slab's first in-grid storage plane (planes outside the
+// global grid read zeros).
+int tm_tile_width(int ldx) {
+  int best = TM_MAXTX, cost = INT_MAX;
+  for (int tx = TM_MAXTX; tx >= 16; tx /= 2) {
+    const int ntx = (ldx + 1 + tx - 1) / tx;
+    if (ntx * (tx + 4) < cost) { cost = ntx * (tx + 4); best = tx; }
+  }
+  return best;
 }
-struct CpTile { int x0, y0, tx, ty, xs, ys, xe, ye; };
-static void cp_tile_rect(int xa, int xb, int ya, int yb, int maxpts, std::vector<CpTile>& out) {
-  const int w = xb - xa, h = yb - ya;
-  const int ntx = (w + 63) / 64, tx = (w + ntx - 1) / ntx;
-  int tymax = std::min(64, maxpts / tx);
-  while (tymax > 2 && (tx + 2) * (tymax + 2) > CP_HALO) tymax--;
-  tymax = std::max(2, tymax & ~1);
-  int nty = (h + tymax - 1) / tymax;
-  int ty = (h + nty - 1) / nty;
-  ty = std::min(tymax, ty + (ty & 1));
-  if (ty > h && h >= 2) ty = h & ~1;   // stay inside the band (a 1-row band borrows a neighbour row)
-  nty = (h + ty - 1) / ty;
+void tm_geometry(hz_coeffs* c) {
+  const hz_grid& g = c->grid;
+  const int tx = tm_tile_width(c->ldx);
+  c->tm_tx = tx;
+  c->tm_ty = tm_rows(tx);
+  c->tm_org = g.z0 == 0 ? 1 : 0;
+  const int last = (g.z0 + g.nz_local == g.nz_global) ? g.nz_local : g.nz_local + 1;
+  c->tm_nval = last - c->tm_org + 1;
+}
+
+// 3-D (w: x, y, plane) or 4-D (u: x, y, plane, RHS) map of a pitched slab array; box = one halo tile
+hz_status tm_encode(const hz_coeffs* c, CUtensorMap* map, const void* base, size_t esz, int nrhs) {
+  HZ_TRY(tm_encoder());
+  const hz_grid& g = c->grid;
+  const char* org = reinterpret_cast<const char*>(base) + (size_t)c->tm_org * (size_t)c->plane() * esz;
+  const cuuint64_t dims[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)c->tm_nval, (cuuint64_t)nrhs};
+  const cuuint64_t strides[3] = {(cuuint64_t)c->ldx * esz, (cuuint64_t)c->plane() * esz, (cuuint64_t)c->fstride() * esz};
+  const cuuint32_t box[4] = {(cuuint32_t)(esz == 4 ? tm_bxw(c->tm_tx) : tm_bxu(c->tm_tx)), (cuuint32_t)(c->tm_ty + 2), 1u, 1u};
+  const cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  const int rank = esz == 4 ? 3 : 4;
+  CUresult r = g_encode(map, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank,
+                        const_cast<char*>(org), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return HZ_ERR_CUDA;
+  }
+  return HZ_OK;
+}
+
+const CUtensorMap* tm_umap(hz_coeffs* c, const void* u, int nrhs) {
+  const auto key = std::make_pair(u, nrhs);
+  auto it = c->tmap_u.find(key);
+  if (it != c->tmap_u.end()) return &it->second;
+  if (c->tmap_u.size() >= 32) c->tmap_u.clear();
+  CUtensorMap m;
+  if (tm_encode(c, &m, u, 8, nrhs) != HZ_OK) return nullptr;
+  return &(c->tmap_u[key] = m);
+}
+
+// Work list for ngroups RHS groups of nr RHS per CTA: each tile of the ntx × nty grid marches the
+// slab in z-chunks whose count balances the launch over whole waves of resident CTAs against the 2
+// halo planes a chunk re-reads; tiles with x/y-PML points run the x/y-PML body (cut into 1.5× more
+// chunks: they cost more per point), the others run the z-PML body on the chunks [0, zl) and
+// [zh, nzl) that touch the z-PML and the PML-free body in between.  x/y-PML items come first.
+void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], const int hi[3], int slots, int ngroups,
+                    std::vector<int4>& out) {
+  const int nzl = g.nz_local;
+  const int ntx = (ldx + 1 + tx - 1) / tx, nty = (g.ny + ty - 1) / ty;
+  std::vector<std::pair<int, int>> xy, in;
   for (int j = 0; j < nty; j++)
     for (int i = 0; i < ntx; i++) {
-      CpTile t;
-      t.xs = xa + i * tx;
-      t.xe = std::min(t.xs + tx, xb);
-      t.x0 = std::min(t.xs, xb - tx);
-      t.ys = ya + j * ty;
-      t.ye = std::min(t.ys + ty, yb);
-      t.y0 = std::max(0, std::min(t.ys, yb - ty));
-      t.tx = tx;
-      t.ty = ty;
-      out.push_back(t);
+      const int x0 = i * tx, y0 = j * ty;   // computes columns [x0 − 1, x0 + tx − 1)
+      const int xa = std::max(x0 - 1, 0), x1 = std::min(x0 + tx - 1, g.nx) - 1, y1 = std::min(y0 + ty, g.ny) - 1;
+      const bool pml = xa < lo[0] || x1 > hi[0] || y0 < lo[1] || y1 > hi[1] || hi[0] < lo[0] || hi[1] < lo[1];
+      (pml ? xy : in).push_back({x0, y0});
     }
-}
-
-hz_status cp_geometry(hz_coeffs* c) {
-  const hz_grid& g = c->grid;
-  if (g.nx > 65535 || g.ny > 65535 || g.nz_local > 65535) { c->cp_on = false; return HZ_OK; }   // item packing
-  c->cp_on = getenv("HZ_NO_CP") == nullptr;
-  return HZ_OK;
-}
-
-const hz_coeffs::CpPlan* cp_plan(hz_coeffs* c, int ngroups, int nr) {
-  const int key = ngroups * 8 + nr;
-  auto it = c->cp_plans.find(key);
-  if (it != c->cp_plans.end()) return it->second.get();
-  const hz_grid& g = c->grid;
-  const int nzl = g.nz_local;
-  std::vector<CpTile> xy, in;
-  for (const CpBand& by : cp_bands(g.ny, c->lo[1], c->hi[1]))
-    for (const CpBand& bx : cp_bands(g.nx, c->lo[0], c->hi[0]))
-      cp_tile_rect(bx.a, bx.b, by.a, by.b, CP_TILE_PTS(cp_rows(nr)), (bx.pml || by.pml) ? xy : in);
+  const double nt = (double)(xy.size() + in.size());
   int nch = 1;
-  if (const char* e = getenv("HZ_CP_ZC")) nch = std::max(1, (nzl + std::max(1, atoi(e)) - 1) / std::max(1, atoi(e)));
-  else {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->ctx->device);
-    const double slots = (double)sms * cp_occupancy(c->tab_n, nr);
-    const double nt = (double)(xy.size() + in.size());
-    double best_eff = -1;
-    for (int n = 1; n <= std::max(1, nzl / 4); n++) {
-      const double waves = nt * n * ngroups / slots;
-      const double L = (double)nzl / n;
-      const double eff = waves / std::ceil(waves) * L / (L + 2.0);
-      if (eff > best_eff + 1e-9) { best_eff = eff; nch = n; }
-    }
+  double best = -1;
+  for (int n = 1; n <= std::max(1, nzl / 4); n++) {
+    const double waves = nt * n * ngroups / std::max(1, slots);
+    const double L = (double)nzl / n;
+    const double eff = waves / std::ceil(waves) * L / (L + 2.0);
+    if (eff > best + 1e-9) { best = eff; nch = n; }
   }
-  // tiles outside the x/y-PML: the z-PML slabs [0, zl) and [zh, nzl) are items of their own (z-PML
-  // body), the planes between are cut like the x/y-PML tiles' slab (PML-free body)
-  const int zl = std::min(std::max(c->lo[2] - g.z0, 0), nzl);
-  const int zh = std::min(std::max(c->hi[2] - g.z0 + 1, zl), nzl);
+  const int zl = std::min(std::max(lo[2] - g.z0, 0), nzl);
+  const int zh = std::min(std::max(hi[2] - g.z0 + 1, zl), nzl);
   const int nin = std::max(1, (int)std::lround((double)nch * (zh - zl) / std::max(1, nzl)));
-  auto item = [](const CpTile& t, int a, int b, int mode) {
-    return cp_item(t.x0, t.y0, t.tx, t.ty, t.xs, t.ys, t.xe, t.ye, a, b, mode);
-  };
-  std::vector<int4> vxy, vz, vin;
-  // x/y-PML tiles cost more per point: cut them into proportionally shorter chunks (HZ_CP_XYF, default
-  // 1.5) so their CTAs end with the others
-  double xyf = 1.5;
-  if (const char* e = getenv("HZ_CP_XYF")) xyf = atof(e);
-  const int nxy = std::max(1, std::min(std::max(1, nzl / 2), (int)std::lround(nch * xyf)));
+  const int nxy = std::max(1, std::min(std::max(1, nzl / 2), (int)std::lround(nch * 1.5)));
+  out.clear();
   for (int k = 0; k < nxy; k++) {   // chunk-major: concurrently running CTAs share z-planes in L2
     const int a = (int)((long long)nzl * k / nxy), b = (int)((long long)nzl * (k + 1) / nxy);
     if (b > a)
-      for (const CpTile& t : xy) vxy.push_back(item(t, a, b, CP_PMLXY));
+      for (auto& t : xy) out.push_back(tm_item(t.first, t.second, a, b, TM_PMLXY));
   }
-  for (const CpTile& t : in) {
-    if (zl > 0) vz.push_back(item(t, 0, zl, CP_PMLZ));
-    if (zh < nzl) vz.push_back(item(t, zh, nzl, CP_PMLZ));
+  for (auto& t : in) {
+    if (zl > 0) out.push_back(tm_item(t.first, t.second, 0, zl, TM_PMLZ));
+    if (zh < nzl) out.push_back(tm_item(t.first, t.second, zh, nzl, TM_PMLZ));
   }
   for (int k = 0; k < nin; k++) {
     const int a = zl + (int)((long long)(zh - zl) * k / nin), b = zl + (int)((long long)(zh - zl) * (k + 1) / nin);
     if (b > a)
-      for (const CpTile& t : in) vin.push_back(item(t, a, b, CP_LEAN));
+      for (auto& t : in) out.push_back(tm_item(t.first, t.second, a, b, TM_LEAN));
   }
-  vz.insert(vz.end(), vin.begin(), vin.end());
-  vin.swap(vz);
-  std::unique_ptr<hz_coeffs::CpPlan> pl(new hz_coeffs::CpPlan);
-  pl->n_xy = (int)vxy.size();
-  pl->n_in = (int)vin.size();
-  vxy.insert(vxy.end(), vin.begin(), vin.end());
-  if (pl->work.ensure(std::max<size_t>(1, vxy.size()) * sizeof(int4)) != cudaSuccess) return nullptr;
-  if (!vxy.empty() && cudaMemcpy(pl->work.p, vxy.data(), vxy.size() * sizeof(int4), cudaMemcpyHostToDevice) != cudaSuccess)
+}
+
+const hz_coeffs::TmPlan* tm_plan(hz_coeffs* c, int ngroups, int nr) {
+  const int key = ngroups * 8 + nr;
+  auto it = c->tm_plans.find(key);
+  if (it != c->tm_plans.end()) return it->second.get();
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->ctx->device);
+  const int slots = sms * tm_occupancy(c->tab_n, c->tm_tx, c->tm_ty, nr);
+  std::vector<int4> items;
+  tm_build_items(c->grid, c->ldx, c->tm_tx, c->tm_ty, c->lo, c->hi, slots, ngroups, items);
+  std::unique_ptr<hz_coeffs::TmPlan> pl(new hz_coeffs::TmPlan);
+  pl->n_items = (int)items.size();
+  if (pl->work.ensure(std::max<size_t>(1, items.size()) * sizeof(int4)) != cudaSuccess) return nullptr;
+  if (!items.empty() && cudaMemcpy(pl->work.p, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice) != cudaSuccess)
     return nullptr;
   auto* raw = pl.get();
-  c->cp_plans[key] = std::move(pl);
+  c->tm_plans[key] = std::move(pl);
   return raw;
 }
 
 }  // namespace
 
-extern "C" int hz_debug_plan_tiles(int nx, int ny, int lo_x, int hi_x, int lo_y, int hi_y, int rows_per_thread,
-                                   int* out, int max_tiles) {
-  if (nx < 3 || ny < 3 || nx > 65535 || ny > 65535 || (rows_per_thread != 1 && rows_per_thread != 2) ||
-      (max_tiles > 0 && out == nullptr))
+// test hook (include/hz_debug.h): the tensor-map apply's work list for a single slab
+extern "C" int hz_debug_plan_tiles(int nx, int ny, int nz, int lo_x, int hi_x, int lo_y, int hi_y, int lo_z, int hi_z,
+                                   int slots, int ngroups, int* out, int max_items, int* tile_wh) {
+  if (nx < 3 || ny < 3 || nz < 1 || nx > 65535 || ny > 65535 || nz > 65535 || slots < 1 || ngroups < 1 ||
+      (max_items > 0 && out == nullptr))
     return -1;
-  std::vector<CpTile> xy, in;
-  for (const CpBand& by : cp_bands(ny, lo_y, hi_y))
-    for (const CpBand& bx : cp_bands(nx, lo_x, hi_x))
-      cp_tile_rect(bx.a, bx.b, by.a, by.b, CP_TILE_PTS(rows_per_thread), (bx.pml || by.pml) ? xy : in);
-  int n = 0;
-  for (int cls = 0; cls < 2; cls++)
-    for (const CpTile& t : cls == 0 ? xy : in) {
-      if (n < max_tiles) {
-        int* o = out + 9 * n;
-        o[0] = t.x0; o[1] = t.y0; o[2] = t.tx; o[3] = t.ty; o[4] = t.xs; o[5] = t.ys; o[6] = t.xe; o[7] = t.ye;
-        o[8] = cls == 0 ? 1 : 0;
-      }
-      n++;
-    }
-  return n;
+  hz_grid g{nx, ny, nz, 0, nz, 1.0, 0};
+  const int ldx = hz_field_ldx(nx);
+  const int tx = tm_tile_width(ldx);
+  const int ty = tm_rows(tx);
+  const int lo[3] = {lo_x, lo_y, lo_z}, hi[3] = {hi_x, hi_y, hi_z};
+  std::vector<int4> items;
+  tm_build_items(g, ldx, tx, ty, lo, hi, slots, ngroups, items);
+  for (int n = 0; n < (int)items.size() && n < max_items; n++) {
+    const int4 t = items[n];
+    int* o = out + 5 * n;
+    o[0] = t.x & 0xffff; o[1] = t.x >> 16; o[2] = t.y & 0xffff; o[3] = t.y >> 16; o[4] = t.z;
+  }
+  if (tile_wh) { tile_wh[0] = tx; tile_wh[1] = ty; }
+  return (int)items.size();
 }
 
 namespace {
 
-// complex64 launches go through apply27_cp: point the params at the work list for this RHS count
+// One operator apply: complex64 (arithmetic and storage) through the tensor-map kernel, everything
+// else (complex128, the fp64 residual of the complex64 solver) through the register path.  Dot
+// epilogues get their partial / ticket scratch here.
 template <typename R, typename S>
-hz_status cp_attach(const hz_coeffs* c, ApplyParams<R, S>& p, int nrhs) {
-  if (!(sizeof(R) == 4 && sizeof(S) == 4 && c->cp_on)) return HZ_OK;
-  const int nr = cp_group(nrhs), ng = (nrhs + nr - 1) / nr;
-  const hz_coeffs::CpPlan* pl = cp_plan(const_cast<hz_coeffs*>(c), ng, nr);
-  if (!pl) { set_error("cp_plan: device allocation / copy failed"); return HZ_ERR_CUDA; }
-  p.cp_work = pl->work.as<int4>();
-  p.cp_n_pml = pl->n_xy;
-  p.cp_n_int = pl->n_in;
-  p.cp_nblocks = pl->n_xy + pl->n_in;
+hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int epi, cudaStream_t s) {
+  hz_coeffs* c = const_cast<hz_coeffs*>(cc);
+  const int K = epi_k(epi);
+  constexpr bool TM = sizeof(R) == 4 && sizeof(S) == 4;
+  TmLaunch L{nullptr, nullptr};
+  long long nb = 0;
+  if constexpr (TM) {
+    const int nr = tm_group(nrhs, epi), ng = (nrhs + nr - 1) / nr;
+    const hz_coeffs::TmPlan* pl = tm_plan(c, ng, nr);
+    if (!pl) { set_error("tm_plan: device allocation / copy failed"); return HZ_ERR_CUDA; }
+    p.tm_work = pl->work.template as<int4>();
+    p.tm_nblocks = pl->n_items;
+    L.w = &c->tmap_w;
+    L.u = tm_umap(c, p.u, nrhs);
+    if (!L.u) return HZ_ERR_CUDA;
+    nb = pl->n_items;
+  } else {
+    ApplyParams<R, S> pp = p;
+    nb = apply_plan<R, S>(pp);
+  }
+  if (K > 0) {
+    HZ_CUDA(c->partials.ensure(sizeof(double) * (size_t)nb * K * nrhs));
+    if (c->tickets.n < sizeof(unsigned) * (size_t)nrhs) {
+      HZ_CUDA(c->tickets.ensure(sizeof(unsigned) * (size_t)nrhs));
+      HZ_CUDA(cudaMemsetAsync(c->tickets.p, 0, c->tickets.n, s));
+    }
+    p.partials = c->partials.as<double>();
+    p.tickets = c->tickets.as<unsigned>();
+  }
+  if constexpr (TM) {
+    HZ_CUDA(launch_apply_tm(L, p, nrhs, c->mass == HZ_MASS_COLLOC, epi, s));
+  } else {
+    HZ_CUDA(launch_apply<R, S>(p, nrhs, c->mass == HZ_MASS_COLLOC, epi, s));
+  }
+  count_launch(apply_last_launches());
   return HZ_OK;
 }
 
@@ -626,8 +831,9 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
     return HZ_ERR_INVALID_ARG;
   }
   cudaStream_t s = 0;
+  c->ldx = hz_field_ldx(g->nx);
   const long long plane = c->plane();
-  const long long nloc = plane * g->nz_local;
+  const long long nloc = (long long)g->nx * g->ny * g->nz_local;   // owned points
   // ---- table: rank 0's rows broadcast to all ranks (bitwise-identical weights everywhere)
   c->table = table->t;
   if (ctx->nranks > 1) {
@@ -635,7 +841,7 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
     const size_t nb = 5 * (size_t)c->table.n_g * sizeof(double);
     HZ_CUDA(tb.ensure(nb));
     HZ_CUDA(cudaMemcpy(tb.p, c->table.rows5.data(), nb, cudaMemcpyHostToDevice));
-    HZ_TRY(nccl_check(g_nccl.Broadcast(tb.p, tb.p, 5 * (size_t)c->table.n_g, ncclDouble, 0, ctx->comm, s), "ncclBroadcast"));
+    HZ_TRY(comm_bcast(ctx, tb.as<double>(), 5 * (size_t)c->table.n_g, s));
     HZ_CUDA(cudaMemcpy(c->table.rows5.data(), tb.p, nb, cudaMemcpyDeviceToHost));
   }
   // device table rows: (t1, t2, mu0, mu1, mu2 | forward differences), t1 = ws2/12, t2 = ws3/8 (A6)
@@ -708,23 +914,25 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
     }
   }
   // ---- velocity with halo planes
+  // pitched [nzl+2][ny][ldx] copy of the caller's [nz][ny][nx] model; pad columns and the halo planes
+  // outside the global grid stay 0 (never read as model values: the apply zero-fills those points)
   HZ_CUDA(c->v.ensure((size_t)(g->nz_local + 2) * plane * sizeof(R)));
-  {
-    R one = R(1);
-    std::vector<R> ones((size_t)plane, one);
-    HZ_CUDA(cudaMemcpy(c->v.as<R>(), ones.data(), plane * sizeof(R), cudaMemcpyHostToDevice));
-    HZ_CUDA(cudaMemcpy(c->v.as<R>() + (g->nz_local + 1) * plane, ones.data(), plane * sizeof(R), cudaMemcpyHostToDevice));
-  }
+  HZ_CUDA(cudaMemsetAsync(c->v.p, 0, (size_t)(g->nz_local + 2) * plane * sizeof(R), s));
   {
     const cudaMemcpyKind kind = is_device_ptr(v_in) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const R* vin = reinterpret_cast<const R*>(v_in);
+    const size_t rowb = (size_t)g->nx * sizeof(R), pitch = (size_t)c->ldx * sizeof(R);
+    const size_t vplane = (size_t)g->nx * g->ny;   // elements of one caller plane
+    auto copy_planes = [&](int dst_plane, const R* src, int nplanes) {
+      return cudaMemcpy2DAsync(c->v.as<R>() + (size_t)dst_plane * plane, pitch, src, rowb, rowb,
+                               (size_t)nplanes * g->ny, kind, s);
+    };
     if (g->v_halo) {
-      const R* vin = reinterpret_cast<const R*>(v_in);
-      HZ_CUDA(cudaMemcpy(c->v.as<R>() + plane, vin + plane, nloc * sizeof(R), kind));
-      if (g->z0 > 0) HZ_CUDA(cudaMemcpy(c->v.as<R>(), vin, plane * sizeof(R), kind));
-      if (g->z0 + g->nz_local < g->nz_global)
-        HZ_CUDA(cudaMemcpy(c->v.as<R>() + (g->nz_local + 1) * plane, vin + (g->nz_local + 1) * plane, plane * sizeof(R), kind));
+      HZ_CUDA(copy_planes(1, vin + vplane, g->nz_local));
+      if (g->z0 > 0) HZ_CUDA(copy_planes(0, vin, 1));
+      if (g->z0 + g->nz_local < g->nz_global) HZ_CUDA(copy_planes(g->nz_local + 1, vin + (size_t)(g->nz_local + 1) * vplane, 1));
     } else {
-      HZ_CUDA(cudaMemcpy(c->v.as<R>() + plane, v_in, nloc * sizeof(R), kind));
+      HZ_CUDA(copy_planes(1, vin, g->nz_local));
     }
   }
   // ---- statistics: domain check, v range, clamps
@@ -732,8 +940,8 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
   HZ_CUDA(st.ensure(4 * sizeof(unsigned long long)));
   unsigned long long init[4] = {~0ULL, 0ULL, 0ULL, 0ULL};
   HZ_CUDA(cudaMemcpy(st.p, init, sizeof(init), cudaMemcpyHostToDevice));
-  HZ_CUDA(launch_vstats<R>(c->v.as<R>() + plane, nloc, (R)(1.0 / (freq * g->h)), (R)c->g_min, (R)c->g_max,
-                           st.as<unsigned long long>(), s));
+  HZ_CUDA(launch_vstats<R>(c->v.as<R>() + plane, nloc, g->nx, c->ldx, (R)(1.0 / (freq * g->h)), (R)c->g_min,
+                           (R)c->g_max, st.as<unsigned long long>(), s));
   count_launch();
   unsigned long long res[4];
   HZ_CUDA(cudaMemcpy(res, st.p, sizeof(res), cudaMemcpyDeviceToHost));
@@ -749,9 +957,8 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
     HZ_CUDA(sb.ensure(4 * sizeof(double)));
     double sv[4] = {stats[0], stats[1], vmax, -vmin};
     HZ_CUDA(cudaMemcpy(sb.p, sv, sizeof(sv), cudaMemcpyHostToDevice));
-    HZ_TRY(nccl_check(g_nccl.AllReduce(sb.p, sb.p, 2, ncclDouble, ncclSum, ctx->comm, s), "ncclAllReduce"));
-    HZ_TRY(nccl_check(g_nccl.AllReduce(sb.as<double>() + 2, sb.as<double>() + 2, 2, ncclDouble, ncclMax, ctx->comm, s),
-                      "ncclAllReduce"));
+    HZ_TRY(comm_allreduce(ctx, sb.as<double>(), 2, 0, s));
+    HZ_TRY(comm_allreduce(ctx, sb.as<double>() + 2, 2, 1, s));
     HZ_CUDA(cudaMemcpy(sv, sb.p, sizeof(sv), cudaMemcpyDeviceToHost));
     stats[0] = sv[0];
     stats[1] = sv[1];
@@ -817,17 +1024,20 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
   }
   // ---- launch geometry: strips of NY rows; z chunks sized to give >= ~4 waves
   {
-    const long long bx = apply_nblocks_x<R>(g->nx, g->ny);
+    const long long bx = apply_nblocks_x<double>(g->nx, g->ny);
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    const long long target = 4LL * dev_sms * apply_occupancy<R>(mass == HZ_MASS_COLLOC);
+    const long long target = 4LL * dev_sms * apply_occupancy<double>(mass == HZ_MASS_COLLOC);
     long long nch = (target + bx - 1) / bx;
     const long long maxch = std::max(1, g->nz_local / 8);
     nch = std::max(1LL, std::min(nch, maxch));
     c->zc = (int)((g->nz_local + nch - 1) / nch);
     c->nchunks = (g->nz_local + c->zc - 1) / c->zc;
   }
-  if (sizeof(R) == 4) HZ_TRY(cp_geometry(c.get()));
+  if (sizeof(R) == 4) {   // complex64: tile geometry and the tensor map of w for apply27_tm
+    tm_geometry(c.get());
+    HZ_TRY(tm_encode(c.get(), &c->tmap_w, c->w.p, 4, 1));
+  }
   // ---- GAm: the 27-node mean weights of every owned row, once (A19)
   if (rule != HZ_RULE_GA) {
     HZ_CUDA(c->gam.ensure(5 * (size_t)c->fstride() * sizeof(R)));
@@ -855,7 +1065,11 @@ hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, c
     set_error("hz_assemble_coeffs: bad grid (dims >= 3, slab inside the global grid; S:156)");
     return HZ_ERR_INVALID_ARG;
   }
-  if ((long long)(g.nz_local + 2) * g.nx * g.ny >= (1LL << 31)) {
+  if (g.nx > 65532 || g.ny > 65535 || g.nz_local > 65535) {
+    set_error("hz_assemble_coeffs: nx <= 65532, ny and nz_local <= 65535 (apply work-item packing)");
+    return HZ_ERR_INVALID_ARG;
+  }
+  if ((long long)(g.nz_local + 2) * hz_field_ldx(g.nx) * g.ny >= (1LL << 31)) {
     set_error("hz_assemble_coeffs: slab of >= 2^31 points per field (32-bit offsets in the apply); "
               "split the grid over more z-slabs");
     return HZ_ERR_INVALID_ARG;
@@ -874,15 +1088,17 @@ hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, c
 void hz_coeffs_destroy(hz_coeffs* c) {
   if (!c) return;
   // buffers go back to the cache for reuse: let queued work that still reads them finish first
+  cudaSetDevice(c->ctx->device);
   cudaDeviceSynchronize();
   delete c;
 }
 
 hz_status hz_coeffs_export(const hz_coeffs* c, void* record, void* pml_host, int nmax) {
   if (!c) { set_error("hz_coeffs_export: NULL coeffs"); return HZ_ERR_INVALID_ARG; }
+  HZ_TRY(set_device(c->ctx));
   cudaStream_t s = 0;
   if (record) {
-    const size_t nb = 8 * (size_t)c->plane() * c->grid.nz_local * c->esz();
+    const size_t nb = 8 * (size_t)c->npoints() * c->esz();
     const bool dev = is_device_ptr(record);
     DBuf tmp;
     void* dst = record;
@@ -946,6 +1162,7 @@ static hz_status apply_t(const hz_coeffs* c, void* u, void* au, int nrhs, cudaSt
 extern "C" hz_status hz_apply_impedance(const hz_coeffs* c, void* u, void* au, int nrhs, void* stream) {
   if (!c || !u || !au || nrhs < 1) { set_error("hz_apply_impedance: bad arguments"); return HZ_ERR_INVALID_ARG; }
   if (u == au) { set_error("hz_apply_impedance: u and au must not alias"); return HZ_ERR_INVALID_ARG; }
+  HZ_TRY(set_device(c->ctx));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return c->dtype == HZ_C64 ? apply_t<float>(c, u, au, nrhs, s) : apply_t<double>(c, u, au, nrhs, s);
 }
@@ -994,6 +1211,7 @@ static hz_status sources_t(const hz_coeffs* c, int nsrc, const long long* nodes,
 extern "C" hz_status hz_point_sources(const hz_coeffs* c, int nsrc, const long long* node_xyz,
                                       const double* amp_re_im, int consistent, void* b, void* stream) {
   if (!c || nsrc < 1 || !node_xyz || !b) { set_error("hz_point_sources: bad arguments"); return HZ_ERR_INVALID_ARG; }
+  HZ_TRY(set_device(c->ctx));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return c->dtype == HZ_C64 ? sources_t<float>(c, nsrc, node_xyz, amp_re_im, consistent, b, s)
                             : sources_t<double>(c, nsrc, node_xyz, amp_re_im, consistent, b, s);
@@ -1017,8 +1235,8 @@ static hz_status eqerror_t(const hz_coeffs* c, const void* uref, const void* u, 
   const int nb = 148 * 4;
   HZ_CUDA(part.ensure(sizeof(double) * 4 * nb));
   const hz_grid& g = c->grid;
-  HZ_CUDA(launch_eqerror<R>(reinterpret_cast<const C*>(rd), reinterpret_cast<const C*>(ud), g.nx, g.ny, g.nz_local, g.z0,
-                            g.nz_global, src, g.h, npml, ball, part.as<double>(), nb, s));
+  HZ_CUDA(launch_eqerror<R>(reinterpret_cast<const C*>(rd), reinterpret_cast<const C*>(ud), g.nx, g.ny, c->ldx, g.nz_local,
+                            g.z0, g.nz_global, src, g.h, npml, ball, part.as<double>(), nb, s));
   count_launch();
   std::vector<double> hp(4 * nb);
   HZ_CUDA(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * 4 * nb, cudaMemcpyDeviceToHost, s));
@@ -1042,6 +1260,7 @@ static hz_status eqerror_t(const hz_coeffs* c, const void* uref, const void* u, 
 extern "C" hz_status hz_eqerror(const hz_coeffs* c, const void* u_ref, const void* u, const long long src_xyz[3],
                                 int npml_mask, double ball_cells, double* err_out, void* stream) {
   if (!c || !u_ref || !u || !src_xyz || !err_out || npml_mask < 0) { set_error("hz_eqerror: bad arguments"); return HZ_ERR_INVALID_ARG; }
+  HZ_TRY(set_device(c->ctx));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return c->dtype == HZ_C64 ? eqerror_t<float>(c, u_ref, u, src_xyz, npml_mask, ball_cells, err_out, s)
                             : eqerror_t<double>(c, u_ref, u, src_xyz, npml_mask, ball_cells, err_out, s);
@@ -1050,7 +1269,7 @@ extern "C" hz_status hz_eqerror(const hz_coeffs* c, const void* u_ref, const voi
 template <typename R>
 static hz_status matrix_t(const hz_coeffs* c, long long* cols, void* vals, cudaStream_t s) {
   typedef typename Cx<R>::T C;
-  const size_t n = (size_t)c->grid.nz_local * c->plane() * 27;
+  const size_t n = (size_t)c->npoints() * 27;
   DBuf dc, dv;
   long long* cd = cols;
   void* vd = vals;
@@ -1068,6 +1287,7 @@ static hz_status matrix_t(const hz_coeffs* c, long long* cols, void* vals, cudaS
 
 extern "C" hz_status hz_export_matrix(const hz_coeffs* c, long long* cols, void* vals, void* stream) {
   if (!c || !cols || !vals) { set_error("hz_export_matrix: bad arguments"); return HZ_ERR_INVALID_ARG; }
+  HZ_TRY(set_device(c->ctx));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return c->dtype == HZ_C64 ? matrix_t<float>(c, cols, vals, s) : matrix_t<double>(c, cols, vals, s);
 }
@@ -1168,17 +1388,18 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
     HZ_CUDA(w.r2.ensure(fb));
     HZ_CUDA(w.dotG.ensure(sizeof(double) * nrhs));
   }
-  if (sizeof(R) == 4) {
-    HZ_CUDA(w.xlo.ensure(fb));
-    HZ_CUDA(cudaMemsetAsync(w.xlo.p, 0, fb, s));
-  }
+  if (sizeof(R) == 4) HZ_CUDA(w.xlo.ensure(fb));
+  // the workspace starts at zero: pad columns stay 0 in every Krylov vector (the applies write
+  // zeros there, the fp64 residual does not touch them), so the flat dot products see only points
+  for (DBuf* d : {&w.rhat, &w.p, &w.v, &w.t, &w.r, &w.r1, &w.r2, &w.xlo})
+    if (d->p && d->n >= fb) HZ_CUDA(cudaMemsetAsync(d->p, 0, fb, s));
   HZ_CUDA(w.dotA.ensure(sizeof(double) * 2 * nrhs));
   HZ_CUDA(w.dotB.ensure(sizeof(double) * 7 * nrhs));
   HZ_CUDA(w.dotR.ensure(sizeof(double) * 3 * nrhs));
   HZ_CUDA(w.dotN.ensure(sizeof(double) * nrhs));
   HZ_CUDA(w.state.ensure(sizeof(SolverState) * nrhs));
   HZ_CUDA(w.active.ensure(sizeof(int) * nrhs));
-  const long long n = c->plane() * c->grid.nz_local;
+  const long long n = c->plane() * c->grid.nz_local;   // storage elements of the owned planes (pads included)
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->ctx->device);
   const int vblocks = (int)std::max(1LL, std::min((n + 1023) / 1024, (long long)(8 * sms + nrhs - 1) / nrhs));
@@ -1251,6 +1472,7 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   bool use_lo = sizeof(R) == 4;   // false for the final residual of the rounded output x
   auto resid = [&](bool with_rhat) -> hz_status {
     HZ_TRY(halo_exchange(c, x, nrhs, sizeof(C), s));
+    if (use_lo) HZ_TRY(halo_exchange(c, w.xlo.p, nrhs, sizeof(C), s));   // the compensation word's halo too
     timer.mark(s);
     if constexpr (sizeof(R) == 4) {
       ApplyParams<double, float> p = make_params<double, float>(c);
@@ -1283,8 +1505,8 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   };
 
   // ‖b‖²
-  HZ_CUDA(launch_norm2<R>(b, c->fstride(), c->plane(), n, nrhs, vblocks, w.partials.as<double>(), w.dotN.as<double>(),
-                          w.tickets.as<unsigned>(), s));
+  HZ_CUDA(launch_norm2<R>(b, c->fstride(), c->plane(), c->npoints(), c->grid.nx, c->ldx, nrhs, vblocks,
+                          w.partials.as<double>(), w.dotN.as<double>(), w.tickets.as<unsigned>(), s));
   count_launch();
   HZ_TRY(allreduce_sum(c, w.dotN.as<double>(), nrhs, s));
   std::vector<double> bn2(nrhs);
@@ -1311,6 +1533,10 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   HZ_TRY(init());
 
   int restarts = 0, replacements = 0;
+  // breakdown restarts per RHS: a RHS that breaks down more than restart_cap times is retired on its
+  // own (HZ_BREAKDOWN); the cap lets the stall window act first on a RHS at its rounding floor
+  std::vector<int> rs_count(nrhs, 0);
+  bool broke_any = false;
   int it = 0;
   std::vector<double> hdot(3 * nrhs);
   std::vector<SolverState> hst(nrhs);
@@ -1321,6 +1547,7 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   const int stall_iters = o.stall_window > 0   ? o.stall_window
                           : o.stall_window < 0 ? INT_MAX
                                                : std::max(20 * std::max(1, o.replace_every), 1000);
+  const int restart_cap = std::max(50, stall_iters == INT_MAX ? INT_MAX / 2 : stall_iters / std::max(1, o.check_every) + 1);
   // initial convergence check (x0 may already solve the system)
   HZ_CUDA(cudaMemcpyAsync(hdot.data(), w.dotR.p, sizeof(double) * 3 * nrhs, cudaMemcpyDeviceToHost, s));
   HZ_CUDA(cudaStreamSynchronize(s));
@@ -1414,10 +1641,19 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
       bool cand = false, brk = false;
       for (int r = 0; r < nrhs; r++) {
         if (!active[r]) continue;
-        if (hst[r].flags & 1) brk = true;
-        else if (hdot[3 * r] <= rtol2 * bn2[r]) cand = true;
+        if (hst[r].flags & 1) {
+          brk = true;
+          if (++rs_count[r] > restart_cap) {   // this RHS alone is retired
+            active[r] = 0;
+            broke_any = true;
+          }
+        } else if (hdot[3 * r] <= rtol2 * bn2[r]) {
+          cand = true;
+        }
       }
       if (brk) {  // restart broken RHS with r̂0 = r = b − A x (all active RHS restart together)
+        HZ_CUDA(cudaMemcpyAsync(w.active.p, active.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, s));
+        if (n_active() == 0) break;
         HZ_TRY(resid(false));
         // the recomputed true residuals also feed the convergence / stagnation test, so a RHS at its
         // rounding floor (where breakdowns recur) is retired by the stall window, not the restart cap
@@ -1426,7 +1662,6 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
         HZ_TRY(retire(true));
         HZ_TRY(init());
         restarts++;
-        if (restarts > 50) break;
         continue;
       }
       if (replaced) {
@@ -1472,17 +1707,36 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
     stats->stagnated = stagnated_any ? 1 : 0;
   }
   if (conv) return HZ_OK;
-  return restarts > 50 ? HZ_BREAKDOWN : HZ_NOT_CONVERGED;
+  return broke_any ? HZ_BREAKDOWN : HZ_NOT_CONVERGED;
 }
 
 }  // namespace
 
+extern "C" hz_solve_opts hz_solve_opts_default(void) {
+  hz_solve_opts o;
+  memset(&o, 0, sizeof(o));
+  o.rtol = 1e-6;
+  o.max_iter = 20000;
+  o.replace_every = 50;
+  o.check_every = 10;
+  o.ell = 1;
+  return o;
+}
+
 extern "C" hz_status hz_solve(const hz_coeffs* c, const void* b, void* x, int nrhs, const hz_solve_opts* opts,
                               double* relres_out, int* iters_out, hz_solve_stats* stats, void* stream) {
   if (!c || !b || !x || nrhs < 1) { set_error("hz_solve: bad arguments"); return HZ_ERR_INVALID_ARG; }
-  hz_solve_opts o = {1e-6, 20000, 50, 10, 0, 1, 0};
+  HZ_TRY(set_device(c->ctx));
+  hz_solve_opts o = hz_solve_opts_default();
   if (opts) o = *opts;
+  // zero selects each field's default (a zero-initialised struct is the default configuration)
+  if (o.rtol == 0) o.rtol = 1e-6;
+  if (o.max_iter == 0) o.max_iter = 20000;
+  if (o.replace_every == 0) o.replace_every = 50;
+  if (o.check_every == 0) o.check_every = 10;
   if (!(o.rtol > 0) || o.max_iter < 1) { set_error("hz_solve: need rtol > 0, max_iter >= 1"); return HZ_ERR_INVALID_ARG; }
+  if (o.replace_every < 0) o.replace_every = 0;   // < 0: no residual replacement
+  if (o.check_every < 1) { set_error("hz_solve: check_every must be >= 0"); return HZ_ERR_INVALID_ARG; }
   if (o.ell == 0) o.ell = 1;
   if (o.ell != 1 && o.ell != 2) { set_error("hz_solve: ell must be 1 (BiCGSTAB) or 2 (BiCGStab(2))"); return HZ_ERR_INVALID_ARG; }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -6,9 +6,9 @@
 //          + Σ_a Σ_e D_a(n_a,e) Σ_{p,q} T(p,q; w_n) u_{n+e ê_a+p ê_b+q ê_c}   A6 (App. A), A8
 //   w_n = linear interpolation of the Tikhonov table at G = v_n/(f h), clamped   P:36, A13
 //
-// The kernels: apply27_cp.cuh (complex64, RHS-fused, every tile class in one launch),
-// apply27.cuh (register path: complex128 and the fp64 residual of the complex64 solver),
-// apply27_tma.cuh (bulk-copy interior kernel, the HZ_NO_CP reference path).  DESIGN.md §5.
+// The kernels: apply27_tm.cuh (complex64: tensor-map TMA tiles, RHS-fused, every tile class in one
+// launch), apply27.cuh (register path: complex128 and the fp64 residual of the complex64 solver).
+// DESIGN.md §5.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -33,10 +33,10 @@ struct ApplyParams {
   typedef typename Cx<R>::T C;
   typedef typename Cx<S>::T CS;
   int nx, ny, nzl;            // local slab dims
+  int ldx;                    // row pitch of every field / model array (elements): nx rounded up to 4
   int z0, nzg;                // global index of local plane 0, global nz
-  long long plane;            // nx*ny
+  long long plane;            // ny*ldx
   long long fstride;          // (nzl+2)*plane: per-RHS field stride (elements)
-  long long nlanes;           // nstrips*nx (set by the launcher)
   // z-chunks of the local planes: [0, zlo) (if nlow = 1), nint chunks of ≤ zc planes covering
   // [zlo, zhi) (the planes whose outputs are outside the z-PML and the grid's first/last plane), then
   // [zhi, nzl) (if non-empty); nchunks = nlow + nint + nhigh.  See chunk_range().
@@ -45,23 +45,21 @@ struct ApplyParams {
   // interior "box" (no PML, no boundary) covered by the lean launch: strips [box_s0, box_s1),
   // x-tiles [box_t0, box_t1), z-chunks [box_c0, box_c1); box_nbx CTAs per chunk
   int box_s0, box_s1, box_t0, box_t1, box_c0, box_c1, box_nbx;
-  // complex64 interior launch (apply27_tma): the box as points [tma_x0, tma_x1) × [tma_y0, tma_y1),
-  // tiled by tma_ntx × tma_nty CTA tiles (then box_nbx = tma_ntx · tma_nty)
-  int tma_x0, tma_x1, tma_y0, tma_y1, tma_ntx, tma_nty;
   // general launch work list per RHS: the boundary z-chunks (low, high) × all warps (nbx CTAs each),
   // then the interior z-chunks × the "frame" of warps outside the box (nbx_frame CTAs each)
   int nbound, nbx_frame, frame_warps, gen_blocks;
-  // complex64 RHS-fused launch (apply27_cp): work items (cp_item) — first cp_n_pml x/y-PML tiles,
-  // then cp_n_int tiles outside the x/y-PML; cp_nblocks = dot partial slots per RHS
-  const int4* cp_work;
-  int cp_n_pml, cp_n_int, cp_nblocks;
-  const S* v;                 // [nzl+2][ny][nx] velocity incl. halo planes
-  const S* w;                 // [nzl+2][ny][nx] 1/v² incl. halo planes (apply input)
-  const S* gam;               // GAm rule (A19): [5][nzl+2][ny][nx] row weights (t1, t2, μ0, μ1, μ2)
+  // complex64 tensor-map launch (apply27_tm): work items (tm_item), x/y-PML tiles first;
+  // tm_nblocks = items = dot partial slots per RHS; tiles of tm_tx × tm_ty points; tm_org = first
+  // storage plane covered by the tensor maps (planes outside the global grid are zero-filled)
+  const int4* tm_work;
+  int tm_nblocks, tm_tx, tm_ty, tm_org;
+  const S* v;                 // [nzl+2][ny][ldx] velocity incl. halo planes
+  const S* w;                 // [nzl+2][ny][ldx] 1/v² incl. halo planes (apply input)
+  const S* gam;               // GAm rule (A19): [5][nzl+2][ny][ldx] row weights (t1, t2, μ0, μ1, μ2)
                               // averaged over the 27 stencil nodes (stride fstride), or null (GA)
   const R* ctab;              // [n_g][CTAB_STRIDE] pre-scaled class coefficients + differences
   int tab_lo, tab_n;          // rows [tab_lo, tab_lo + tab_n) cover every G of the model (staged in smem)
-  const CS* u;                // [nrhs][nzl+2][ny][nx]
+  const CS* u;                // [nrhs][nzl+2][ny][ldx]
   const CS* ulo;              // optional low part of u (mixed-precision residual of the c64 solver:
                               // u = u + ulo in fp64; only read when R != S), else null
   CS* au;                     // output

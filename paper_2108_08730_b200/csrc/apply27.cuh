@@ -5,7 +5,7 @@
 //   w_n = clamped linear interpolation of the Tikhonov weight table at G_n = v_n/(f h)  P:36, A13
 //
 // B200 design (HBM-bound: 4 + 16·nrhs bytes/point for complex64):
-//  * Data: u (complex, [nrhs][nzl+2][ny][nx]) and w = 1/v² (real, [nzl+2][ny][nx], library-owned) are
+//  * Data: u (complex, [nrhs][nzl+2][ny][ldx]) and w = 1/v² (real, [nzl+2][ny][ldx], library-owned) are
 //    the only per-point inputs; the row coefficients are recomputed from w in registers (G = 1/(√w f h)).
 //    The coefficient table is pre-scaled on the host to the class coefficients
 //    (c1..c3 = h⁻²(t0−4t1, 2t1−2t2, 3t2), m1..m3 = ω²μ1..3) with forward differences, 12 values per
@@ -116,14 +116,8 @@ struct PlaneRegs {
 // shuffles, and out-of-grid columns/rows load zeros: Dirichlet without masks).  XT = 30 outputs/warp.
 constexpr int XT = 30;
 
-#ifndef HZ_MINB_F
-#define HZ_MINB_F 3
-#endif
-template <typename R> struct ApplyBounds { enum { MINB = HZ_MINB_F }; };
-#ifndef HZ_MINB_D
-#define HZ_MINB_D 3
-#endif
-template <> struct ApplyBounds<double> { enum { MINB = HZ_MINB_D }; };
+// resident CTAs per SM (4 warps each) the register budget is sized for
+template <typename R> struct ApplyBounds { enum { MINB = 3 }; };
 
 // The apply is two launches of this template (same arithmetic per point, so results do not depend on
 // which launch computes a point):
@@ -176,7 +170,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nx = p.nx, ny = p.ny;
+  const int nx = p.nx, ny = p.ny, lx = p.ldx;
   const int ntx = (nx + XT - 1) / XT;
   const int nstrips = (ny + NY - 1) / NY;
   const int gw = gw0 + warp;
@@ -230,10 +224,8 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
       const int y = y0 + i;
       yp = yp || (is_out && y < ny && (y < p.lo[1] || y > p.hi[1]));
     }
-#ifndef HZ_NO_PML
     gen_x = __any_sync(FULL, xp);
     gen_y = __any_sync(FULL, yp);
-#endif
   }
   const bool gen_col = gen_x || gen_y;
 
@@ -245,7 +237,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
   const CS* __restrict__ ubase = p.u + (long long)rhs * p.fstride;
   const CS* __restrict__ ulbase = (MIXED && p.ulo != nullptr) ? p.ulo + (long long)rhs * p.fstride : nullptr;
   const S* __restrict__ wbase = MIXED ? p.v : p.w;
-  const int loff = (y0 - 1) * nx + x;          // (storage plane 0, row y0-1, column x); < 0 only if masked
+  const int loff = (y0 - 1) * lx + x;          // (storage plane 0, row y0-1, column x); < 0 only if masked
   const C czv = czero(R(0));
   const int zlo = p.lo[2], zhi = p.hi[2];
   const int zbase = p.z0;
@@ -259,8 +251,8 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
     if (!MIXED && (INTERIOR || (full_tile && zbase + pl >= 0 && zbase + pl < p.nzg))) {
 #pragma unroll
       for (int r = 0; r < NY + 2; r++) {
-        P.u[r] = to_cx(ldg_c(ubase + (unsigned)(off + r * nx)), R(0));
-        P.w[r] = (R)__ldg(wbase + (unsigned)(off + r * nx));
+        P.u[r] = to_cx(ldg_c(ubase + (unsigned)(off + r * lx)), R(0));
+        P.w[r] = (R)__ldg(wbase + (unsigned)(off + r * lx));
       }
       return;
     }
@@ -269,7 +261,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
 #pragma unroll
     for (int r = 0; r < NY + 2; r++) {
       const bool ok = (m >> r) & 1u;
-      const unsigned o = (unsigned)(off + r * nx);
+      const unsigned o = (unsigned)(off + r * lx);
       if (!MIXED) {
         P.u[r] = ok ? to_cx(ldg_c(ubase + o), R(0)) : czv;
         P.w[r] = ok ? (R)__ldg(wbase + o) : R(0);
@@ -284,11 +276,11 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
   auto fetch_w = [&](R (&wc)[NY], int pl) {
     const int zg = zbase + pl;
     const bool pin = INTERIOR || (zg >= 0 && zg < p.nzg);
-    const int off = loff + (pl + 1) * plane + nx;
+    const int off = loff + (pl + 1) * plane + lx;
 #pragma unroll
     for (int i = 0; i < NY; i++) {
       const bool ok = INTERIOR || (pin && ((rmask >> (i + 1)) & 1u));
-      const unsigned o = (unsigned)(off + i * nx);
+      const unsigned o = (unsigned)(off + i * lx);
       if (!MIXED) {
         wc[i] = ok ? (R)__ldg(wbase + o) : R(0);
       } else {
@@ -318,7 +310,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
       const R wn = wc[i];
       if (valid) {
         if (p.gam != nullptr) {   // GAm: the row's 27-node mean weights (A19)
-          gam_row<R, S>(p.gam, p.fstride, (long long)(pl + 2) * plane + loff + (i + 1) * nx, p.ih2, p.w2, cn[i].c1,
+          gam_row<R, S>(p.gam, p.fstride, (long long)(pl + 2) * plane + loff + (i + 1) * lx, p.ih2, p.w2, cn[i].c1,
                         cn[i].c2, cn[i].c3, cn[i].m1, cn[i].m2, cn[i].m3);
         } else {
         const R vv = rsqrt_r(wn);                           // w > 0 on valid rows
@@ -371,7 +363,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
       e1[i] = czv;
       e2[i] = czv;
       if (K > 0 && fin && (INTERIOR || ((rmask >> (i + 1)) & 1u))) {
-        const long long o = (long long)rhs * p.fstride + (unsigned)(loff + pl * plane + (i + 1) * nx);
+        const long long o = (long long)rhs * p.fstride + (unsigned)(loff + pl * plane + (i + 1) * lx);
         if (EPI != EPI_RESID || p.rhat != nullptr) e1[i] = to_cx(ldg_c(p.rhat + o), R(0));
         if (EPI == EPI_DOT4) e2[i] = to_cx(ldg_c(p.u + o), R(0));
         if (EPI == EPI_RESID) e2[i] = to_cx(ldg_c(p.bvec + o), R(0));
@@ -385,9 +377,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
       zp_prev = do_prev && (zg - 1 < zlo || zg - 1 > zhi);
       zp_cur = (pl >= zc0 && pl < zc1) && (zg < zlo || zg > zhi);
       zp_next = do_next && (zg + 1 < zlo || zg + 1 > zhi);
-#ifndef HZ_NO_PML
       zcorr = zp_prev || zp_cur || zp_next;
-#endif
     }
 
     // ---- in-plane x sums: X = u(x-1) + u(x+1), Xq = q(x-1) + q(x+1), q = u·w
@@ -502,7 +492,7 @@ __global__ void __launch_bounds__(32 * W, ApplyBounds<R>::MINB) apply27_v2(Apply
       mP[i] = mN[i];
       // ---- finalize output (row i, plane pl-1), epilogue
       if (do_prev && is_out && (INTERIOR || ((rmask >> (i + 1)) & 1u))) {
-        const long long o = (long long)rhs * p.fstride + (unsigned)(loff + pl * plane + (i + 1) * nx);
+        const long long o = (long long)rhs * p.fstride + (unsigned)(loff + pl * plane + (i + 1) * lx);
         if (EPI == EPI_RESID) {
           const C rr = csub(e2[i], a);
           p.au[o] = from_cx(rr, S(0));

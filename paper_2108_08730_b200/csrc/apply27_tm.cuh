@@ -1,0 +1,633 @@
+// K2 for complex64 (north-star steps a2–a6): tensor-map TMA plane tiles sliding in z, two x-points
+// per thread, RHS-fused.  DESIGN.md §5.
+//
+//   (Au)_n = ω² Σ_d μ_{|d|}(w_n) u_{n+d} / v²_{n+d}                        Eq. 8, A2, A4
+//          + Σ_a Σ_e D_a(n_a, e) Σ_{p,q} T(p,q; w_n) u_{n+e ê_a+p ê_b+q ê_c}   A6 (App. A), A8
+//   w_n = clamped linear interpolation of the Tikhonov weight table at G_n = v_n/(f h)  P:36, A13
+//
+// Design (HBM-bound: 4 + 16·nrhs bytes per point and apply):
+//  * Fields are [nrhs][nz+2][ny][ldx] with a 32-byte row pitch (ldx = nx rounded up to 4), so one
+//    3-D (w) and one 4-D (u: x, y, plane, RHS) tensor map describe them.  A CTA owns a tx × ty tile
+//    (tx a multiple of 4, ≤ 64, the same for every tile of the grid) for NR right-hand sides and marches
+//    a z-chunk.  Per input plane ONE thread issues one TMA box per field — the halo tile of w and of
+//    each RHS's u — into a ring of TM_STAGES shared-memory stages with one mbarrier each
+//    (expect_tx); coordinates outside the grid (x, y, and z where the map is trimmed to the slab's
+//    in-grid planes) are zero-filled by the TMA unit: the Dirichlet boundary (A9) costs no code.
+//  * A stage is refilled as soon as every warp has finished with it: warps 1..7 `bar.arrive` on the
+//    stage's named barrier, warp 0 `bar.sync`s on it and its lane 0 issues the next plane — no
+//    CTA-wide barrier per plane; fast warps run up to TM_STAGES − 2 planes ahead.
+//  * Thread (pair c, row r) computes the two points (x0 − 1 + 2c, x0 + 2c) of its row: per halo row it
+//    reads the four u columns 2c .. 2c+3 as two 16-byte shared loads and the four w as two 8-byte
+//    loads, and the x-neighbour / y-neighbour class sums come from registers:
+//    P0 = u, P1 = 4 in-plane faces, P2 = 4 in-plane corners, Q0..Q2 of q = u·w (Eq. 8), scattered into
+//    the partial outputs of planes k−1, k, k+1 (18 packed FFMA2 per point).  Row coefficients are
+//    built once per point and plane from w (one MUFU.RSQ, clamped linear interpolation of the table
+//    staged in shared memory) and shared by the NR fields; c0 and m0 follow from the sum rules.
+//  * PML: warp-uniform branches (the same per-axis A8 corrections as the complex128 kernel); a
+//    correction with δ = 0 adds exact zeros, so every point is computed with the same operation
+//    sequence whichever tile, chunk, launch or slab computes it (bitwise z-slab invariance).
+//  * Output: one 8-byte store per point; the pad columns [nx, ldx) are written as zeros.
+//  * Epilogues (BiCGSTAB dots): each thread's pair products in fp32, summed over planes in fp64, then
+//    an fp64 block and grid reduction in a fixed order (tm_reduce).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "apply27.cuh"
+
+namespace hz {
+
+constexpr int TM_NTHR = 256;     // threads per CTA
+constexpr int TM_STAGES = 5;     // shared-memory ring depth (planes in flight ≤ TM_STAGES)
+constexpr int TM_MAXTX = 64;     // widest tile
+
+// PML mode of a work item: 0 none, 1 z-PML planes only, 2 x/y-PML columns/rows (+ z)
+enum { TM_LEAN = 0, TM_PMLZ = 1, TM_PMLXY = 2 };
+
+// work item {x0 | y0 << 16, z0 | z1 << 16, mode, 0}: tile origin (x0, y0), local planes [z0, z1)
+__host__ __device__ inline int4 tm_item(int x0, int y0, int z0, int z1, int mode) {
+  return make_int4(x0 | (y0 << 16), z0 | (z1 << 16), mode, 0);
+}
+
+// tile geometry shared by host and device: box widths and stage sizes (bytes, 128-aligned)
+// A tile of tx ∈ {16, 32, 64} columns with origin X0 (a multiple of tx) computes the points
+// x ∈ [X0 − 1, X0 + tx − 1): pair c is (X0 − 1 + 2c, X0 + 2c).  The TMA unit needs the box's innermost
+// start coordinate 16-byte aligned (a misaligned start faults), so the u box starts at X0 − 2 and the
+// w box at X0 − 4 — and with the pair starting one column left of X0, a thread's four columns
+// x − 1 .. x + 2 sit at 16-byte (u) / 8-byte (w) aligned shared addresses: two vector loads each.  The
+// w box is widened to a row pitch ≡ 16 (mod 32) words so the two rows a half-warp reads hit disjoint
+// banks.  A warp covers 8 pairs × 4 rows (so only the warps holding x- or y-PML points take the PML
+// corrections), the 8 warps of a CTA tx/16 × 128/tx such blocks: ty = 512/tx rows.
+__host__ __device__ constexpr int tm_bxu(int tx) { return tx + 2; }
+__host__ __device__ constexpr int tm_bxw(int tx) { return ((tx + 4 + 15) / 32) * 32 + 16; }
+__host__ __device__ constexpr uint32_t tm_r128(uint32_t b) { return (b + 127u) & ~127u; }
+// bytes one box delivers (the mbarrier's transaction count) and its 128-byte aligned slot in a stage
+__host__ __device__ constexpr uint32_t tm_wbox(int tx, int ty) { return (uint32_t)tm_bxw(tx) * (ty + 2) * 4u; }
+__host__ __device__ constexpr uint32_t tm_ubox(int tx, int ty) { return (uint32_t)tm_bxu(tx) * (ty + 2) * 8u; }
+__host__ __device__ constexpr uint32_t tm_wbytes(int tx, int ty) { return tm_r128(tm_wbox(tx, ty)); }
+__host__ __device__ constexpr uint32_t tm_ubytes(int tx, int ty) { return tm_r128(tm_ubox(tx, ty)); }
+__host__ __device__ constexpr uint32_t tm_stage_bytes(int tx, int ty, int nr) { return tm_wbytes(tx, ty) + (uint32_t)nr * tm_ubytes(tx, ty); }
+__host__ __device__ constexpr uint32_t tm_tab_bytes(int tab_n) { return tm_r128((uint32_t)tab_n * 12u * 4u); }
+__host__ __device__ constexpr size_t tm_smem_bytes(int tab_n, int tx, int ty, int nr) {
+  return (size_t)tm_tab_bytes(tab_n) + 128 + (size_t)TM_STAGES * tm_stage_bytes(tx, ty, nr);
+}
+// rows per CTA for a tile width tx: TM_NTHR threads of tx/2 column pairs per row
+__host__ __device__ constexpr int tm_rows(int tx) { return TM_NTHR / (tx / 2); }
+
+// ---- TMA / mbarrier / named-barrier primitives (PTX) -------------------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// Wait for the phase with the given parity to complete.  A transfer that never completes (a
+// programming error) traps after ~2^30 polls instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t n = 0;; n++) {
+    asm volatile(
+        "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (n > (1u << 30)) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void bar_sync_n(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(TM_NTHR) : "memory"); }
+__device__ __forceinline__ void bar_arrive_n(int id) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(TM_NTHR) : "memory"); }
+
+// conj(a)·b of complex64 data in fp32 (a thread's pair of points; the sums over planes, threads, blocks
+// and the grid are fp64)
+__device__ __forceinline__ void tm_cdot(float& re, float& im, float2 a, float2 b) {
+  re = fmaf(a.x, b.x, fmaf(a.y, b.y, re));
+  im = fmaf(a.x, b.y, fmaf(-a.y, b.x, im));
+}
+__device__ __forceinline__ void tm_norm(float& s, float2 a) { s = fmaf(a.x, a.x, fmaf(a.y, a.y, s)); }
+
+// complex multiply-add with a per-thread constant d (PML δ): acc + d·b as two packed FMAs,
+// dn = (−d.y, d.y) precomputed once
+__device__ __forceinline__ float2 zfma_c(float2 d, float2 dn, float2 b, float2 acc) {
+  acc = pk_fma(make_float2(d.x, d.x), b, acc);
+  return pk_fma(dn, make_float2(b.y, b.x), acc);
+}
+__device__ __forceinline__ float2 zneg_sw(float2 d) { return make_float2(-d.y, d.y); }
+
+// Dot epilogue reduction of one CTA for its NR right-hand sides (all K values at once, fixed order):
+// warp shuffles (fp64) → per-warp sums in shared memory → one thread per (RHS, value) writes the
+// block's partial; the last CTA of the RHS group (ticket of the group's first RHS) reduces the
+// partials of all CTAs with one warp per (RHS, value): lanes stride the blocks, then a shuffle tree.
+template <int NR, int K, int NT>
+__device__ __forceinline__ void tm_reduce(const double (&part)[NR][K], const bool (&act)[NR], const ApplyParams<float, float>& p,
+                                          int rhs0, int slot) {
+  constexpr int NWARP = NT / 32;
+  __shared__ double red[NWARP][NR * K];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblocks = p.tm_nblocks;
+#pragma unroll
+  for (int r = 0; r < NR; r++)
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      double v = part[r][k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][r * K + k] = v;
+    }
+  __syncthreads();
+  if (threadIdx.x < NR * K) {
+    const int r = threadIdx.x / K, k = threadIdx.x - r * K;
+    if (act[r]) {
+      double v = 0.0;
+      for (int w = 0; w < NWARP; w++) v += red[w][threadIdx.x];
+      p.partials[((long long)(rhs0 + r) * nblocks + slot) * K + k] = v;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(p.tickets + rhs0, 1u) == (unsigned)nblocks - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int q = warp; q < NR * K; q += NWARP) {
+    const int r = q / K, k = q - r * K;
+    if (!act[r]) continue;
+    const volatile double* pp = p.partials + (long long)(rhs0 + r) * nblocks * K + k;
+    double v = 0.0;
+    for (int b = lane; b < nblocks; b += 32) v += pp[(long long)b * K];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) p.dots[(long long)(rhs0 + r) * K + k] = v;
+  }
+  if (threadIdx.x == 0) p.tickets[rhs0] = 0u;
+}
+
+// One work item: tile (x0, y0) of tx × ty points, local output planes [zc0, zc1), NR RHS.  One row
+// per thread (its points (x, y) and (x+1, y)): halo rows b = y−1, c = y, a = y+1.
+template <int NR, bool COLLOC, int EPI, int PM, bool GAM>
+__device__ __forceinline__ void tm_body(const CUtensorMap* tmw, const CUtensorMap* tmu, const ApplyParams<float, float>& p,
+                                        const int4 item, int slot) {
+  typedef float R;
+  typedef float2 C;
+  constexpr bool PML = PM != TM_LEAN;
+  constexpr bool PXY = PM == TM_PMLXY;
+  constexpr int K = epi_k(EPI);
+  constexpr int S = TM_STAGES;
+  const unsigned FULL = 0xffffffffu;
+
+  // ---- block → (work item, RHS group)
+  const int rhs0 = blockIdx.y * NR;
+  bool act[NR];
+  bool any = false;
+#pragma unroll
+  for (int r = 0; r < NR; r++) {
+    act[r] = rhs0 + r < p.nrhs && (p.active == nullptr || p.active[rhs0 + r] != 0);
+    any = any || act[r];
+  }
+  if (!any) return;   // uniform per CTA
+
+  const int nx = p.nx, ny = p.ny, ldx = p.ldx;
+  const int tx = p.tm_tx, ty = p.tm_ty;
+  const int X0 = item.x & 0xffff, Y0 = item.x >> 16;
+  const int zc0 = item.y & 0xffff, zc1 = item.y >> 16;
+  const int nplanes = zc1 - zc0 + 2;   // input planes zc0-1 .. zc1
+  const int plane = (int)p.plane;      // host: (nzl + 2)·plane < 2^31 (32-bit offsets within a field)
+  const int bxu = tm_bxu(tx), bxw = tm_bxw(tx);
+
+  extern __shared__ __align__(1024) unsigned char smem_tm[];
+  float* stab = reinterpret_cast<float*>(smem_tm);
+  const uint32_t tabB = tm_tab_bytes(p.tab_n);
+  const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(smem_tm + tabB);
+  unsigned char* ring = smem_tm + tabB + 128;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint32_t wB = tm_wbytes(tx, ty), uB = tm_ubytes(tx, ty);
+  const uint32_t stB = wB + (uint32_t)NR * uB;
+  uint32_t txB = tm_wbox(tx, ty);   // transaction bytes per plane: the boxes exactly, not their slots
+#pragma unroll
+  for (int r = 0; r < NR; r++)
+    if (act[r]) txB += tm_ubox(tx, ty);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // producer: plane j → stage j % S (coordinates: storage plane − the map's first plane)
+  auto issue = [&](int j) {
+    const int st = j % S;
+    const uint32_t bar = mbar0 + 8u * st;
+    const uint32_t dst = ring_s + (uint32_t)st * stB;
+    const int c2 = zc0 + j - p.tm_org;   // storage plane zc0 - 1 + j + 1
+    mbar_expect_tx(bar, txB);
+    tma_load3(dst, tmw, bar, X0 - 4, Y0 - 1, c2);
+#pragma unroll
+    for (int r = 0; r < NR; r++)
+      if (act[r]) tma_load4(dst + wB + (uint32_t)r * uB, tmu, bar, X0 - 2, Y0 - 1, c2, rhs0 + r);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < S; s++) mbar_init(mbar0 + 8u * s, 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int j = 0; j < S && j < nplanes; j++) issue(j);
+  }
+  // stage the coefficient table while the first planes stream in
+  for (int e = tid; e < p.tab_n * CTAB_STRIDE; e += TM_NTHR) stab[e] = p.ctab[(long long)p.tab_lo * CTAB_STRIDE + e];
+  __syncthreads();
+
+  // ---- this thread's points: columns x = X0 − 1 + 2c and x + 1 of row y; warp w covers pairs
+  // 8·(w mod WX) + 0..7 of rows 4·(w / WX) + 0..3 (WX = tx/16 warp columns)
+  const int wx = tx >> 4;
+  const bool pos_ok = true;
+  const int rg = 4 * (warp / wx) + (lane >> 3), c_ = 8 * (warp % wx) + (lane & 7);
+  const int x = X0 - 1 + 2 * c_;
+  const int y = Y0 + rg;
+  const bool yok = pos_ok && y < ny;
+  // a point is stored if it lies in the pitched row (a pad column gets a zero), computed if in the grid
+  const bool sto[2] = {yok && x >= 0 && x < ldx, yok && x + 1 < ldx};
+  const bool in_[2] = {sto[0] && x < nx, sto[1] && x + 1 < nx};
+  const bool st_ = sto[0] || sto[1];
+  const int sbw = rg * bxw + 2 * c_ + 2;   // stage element (row y-1, column x-1) in the w box
+  const int sbu = rg * bxu + 2 * c_;       // ... in a u box
+
+  // PML: warp-uniform flags for x-PML columns / y-PML rows among the warp's points; the deltas
+  // δ± = a± − h⁻² are read from the (L1-resident) 1-D arrays where they are used
+  bool gen_x = false, gen_y = false;
+  const C z2 = make_float2(0.f, 0.f);
+  const int xe0 = min(max(x, 0), nx - 1), xe1 = min(x + 1, nx - 1), ye = min(y, ny - 1);
+  if (PXY) {
+    bool xp = false;
+#pragma unroll
+    for (int e = 0; e < 2; e++) xp = xp || (in_[e] && (x + e < p.lo[0] || x + e > p.hi[0]));
+    const bool yp = pos_ok && y < ny && (y < p.lo[1] || y > p.hi[1]);
+    gen_x = __any_sync(FULL, xp);
+    gen_y = __any_sync(FULL, yp);
+  }
+  const bool gen_col = gen_x || gen_y;
+  (void)st_;
+  const int zlo = p.lo[2], zhi = p.hi[2];
+
+  constexpr int SP = SmemPitch<R>::V;
+  const R s_k1 = p.inv_fh * p.inv_dg, s_k0 = -p.g_min * p.inv_dg, s_max = (R)(p.n_g - 1);
+  const R w2 = p.w2;
+  const R i3h = p.inv3ih2, i2h = p.inv2ih2, i1h = p.invih2;
+  auto c0_of = [](const Coef6<R>& c) { return -fma(R(6), c.c1, fma(R(12), c.c2, R(8) * c.c3)); };
+  auto m0_of = [&](const Coef6<R>& c, R m0s) { return fma(w2, m0s, -fma(R(6), c.m1, fma(R(12), c.m2, R(8) * c.m3))); };
+
+  double part[NR][K > 0 ? K : 1];
+#pragma unroll
+  for (int r = 0; r < NR; r++)
+#pragma unroll
+    for (int k = 0; k < (K > 0 ? K : 1); k++) part[r][k] = 0.0;
+
+  // output element (row y, column x) in storage plane 0 of the group's first RHS: + pl·plane (x ≥ −1:
+  // element −1 of row 0 is only formed for a point that is never stored)
+  const uint32_t fs = (uint32_t)p.fstride;
+  const uint32_t orow = (uint32_t)(y * ldx + x);
+  R gpf[2][5];   // GAm / record: the 5 weights of this thread's points of the next coefficient plane
+  auto gam_load = [&](int splane) {
+    const uint32_t e = (uint32_t)(splane * plane) + orow;   // 32-bit: wraps back for x = −1 (orow = −1 + y·ldx)
+#pragma unroll
+    for (int k = 0; k < 5; k++)
+#pragma unroll
+      for (int q = 0; q < 2; q++) gpf[q][k] = in_[q] ? __ldg(p.gam + k * p.fstride + (e + (uint32_t)q)) : R(0);
+  };
+  if (GAM) gam_load(zc0 + 1);   // rows of output plane zc0 (storage zc0 + 1), used by call j = 0
+  const float2* __restrict__ rh0 = p.rhat + (long long)rhs0 * p.fstride;
+  float2* __restrict__ au0 = p.au + (long long)rhs0 * p.fstride;
+
+  // One input plane j (local pl = zc0-1+j).  Three register slots per quantity rotate through the
+  // roles prev (output pl-1) / cur (output pl) / next (output pl+1) over three consecutive calls:
+  // cX = coefficients (+ m0 scale), aX = partial sums, sX = centre u (DOT4's s).
+  auto body = [&](Coef6<R> (&cP)[2], Coef6<R> (&cC)[2], Coef6<R> (&cN)[2], R (&mP)[2], R (&mC)[2], R (&mN)[2],
+                  C (&aP)[NR][2], C (&aC)[NR][2], C (&aN)[NR][2], C (&sP)[NR][2], C (&sC)[NR][2], int j) {
+    const int pl = zc0 - 1 + j;
+    const bool do_prev = (pl - 1 >= zc0);
+    const bool do_next = (pl + 1 < zc1);
+    const int oplane = pl * plane;   // storage plane pl = local output plane pl-1
+    // epilogue operand r̂0 of the outputs finalised here (plane pl-1), loaded before the wait
+    C e1[NR][2];
+#pragma unroll
+    for (int r = 0; r < NR; r++)
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        e1[r][q] = z2;
+        if (K > 0 && act[r] && do_prev && in_[q]) e1[r][q] = __ldg(rh0 + ((uint32_t)r * fs + orow + (uint32_t)(oplane + q)));
+      }
+    mbar_wait(mbar0 + 8u * (j % S), (uint32_t)(j / S) & 1u);
+    if (j + 1 < nplanes) mbar_wait(mbar0 + 8u * ((j + 1) % S), (uint32_t)((j + 1) / S) & 1u);
+
+    const unsigned char* st = ring + (size_t)(j % S) * stB;
+    const float* sw = reinterpret_cast<const float*>(st) + sbw;
+    const int zg = p.z0 + pl;
+    bool zp_prev = false, zp_cur = false, zp_next = false, zcorr = false;
+    if (PML) {
+      zp_prev = do_prev && (zg - 1 < zlo || zg - 1 > zhi);
+      zp_cur = (pl >= zc0 && pl < zc1) && (zg < zlo || zg > zhi);
+      zp_next = do_next && (zg + 1 < zlo || zg + 1 > zhi);
+      zcorr = zp_prev || zp_cur || zp_next;
+    }
+    // ---- coefficients of the output points of plane pl+1 (w from the next stage) into the free slot
+    {
+      const float* swn = reinterpret_cast<const float*>(ring + (size_t)((j + 1) % S) * stB) + sbw + bxw;
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const R wn = do_next ? swn[1 + e] : R(1);
+        if (GAM) {   // GAm: the row's 27-node mean weights (A19), prefetched one plane ahead
+          if (do_next) {
+            const R t1 = gpf[e][0], t2 = gpf[e][1], mu0 = gpf[e][2], mu1 = gpf[e][3], mu2 = gpf[e][4];
+            const R t0 = R(1) - R(4) * (t1 + t2);
+            cN[e].c1 = p.ih2 * (t0 - R(4) * t1);
+            cN[e].c2 = p.ih2 * (R(2) * (t1 - t2));
+            cN[e].c3 = p.ih2 * (R(3) * t2);
+            cN[e].m1 = w2 * mu1;
+            cN[e].m2 = w2 * mu2;
+            cN[e].m3 = w2 * ((R(1) - mu0 - R(6) * mu1 - R(12) * mu2) * R(0.125));
+          } else {
+            cN[e] = Coef6<R>{R(0), R(0), R(0), R(0), R(0), R(0)};
+          }
+        } else {
+          // a2 + a3: G = 1/(√w f h) → clamped table index → linear interpolation (A13)
+          const R vv = rsqrt_r(fmax(wn, R(1e-30)));
+          R sidx = fma(vv, s_k1, s_k0);
+          sidx = fmin(fmax(sidx, R(0)), s_max);
+          const int ii = min((int)sidx, p.n_g - 2);
+          const R tau = sidx - (R)ii;
+          const int li = min(max(ii - p.tab_lo, 0), p.tab_n - 2);
+          const R* row = stab + li * SP;
+          const float4 ta = lds4<R>(row), tb = lds4<R>(row + 4), td = lds4<R>(row + 8);
+          cN[e].c1 = fma(tau, tb.z, ta.x);
+          cN[e].c2 = fma(tau, tb.w, ta.y);
+          cN[e].c3 = fma(tau, td.x, ta.z);
+          cN[e].m1 = fma(tau, td.y, ta.w);
+          cN[e].m2 = fma(tau, td.z, tb.x);
+          cN[e].m3 = fma(tau, td.w, tb.y);
+        }
+        if (COLLOC) {
+          cN[e].m1 *= wn;
+          cN[e].m2 *= wn;
+          cN[e].m3 *= wn;
+        }
+        mN[e] = COLLOC ? wn : R(1);
+      }
+      if (GAM && pl + 2 < zc1) gam_load(pl + 3);   // the next call's rows
+    }
+    C dzp = z2, dzc = z2, dzn = z2;
+    if (PML && zcorr) {
+      if (zp_prev) dzp = p.dp[2][zg - 1];
+      if (zp_cur) {
+        const C dz = cadd(p.dm[2][zg], p.dp[2][zg]);
+        dzc = make_cx(-dz.x, -dz.y);
+      }
+      if (zp_next) dzn = p.dm[2][zg + 1];
+    }
+
+    // ---- per RHS: in-plane class sums of the two points, accumulated halo row by halo row:
+    // P0 = u0, P1 = 4 faces (x-neighbours in the centre row + centre column of the rows below /
+    // above), P2 = 4 corners, Q0..Q2 of q = u·w (Eq. 8).  Rows in the order below, centre, above; the
+    // x/y-PML body takes the centre row first so that the stretched parts ΔL1 = δx(u) + δy(u),
+    // ΔL2 = δx(Y) + δy(X) (A8) accumulate from each row directly (a tile is always computed by the
+    // same body, so each point's operation sequence is fixed).
+    float Wall[3][4];   // w of the three halo rows (loaded once per plane for NR = 2)
+    auto load_w = [&](int k, float (&Wr)[4]) {
+      const float2 wa = *reinterpret_cast<const float2*>(sw + k * bxw);
+      const float2 wb = *reinterpret_cast<const float2*>(sw + k * bxw + 2);
+      Wr[0] = wa.x;
+      Wr[1] = wa.y;
+      Wr[2] = wb.x;
+      Wr[3] = wb.y;
+    };
+    if (!COLLOC && NR > 1) {
+#pragma unroll
+      for (int k = 0; k < 3; k++) load_w(k, Wall[k]);
+    }
+#pragma unroll
+    for (int r = 0; r < NR; r++) {
+      if (!act[r]) continue;
+      const C* su0 = reinterpret_cast<const C*>(st + wB + (size_t)r * uB) + sbu;
+      C u0[2], P1[2], P2[2], Q0[2], Q1[2], Q2[2], L1[2], L2[2], Xc[2];
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        const int k = PXY ? (kk == 0 ? 1 : (kk == 1 ? 0 : 2)) : kk;   // halo row: 0 below, 1 centre, 2 above
+        float Wr[4];
+        if (!COLLOC) {
+          if (NR > 1) {
+#pragma unroll
+            for (int m = 0; m < 4; m++) Wr[m] = Wall[k][m];
+          } else {
+            load_w(k, Wr);
+          }
+        }
+        const C* su = su0 + k * bxu;
+        const float4 A4 = *reinterpret_cast<const float4*>(su);
+        const float4 B4 = *reinterpret_cast<const float4*>(su + 2);
+        const C U[4] = {make_float2(A4.x, A4.y), make_float2(A4.z, A4.w), make_float2(B4.x, B4.y), make_float2(B4.z, B4.w)};
+        C q[4];
+        if (!COLLOC) {
+#pragma unroll
+          for (int m = 0; m < 4; m++) q[m] = cscale(Wr[m], U[m]);
+        }
+        const bool first = kk == 0;
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const C X = cadd(U[e], U[e + 2]);
+          const C Xq = COLLOC ? z2 : cadd(q[e], q[e + 2]);
+          if (k == 1) {   // centre row: the centre, 2 faces (x-neighbours)
+            u0[e] = U[e + 1];
+            P1[e] = first ? X : cadd(P1[e], X);
+            if (!COLLOC) {
+              Q0[e] = q[e + 1];
+              Q1[e] = first ? Xq : cadd(Q1[e], Xq);
+            }
+            if (PXY && gen_col) {
+              Xc[e] = X;
+              L1[e] = z2;
+              L2[e] = z2;
+              if (gen_x) {   // δx(u)
+                const C dm = __ldg(p.dm[0] + (e ? xe1 : xe0)), dp = __ldg(p.dp[0] + (e ? xe1 : xe0));
+                L1[e] = zfma_c(dm, zneg_sw(dm), csub(U[e], U[e + 1]), L1[e]);
+                L1[e] = zfma_c(dp, zneg_sw(dp), csub(U[e + 2], U[e + 1]), L1[e]);
+              }
+            }
+          } else {   // row below / above: a face (centre column), 2 corners (x-neighbours)
+            P1[e] = first ? U[e + 1] : cadd(P1[e], U[e + 1]);
+            P2[e] = k == 0 ? X : cadd(P2[e], X);   // row below: the first side row in both orders
+            if (!COLLOC) {
+              Q1[e] = first ? q[e + 1] : cadd(Q1[e], q[e + 1]);
+              Q2[e] = k == 0 ? Xq : cadd(Q2[e], Xq);
+            }
+            if (PXY && gen_col) {
+              if (gen_x) {   // δx(Y): this row's part
+                const C dm = __ldg(p.dm[0] + (e ? xe1 : xe0)), dp = __ldg(p.dp[0] + (e ? xe1 : xe0));
+                L2[e] = zfma_c(dm, zneg_sw(dm), csub(U[e], U[e + 1]), L2[e]);
+                L2[e] = zfma_c(dp, zneg_sw(dp), csub(U[e + 2], U[e + 1]), L2[e]);
+              }
+              if (gen_y) {   // δy(u), δy(X): this row's part
+                const C d = __ldg((k == 0 ? p.dm[1] : p.dp[1]) + ye);
+                L1[e] = zfma_c(d, zneg_sw(d), csub(U[e + 1], u0[e]), L1[e]);
+                L2[e] = zfma_c(d, zneg_sw(d), csub(X, Xc[e]), L2[e]);
+              }
+            }
+          }
+        }
+      }
+
+      C outv[2];
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const C c0u = u0[e];
+        const C p1 = P1[e], p2 = P2[e];
+        const C q0 = COLLOC ? c0u : Q0[e];
+        const C q1 = COLLOC ? p1 : Q1[e];
+        const C q2 = COLLOC ? p2 : Q2[e];
+        const Coef6<R>& cp = cP[e];
+        const Coef6<R>& cc = cC[e];
+        const Coef6<R>& cn = cN[e];
+        C a = aP[r][e];
+        a = cfma(cp.c1, c0u, a);
+        a = cfma(cp.c2, p1, a);
+        a = cfma(cp.c3, p2, a);
+        a = cfma(cp.m1, q0, a);
+        a = cfma(cp.m2, q1, a);
+        a = cfma(cp.m3, q2, a);
+        C b = aC[r][e];
+        b = cfma(c0_of(cc), c0u, b);
+        b = cfma(cc.c1, p1, b);
+        b = cfma(cc.c2, p2, b);
+        b = cfma(m0_of(cc, mC[e]), q0, b);
+        b = cfma(cc.m1, q1, b);
+        b = cfma(cc.m2, q2, b);
+        C c = cscale(cn.c1, c0u);
+        c = cfma(cn.c2, p1, c);
+        c = cfma(cn.c3, p2, c);
+        c = cfma(cn.m1, q0, c);
+        c = cfma(cn.m2, q1, c);
+        c = cfma(cn.m3, q2, c);
+        if (PML && ((PXY && gen_col) || zcorr)) {
+          // PML transverse weights of the three output rows (t2 = c3 h²/3, t1 = t2 + c2 h²/2, t0 = c1 h² + 4 t1)
+          const R pt2 = cp.c3 * i3h, pt1 = fma(cp.c2, i2h, pt2);
+          const R ct2 = cc.c3 * i3h, ct1 = fma(cc.c2, i2h, ct2), ct0 = fma(cc.c1, i1h, R(4) * ct1);
+          const R nt2 = cn.c3 * i3h, nt1 = fma(cn.c2, i2h, nt2);
+          if (PXY && gen_col) {   // t1 ΔL1 + t2 ΔL2 (planes ±1), t0 ΔL1 + t1 ΔL2 (own plane)
+            a = cfma(pt1, L1[e], a);
+            a = cfma(pt2, L2[e], a);
+            b = cfma(ct0, L1[e], b);
+            b = cfma(ct1, L2[e], b);
+            c = cfma(nt1, L1[e], c);
+            c = cfma(nt2, L2[e], c);
+          }
+          if (zcorr) {   // δz · (t0 P0 + t1 P1 + t2 P2) of each output plane
+            if (zp_prev) {
+              C B3 = cscale(fma(cp.c1, i1h, R(4) * pt1), c0u);
+              B3 = cfma(pt1, p1, B3);
+              B3 = cfma(pt2, p2, B3);
+              a = zfma_c(dzp, zneg_sw(dzp), B3, a);
+            }
+            if (zp_cur) {
+              C B3 = cscale(ct0, c0u);
+              B3 = cfma(ct1, p1, B3);
+              B3 = cfma(ct2, p2, B3);
+              b = zfma_c(dzc, zneg_sw(dzc), B3, b);
+            }
+            if (zp_next) {
+              C B3 = cscale(fma(cn.c1, i1h, R(4) * nt1), c0u);
+              B3 = cfma(nt1, p1, B3);
+              B3 = cfma(nt2, p2, B3);
+              c = zfma_c(dzn, zneg_sw(dzn), B3, c);
+            }
+          }
+        }
+        aC[r][e] = b;   // output pl: "prev" of the next call
+        aN[r][e] = c;   // output pl+1: "cur" of the next call (a's slot is free after this call)
+        outv[e] = in_[e] ? a : z2;
+      }
+      // ---- outputs of plane pl-1, then the dot epilogue
+      if (do_prev) {
+#pragma unroll
+        for (int e = 0; e < 2; e++)
+          if (sto[e]) au0[(uint32_t)r * fs + orow + (uint32_t)(oplane + e)] = outv[e];
+      }
+      if (EPI != EPI_PLAIN) {
+        // the pair's products in fp32 (the same operations whichever tile / chunk / slab computes the
+        // pair), accumulated per thread in fp64: the dot products then depend on the decomposition only
+        // at the 1e-16 level
+        float pp[K > 0 ? K : 1];
+#pragma unroll
+        for (int k = 0; k < (K > 0 ? K : 1); k++) pp[k] = 0.f;
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const C a = do_prev ? outv[e] : z2;
+          const C rh = e1[r][e];
+          if (EPI == EPI_DOT1) {
+            tm_cdot(pp[0], pp[1], rh, a);
+          } else if (EPI == EPI_DOT4) {
+            const C sv = (do_prev && in_[e]) ? sP[r][e] : z2;
+            tm_cdot(pp[0], pp[1], a, sv);
+            tm_norm(pp[2], a);
+            tm_cdot(pp[3], pp[4], rh, sv);
+            tm_cdot(pp[5], pp[6], rh, a);
+            sC[r][e] = u0[e];   // s of output pl: "prev" s of the next call
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < (K > 0 ? K : 1); k++) part[r][k] += (double)pp[k];
+      }
+    }
+    // ---- release this plane's stage: warp 0 waits for every warp, then its lane 0 refills it
+    if (warp == 0) {
+      bar_sync_n(1 + j % S);
+      if (lane == 0 && j + S < nplanes) issue(j + S);
+    } else {
+      bar_arrive_n(1 + j % S);
+    }
+  };
+
+  Coef6<R> cs0[2], cs1[2], cs2[2];
+  R ms0[2], ms1[2], ms2[2];
+  C as0[NR][2], as1[NR][2], as2[NR][2], ss0[NR][2], ss1[NR][2], ss2[NR][2];
+#pragma unroll
+  for (int e = 0; e < 2; e++) {
+    cs0[e] = cs1[e] = cs2[e] = Coef6<R>{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    ms0[e] = ms1[e] = ms2[e] = 0.f;
+#pragma unroll
+    for (int r = 0; r < NR; r++) as0[r][e] = as1[r][e] = as2[r][e] = ss0[r][e] = ss1[r][e] = ss2[r][e] = z2;
+  }
+  // roles (prev, cur, next) = (0,1,2), (1,2,0), (2,0,1); the s slots (prev, cur) rotate likewise
+  for (int j = 0; j < nplanes; j += 3) {
+    body(cs0, cs1, cs2, ms0, ms1, ms2, as0, as1, as2, ss0, ss1, j);
+    if (j + 1 >= nplanes) break;
+    body(cs1, cs2, cs0, ms1, ms2, ms0, as1, as2, as0, ss1, ss2, j + 1);
+    if (j + 2 >= nplanes) break;
+    body(cs2, cs0, cs1, ms2, ms0, ms1, as2, as0, as1, ss2, ss0, j + 2);
+  }
+
+  if constexpr (K > 0) tm_reduce<NR, K, TM_NTHR>(part, act, p, rhs0, slot);
+}
+
+// One launch for every tile class: the work item's mode selects the x/y-PML body, the body with the
+// plane-uniform z corrections (chunks touching the z-PML) or the PML-free body, so CTAs of all classes
+// share the GPU; x/y-PML items come first (heavier, scheduled first).
+// GAM: rows read their stored weights (GAm 27-node means, A19, or the GA record) instead of
+// interpolating the table.
+template <int NR, bool COLLOC, int EPI, bool GAM>
+__global__ void __launch_bounds__(TM_NTHR, 2)
+    apply27_tm(const __grid_constant__ CUtensorMap tmw, const __grid_constant__ CUtensorMap tmu, ApplyParams<float, float> p) {
+  const int4 item = p.tm_work[blockIdx.x];
+  if (item.z == TM_PMLXY)
+    tm_body<NR, COLLOC, EPI, TM_PMLXY, GAM>(&tmw, &tmu, p, item, blockIdx.x);
+  else if (item.z == TM_PMLZ)
+    tm_body<NR, COLLOC, EPI, TM_PMLZ, GAM>(&tmw, &tmu, p, item, blockIdx.x);
+  else
+    tm_body<NR, COLLOC, EPI, TM_LEAN, GAM>(&tmw, &tmu, p, item, blockIdx.x);
+}
+
+}  // namespace hz

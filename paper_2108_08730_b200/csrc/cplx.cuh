@@ -17,7 +17,6 @@ __device__ __forceinline__ float2 u64_as_f2(unsigned long long a) {
 }
 
 // ---- float2 (complex64) ---------------------------------------------------------------------
-#ifndef HZ_SCALAR_CPLX
 // Packed FP32x2 (FFMA2): every op is an fma.rn.f32x2 (a+b = 1·a+b, s·a = s·a+0), so no compiler
 // mul/add contraction choice can make two unrolled copies round differently.
 __device__ __forceinline__ float2 pk_fma(float2 a, float2 b, float2 c) {
@@ -29,17 +28,6 @@ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return pk_fma(make_
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return pk_fma(make_float2(-1.f, -1.f), b, a); }
 __device__ __forceinline__ float2 cscale(float s, float2 a) { return pk_fma(make_float2(s, s), a, make_float2(0.f, 0.f)); }
 __device__ __forceinline__ float2 cfma(float s, float2 a, float2 acc) { return pk_fma(make_float2(s, s), a, acc); }
-#else
-// Scalar IEEE ops with explicit rounding (ptxas pairs them into FFMA2/FADD2/FMUL2 where it can).  An
-// inline-PTX fma.rn.f32x2 version was measured equally fast but gave 1-ulp differences between
-// unrolled copies of the apply body, breaking bitwise z-slab decomposition invariance.
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y)); }
-__device__ __forceinline__ float2 cscale(float s, float2 a) { return make_float2(__fmul_rn(s, a.x), __fmul_rn(s, a.y)); }
-__device__ __forceinline__ float2 cfma(float s, float2 a, float2 acc) {
-  return make_float2(__fmaf_rn(s, a.x, acc.x), __fmaf_rn(s, a.y, acc.y));
-}
-#endif
 // complex * complex (slow paths only)
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);

@@ -9,11 +9,21 @@
 
 #include "apply.cuh"
 #include "apply27.cuh"
-#include "apply27_tma.cuh"
-#include "apply27_cp.cuh"
+#include "apply27_tm.cuh"
 #include "kernels.h"
 
 namespace hz {
+
+// storage element (halo plane 0 first, row pitch ldx) of owned point idx = (zl·ny + y)·nx + x
+template <typename R, typename S>
+__device__ __forceinline__ long long st_elem(const ApplyParams<R, S>& p, long long idx, int& zl, int& y, int& x) {
+  const long long pl = (long long)p.nx * p.ny;
+  zl = (int)(idx / pl);
+  const int rem = (int)(idx - (long long)zl * pl);
+  y = rem / p.nx;
+  x = rem - y * p.nx;
+  return (long long)(zl + 1) * p.plane + (long long)y * p.ldx + x;
+}
 
 // =============================================================================================
 // K1 record export: (k², t0, t1, t2, μ0, μ1, μ2, μ3) per point
@@ -24,12 +34,13 @@ __global__ void record_kernel(ApplyParams<R> p, R w2_over_1, R* __restrict__ rec
   R* tab = reinterpret_cast<R*>(smem_raw);
   for (int i = threadIdx.x; i < p.n_g * TAB_STRIDE; i += blockDim.x) tab[i] = p.tab[i];
   __syncthreads();
-  const long long n = (long long)p.nzl * p.plane;
+  const long long n = (long long)p.nzl * p.ny * p.nx;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long long)gridDim.x * blockDim.x) {
-    const R v = p.v[p.plane + idx];
+    int zl, y, x;
+    const long long e = st_elem(p, idx, zl, y, x);
+    const R v = p.v[e];
     R t1, t2, mu0, mu1, mu2;
     if (p.gam != nullptr) {   // GAm: the row's 27-node mean weights (A19)
-      const long long e = p.plane + idx;
       t1 = p.gam[e], t2 = p.gam[p.fstride + e], mu0 = p.gam[2 * p.fstride + e];
       mu1 = p.gam[3 * p.fstride + e], mu2 = p.gam[4 * p.fstride + e];
     } else {
@@ -49,7 +60,7 @@ __global__ void record_kernel(ApplyParams<R> p, R w2_over_1, R* __restrict__ rec
 // =============================================================================================
 // GAm rule (reading A19): per owned point, the mean of the interpolated free weights
 // (t1, t2, μ0, μ1, μ2) over the in-grid nodes of its 27-point stencil (v halo planes carry the
-// neighbouring slabs).  One-time, at assemble; out: [5][nzl+2][ny][nx] (halo planes not written).
+// neighbouring slabs).  One-time, at assemble; out: [5][nzl+2][ny][ldx] (halo planes not written).
 // radius 0 stores the row's own weights: the "record mode" of the GA rule.
 // =============================================================================================
 template <typename R>
@@ -58,11 +69,10 @@ __global__ void gam_field_kernel(ApplyParams<R> p, R* __restrict__ out, int radi
   R* tab = reinterpret_cast<R*>(smem_raw);
   for (int i = threadIdx.x; i < p.n_g * TAB_STRIDE; i += blockDim.x) tab[i] = p.tab[i];
   __syncthreads();
-  const long long n = (long long)p.nzl * p.plane;
+  const long long n = (long long)p.nzl * p.ny * p.nx;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long long)gridDim.x * blockDim.x) {
-    const int zl = (int)(idx / p.plane);
-    const int rem = (int)(idx - (long long)zl * p.plane);
-    const int y = rem / p.nx, x = rem - y * p.nx;
+    int zl, y, x;
+    const long long e = st_elem(p, idx, zl, y, x);
     R a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
     int cnt = 0;
     for (int dz = -radius; dz <= radius; dz++) {
@@ -73,7 +83,7 @@ __global__ void gam_field_kernel(ApplyParams<R> p, R* __restrict__ out, int radi
         for (int dx = -radius; dx <= radius; dx++) {
           if (x + dx < 0 || x + dx >= p.nx) continue;
           R t1, t2, mu0, mu1, mu2;
-          interp_weights<R>(p.v[(long long)(zl + 1 + dz) * p.plane + (long long)(y + dy) * p.nx + (x + dx)], tab, p.n_g,
+          interp_weights<R>(p.v[e + (long long)dz * p.plane + (long long)dy * p.ldx + dx], tab, p.n_g,
                             p.g_min, p.g_max, p.inv_dg, p.inv_fh, t1, t2, mu0, mu1, mu2);
           a0 += t1;
           a1 += t2;
@@ -85,7 +95,6 @@ __global__ void gam_field_kernel(ApplyParams<R> p, R* __restrict__ out, int radi
       }
     }
     const R ic = R(1) / (R)cnt;
-    const long long e = p.plane + idx;
     out[e] = a0 * ic;
     out[p.fstride + e] = a1 * ic;
     out[2 * p.fstride + e] = a2 * ic;
@@ -114,11 +123,11 @@ __global__ void sources_kernel(ApplyParams<R> p, int nsrc, const long long* __re
   const long long X = nodes[3 * s] + dx, Y = nodes[3 * s + 1] + dy, Z = nodes[3 * s + 2] + dz;
   if (X < 0 || X >= p.nx || Y < 0 || Y >= p.ny || Z < p.z0 || Z >= (long long)p.z0 + p.nzl) return;
   const int zl = (int)(Z - p.z0);
-  const long long o = (long long)s * p.fstride + (long long)(zl + 1) * p.plane + Y * p.nx + X;
+  const long long o = (long long)s * p.fstride + (long long)(zl + 1) * p.plane + Y * p.ldx + X;
   R w = ih3;
   if (consistent) {
     R t1, t2, mu0, mu1, mu2;
-    const long long e = (long long)(zl + 1) * p.plane + Y * p.nx + X;
+    const long long e = (long long)(zl + 1) * p.plane + Y * p.ldx + X;
     if (p.gam != nullptr) {   // GAm: the row's 27-node mean weights (A19)
       t1 = p.gam[e], t2 = p.gam[p.fstride + e], mu0 = p.gam[2 * p.fstride + e];
       mu1 = p.gam[3 * p.fstride + e], mu2 = p.gam[4 * p.fstride + e];
@@ -144,7 +153,7 @@ template <typename R>
 __global__ void winv_kernel(const R* __restrict__ v, R* __restrict__ w, long long n) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const R a = v[i];
-    w[i] = R(1) / (a * a);
+    w[i] = a > R(0) ? R(1) / (a * a) : R(0);   // pad columns (v = 0) get w = 0
   }
 }
 
@@ -160,12 +169,13 @@ template cudaError_t launch_winv<double>(const double*, double*, long long, cuda
 // velocity validation / statistics: min, max, non-finite count, clamped count
 // =============================================================================================
 template <typename R>
-__global__ void vstats_kernel(const R* __restrict__ v, long long n, R inv_fh, R g_min, R g_max,
+__global__ void vstats_kernel(const R* __restrict__ v, long long n, int nx, int ldx, R inv_fh, R g_min, R g_max,
                               unsigned long long* __restrict__ out /* [4]: minbits,maxbits,bad,clamped */) {
   R lmin = R(3.0e38), lmax = R(0);
   unsigned long long bad = 0, clamped = 0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const R x = v[i];
+    const long long row = i / nx;
+    const R x = v[row * ldx + (i - row * nx)];
     if (!(x > R(0)) || !isfinite((double)x)) { bad++; continue; }
     lmin = x < lmin ? x : lmin;
     lmax = x > lmax ? x : lmax;
@@ -389,16 +399,17 @@ __global__ void __launch_bounds__(NT) bicg_update_kernel(VecParams<R> q) {
                            blockIdx.x);
 }
 
-// ‖f‖² per RHS (used for ‖b‖)
+// ‖f‖² per RHS over the owned points (used for ‖b‖: the caller's pad columns are not read)
 template <typename R, int NT>
 __global__ void __launch_bounds__(NT) norm2_kernel(const typename Cx<R>::T* __restrict__ f, long long fstride,
-                                                   long long plane, long long n, double* partials, double* out,
-                                                   unsigned int* tickets) {
+                                                   long long plane, long long n, int nx, int ldx, double* partials,
+                                                   double* out, unsigned int* tickets) {
   const int rhs = blockIdx.y;
   const long long off = (long long)rhs * fstride + plane;
   double part[1] = {0.0};
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const typename Cx<R>::T a = f[off + i];
+    const long long row = i / nx;
+    const typename Cx<R>::T a = f[off + row * ldx + (i - row * nx)];
     part[0] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
   }
   block_grid_reduce<1, NT>(part, partials + (long long)rhs * gridDim.x, out + rhs, tickets + rhs, gridDim.x, blockIdx.x);
@@ -615,18 +626,9 @@ __global__ void __launch_bounds__(NT) bicgl_kernel(VecParams<R> q) {
 // =============================================================================================
 // host-side launchers (kernels.h)
 // =============================================================================================
+// register path: R = double only (complex128, and the fp64 residual of the complex64 solver)
 template <typename R> struct ApplyCfg;
-#ifndef HZ_NY_F
-#define HZ_NY_F 2
-#endif
-#ifndef HZ_W_F
-#define HZ_W_F 4
-#endif
-#ifndef HZ_NY_D
-#define HZ_NY_D 1
-#endif
-template <> struct ApplyCfg<float> { enum { NY = HZ_NY_F, WARPS = HZ_W_F }; };
-template <> struct ApplyCfg<double> { enum { NY = HZ_NY_D, WARPS = 4 }; };
+template <> struct ApplyCfg<double> { enum { NY = 1, WARPS = 4 }; };
 
 template <typename R>
 long long apply_nblocks_x(int nx, int ny) {   // CTAs covering one z-chunk of the (strip, x-tile) space
@@ -634,38 +636,22 @@ long long apply_nblocks_x(int nx, int ny) {   // CTAs covering one z-chunk of th
   const long long nwarps = (long long)((ny + NY - 1) / NY) * ((nx + XT - 1) / XT);
   return (nwarps + W - 1) / W;
 }
-template long long apply_nblocks_x<float>(int, int);
 template long long apply_nblocks_x<double>(int, int);
 
-// Split of one apply into the general launch (everything) and the interior box launch; returns the
-// total number of CTAs per RHS (partials of the dot epilogues).
-// complex64 interior launch geometry (apply27_tma)
-#ifndef HZ_TMA_NY
-#define HZ_TMA_NY 2
-#endif
-#ifndef HZ_TMA_WX
-#define HZ_TMA_WX 4
-#endif
-#ifndef HZ_TMA_WY
-#define HZ_TMA_WY 2
-#endif
-constexpr int TMA_NY = HZ_TMA_NY, TMA_WX = HZ_TMA_WX, TMA_WY = HZ_TMA_WY;
-typedef TmaTile<TMA_NY, TMA_WX, TMA_WY> TmaT;
-
+// Register-path launches (apply27_v2): the general launch (everything) and the interior box launch;
+// returns the total number of CTAs per RHS (partials of the dot epilogues).
 template <typename R, typename S>
 long long apply_plan(ApplyParams<R, S>& p) {
   constexpr int NY = ApplyCfg<R>::NY, W = ApplyCfg<R>::WARPS;
-  constexpr bool TMA = std::is_same<R, float>::value && std::is_same<S, float>::value;
   p.nbx = (int)apply_nblocks_x<R>(p.nx, p.ny);
-  // tiles whose outputs lie in [max(lo,1), min(hi, hmax)] (footprint inside the grid, no PML); in x
-  // the TMA rows' 16-byte alignment overhang (≤ 7 elements past the tile) must stay inside the row
+  // tiles whose outputs lie in [max(lo,1), min(hi, hmax)] (footprint inside the grid, no PML)
   auto range = [](int lo, int hi, int hmax, int T, int& a, int& b) {
     const int l = std::max(lo, 1), h = std::min(hi, hmax);
     a = (l + T - 1) / T;
     b = (h - (T - 1) >= 0) ? (h - (T - 1)) / T + 1 : 0;
     if (b < a) b = a;
   };
-  range(p.lo[0], p.hi[0], TMA ? p.nx - 8 : p.nx - 2, XT, p.box_t0, p.box_t1);
+  range(p.lo[0], p.hi[0], p.nx - 2, XT, p.box_t0, p.box_t1);
   range(p.lo[1], p.hi[1], p.ny - 2, NY, p.box_s0, p.box_s1);
   // z-chunks: planes whose outputs lie in [max(lo,1), min(hi, nzg-2)] (global) are cut into chunks of
   // ≤ zc planes (the interior chunks); the planes below / above form one chunk each
@@ -691,26 +677,10 @@ long long apply_plan(ApplyParams<R, S>& p) {
   }
   const long long bw = (long long)(p.box_s1 - p.box_s0) * (p.box_t1 - p.box_t0);
   p.box_nbx = (int)((bw + W - 1) / W);
-  p.tma_x0 = XT * p.box_t0;
-  p.tma_x1 = XT * p.box_t1;
-  p.tma_y0 = NY * p.box_s0;
-  p.tma_y1 = NY * p.box_s1;
-  p.tma_ntx = p.tma_nty = 0;
-  bool empty = bw == 0 || p.box_c1 <= p.box_c0;
-  if (TMA && !empty) {
-    if (p.tma_x1 - p.tma_x0 < TmaT::TX || p.tma_y1 - p.tma_y0 < TmaT::TY) {
-      p.tma_ntx = p.tma_nty = 0;   // box smaller than one TMA tile: the register-path interior launch
-    } else {
-      p.tma_ntx = (p.tma_x1 - p.tma_x0 + TmaT::TX - 1) / TmaT::TX;
-      p.tma_nty = (p.tma_y1 - p.tma_y0 + TmaT::TY - 1) / TmaT::TY;
-      p.box_nbx = p.tma_ntx * p.tma_nty;
-    }
-  }
-  if (empty) {
+  if (bw == 0 || p.box_c1 <= p.box_c0) {
     p.box_nbx = 0;
     p.box_c0 = p.box_c1 = 0;
     p.box_s0 = p.box_s1 = p.box_t0 = p.box_t1 = 0;
-    p.tma_ntx = p.tma_nty = 0;
   }
   // general work list
   const int ntx = (p.nx + XT - 1) / XT, nstrips = (p.ny + NY - 1) / NY;
@@ -727,7 +697,6 @@ long long apply_plan(ApplyParams<R, S>& p) {
   p.gen_blocks = p.nbound == p.nchunks ? p.nbx * p.nchunks : p.nbound * p.nbx + p.nint * p.nbx_frame;
   return (long long)p.gen_blocks + (long long)p.box_nbx * (p.box_c1 - p.box_c0);
 }
-template long long apply_plan<float, float>(ApplyParams<float, float>&);
 template long long apply_plan<double, double>(ApplyParams<double, double>&);
 template long long apply_plan<double, float>(ApplyParams<double, float>&);
 
@@ -748,86 +717,67 @@ static cudaError_t launch_one(const ApplyParams<R, S>& p, long long nb, cudaStre
   return cudaGetLastError();
 }
 
-template <bool COLLOC, int EPI>
-static cudaError_t launch_tma(const ApplyParams<float, float>& p, long long nb, cudaStream_t s) {
-  auto kern = apply27_tma<TMA_NY, TMA_WX, TMA_WY, COLLOC, EPI>;
-  if (nb <= 0) return cudaSuccess;
-  if (nb >= (1LL << 31)) return cudaErrorInvalidConfiguration;
-  const size_t smem = tma_smem_bytes<TMA_NY, TMA_WX, TMA_WY>(p.tab_n);
-  // the 48 KB default limit counts static (dot-reduction scratch) + dynamic shared memory
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  kern<<<(unsigned)nb, 32 * TMA_WX * TMA_WY, smem, s>>>(p);
-  return cudaGetLastError();
-}
-
 static thread_local int g_last_apply_launches = 0;
 int apply_last_launches() { return g_last_apply_launches; }
 
-// complex64 RHS-fused launch: one launch over the work list (x/y-PML items, then the rest);
-// blockIdx.y = group of NR right-hand sides.  Rows per thread: 2 for one RHS, else 1 so that the
-// two-RHS body fits 128 registers (2 CTAs of 256 threads per SM).
-#ifndef HZ_CP_NY1
-#define HZ_CP_NY1 2
-#endif
-template <int NR> struct CpNY { enum { V = NR == 1 ? HZ_CP_NY1 : 1 }; };
-
+// complex64 tensor-map launch: one launch over the work list (x/y-PML items, then the rest);
+// blockIdx.y = group of NR right-hand sides (1 for a single RHS, else 2).
 template <int NR, bool COLLOC, int EPI, bool GAM>
-static cudaError_t launch_cp_t(const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
-  constexpr int NY = CpNY<NR>::V;
+static cudaError_t launch_tm_t(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
   const int ngroups = (nrhs + NR - 1) / NR;
-  const int nitems = p.cp_n_pml + p.cp_n_int;
+  const int nitems = p.tm_nblocks;
   g_last_apply_launches = nitems > 0 ? 1 : 0;
   if (nitems <= 0) return cudaSuccess;
-  auto kern = apply27_cp<NY, NR, COLLOC, EPI, GAM>;
-  const size_t smem = cp_smem_bytes(p.tab_n, NR, EPI);
+  auto kern = apply27_tm<NR, COLLOC, EPI, GAM>;
+  const size_t smem = tm_smem_bytes(p.tab_n, p.tm_tx, p.tm_ty, NR);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  kern<<<dim3((unsigned)nitems, (unsigned)ngroups), CP_THREADS(NY), smem, s>>>(p, 0);
+  kern<<<dim3((unsigned)nitems, (unsigned)ngroups), TM_NTHR, smem, s>>>(*L.w, *L.u, p);
   return cudaGetLastError();
 }
 template <int NR, bool COLLOC, int EPI>
-static cudaError_t launch_cp(const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
-  return p.gam != nullptr ? launch_cp_t<NR, COLLOC, EPI, true>(p, nrhs, s) : launch_cp_t<NR, COLLOC, EPI, false>(p, nrhs, s);
+static cudaError_t launch_tm(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
+  return p.gam != nullptr ? launch_tm_t<NR, COLLOC, EPI, true>(L, p, nrhs, s) : launch_tm_t<NR, COLLOC, EPI, false>(L, p, nrhs, s);
 }
+// RHS per CTA: two for a plain apply of several fields (the coefficients are built once for both);
+// one when a dot epilogue runs (its fp64 partials would not fit the register budget of two)
+int tm_group(int nrhs, int epi) { return (nrhs > 1 && epi == EPI_PLAIN) ? 2 : 1; }
 
-#ifndef HZ_CP_NR
-#define HZ_CP_NR 2
-#endif
-int cp_group(int nrhs) { return nrhs == 1 ? 1 : HZ_CP_NR; }
-int cp_rows(int nr) { return nr == 1 ? (int)CpNY<1>::V : (int)CpNY<HZ_CP_NR>::V; }
-
-template <typename R, typename S>
-long long apply_slots(ApplyParams<R, S>& p) {
-  if constexpr (std::is_same<R, float>::value && std::is_same<S, float>::value) {
-#ifndef HZ_NO_CP
-    if (p.cp_work != nullptr) return p.cp_nblocks;
-#endif
+template <bool COLLOC, int EPI>
+static cudaError_t launch_tm_epi(const TmLaunch& L, ApplyParams<float, float> p, int nrhs, cudaStream_t s) {
+  p.nrhs = nrhs;
+  if constexpr (EPI == EPI_PLAIN) {
+    if (tm_group(nrhs, EPI) == 2) return launch_tm<2, COLLOC, EPI>(L, p, nrhs, s);
   }
-  return apply_plan(p);
+  return launch_tm<1, COLLOC, EPI>(L, p, nrhs, s);
 }
-template long long apply_slots<float, float>(ApplyParams<float, float>&);
-template long long apply_slots<double, double>(ApplyParams<double, double>&);
-template long long apply_slots<double, float>(ApplyParams<double, float>&);
+cudaError_t launch_apply_tm(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, bool colloc, int epi,
+                            cudaStream_t s) {
+  switch (epi) {
+    case EPI_PLAIN: return colloc ? launch_tm_epi<true, EPI_PLAIN>(L, p, nrhs, s) : launch_tm_epi<false, EPI_PLAIN>(L, p, nrhs, s);
+    case EPI_DOT1: return colloc ? launch_tm_epi<true, EPI_DOT1>(L, p, nrhs, s) : launch_tm_epi<false, EPI_DOT1>(L, p, nrhs, s);
+    case EPI_DOT4: return colloc ? launch_tm_epi<true, EPI_DOT4>(L, p, nrhs, s) : launch_tm_epi<false, EPI_DOT4>(L, p, nrhs, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int tm_occupancy(int tab_n, int tx, int ty, int nr) {
+  int nb = 0;
+  if (nr == 1)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_tm<1, false, EPI_DOT4, false>, TM_NTHR,
+                                                  tm_smem_bytes(tab_n, tx, ty, 1));
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_tm<2, false, EPI_DOT4, false>, TM_NTHR,
+                                                  tm_smem_bytes(tab_n, tx, ty, 2));
+  return nb > 0 ? nb : 1;
+}
 
 template <typename R, typename S, bool COLLOC, int EPI>
 static cudaError_t launch_apply_t(ApplyParams<R, S> p, int nrhs, cudaStream_t s) {
-  if constexpr (std::is_same<R, float>::value && std::is_same<S, float>::value && EPI != EPI_RESID) {
-#ifndef HZ_NO_CP
-    if (p.cp_work != nullptr) {
-      p.nrhs = nrhs;
-      return cp_group(nrhs) == 1 ? launch_cp<1, COLLOC, EPI>(p, nrhs, s) : launch_cp<HZ_CP_NR, COLLOC, EPI>(p, nrhs, s);
-    }
-#endif
-  }
   apply_plan(p);
   p.nrhs = nrhs;
   const long long ngen = (long long)p.gen_blocks * nrhs;
@@ -835,53 +785,37 @@ static cudaError_t launch_apply_t(ApplyParams<R, S> p, int nrhs, cudaStream_t s)
   g_last_apply_launches = (ngen > 0) + (nbox > 0);
   cudaError_t e = launch_one<R, S, COLLOC, EPI, false>(p, ngen, s);
   if (e != cudaSuccess) return e;
-  if constexpr (std::is_same<R, float>::value && std::is_same<S, float>::value) {
-#ifndef HZ_NO_TMA
-    if (p.tma_ntx > 0 && p.gam == nullptr) return launch_tma<COLLOC, EPI>(p, nbox, s);
-#endif
-  }
   return launch_one<R, S, COLLOC, EPI, true>(p, nbox, s);
 }
 
-template <typename R>
-int apply_ny() { return ApplyCfg<R>::NY; }
-template int apply_ny<float>();
-template int apply_ny<double>();
-template <typename R>
-int apply_warps() { return ApplyCfg<R>::WARPS; }
-template int apply_warps<float>();
-template int apply_warps<double>();
-
-template <typename R, typename S>
-cudaError_t launch_apply(const ApplyParams<R, S>& p, int nrhs, bool colloc, int epi, cudaStream_t s) {
+// register path: complex128 (every epilogue)
+template <>
+cudaError_t launch_apply<double, double>(const ApplyParams<double, double>& p, int nrhs, bool colloc, int epi,
+                                         cudaStream_t s) {
   if (!colloc) {
     switch (epi) {
-      case EPI_PLAIN: return launch_apply_t<R, S, false, EPI_PLAIN>(p, nrhs, s);
-      case EPI_DOT1: return launch_apply_t<R, S, false, EPI_DOT1>(p, nrhs, s);
-      case EPI_DOT4: return launch_apply_t<R, S, false, EPI_DOT4>(p, nrhs, s);
-      case EPI_RESID: return launch_apply_t<R, S, false, EPI_RESID>(p, nrhs, s);
+      case EPI_PLAIN: return launch_apply_t<double, double, false, EPI_PLAIN>(p, nrhs, s);
+      case EPI_DOT1: return launch_apply_t<double, double, false, EPI_DOT1>(p, nrhs, s);
+      case EPI_DOT4: return launch_apply_t<double, double, false, EPI_DOT4>(p, nrhs, s);
+      case EPI_RESID: return launch_apply_t<double, double, false, EPI_RESID>(p, nrhs, s);
     }
   } else {
     switch (epi) {
-      case EPI_PLAIN: return launch_apply_t<R, S, true, EPI_PLAIN>(p, nrhs, s);
-      case EPI_DOT1: return launch_apply_t<R, S, true, EPI_DOT1>(p, nrhs, s);
-      case EPI_DOT4: return launch_apply_t<R, S, true, EPI_DOT4>(p, nrhs, s);
-      case EPI_RESID: return launch_apply_t<R, S, true, EPI_RESID>(p, nrhs, s);
+      case EPI_PLAIN: return launch_apply_t<double, double, true, EPI_PLAIN>(p, nrhs, s);
+      case EPI_DOT1: return launch_apply_t<double, double, true, EPI_DOT1>(p, nrhs, s);
+      case EPI_DOT4: return launch_apply_t<double, double, true, EPI_DOT4>(p, nrhs, s);
+      case EPI_RESID: return launch_apply_t<double, double, true, EPI_RESID>(p, nrhs, s);
     }
   }
   return cudaErrorInvalidValue;
 }
-template cudaError_t launch_apply<float, float>(const ApplyParams<float, float>&, int, bool, int, cudaStream_t);
-template cudaError_t launch_apply<double, double>(const ApplyParams<double, double>&, int, bool, int, cudaStream_t);
 
-// mixed precision (c64 storage, fp64 arithmetic): residual and plain apply only
+// mixed precision (c64 storage, fp64 arithmetic): the residual of the complex64 solver
 template <>
 cudaError_t launch_apply<double, float>(const ApplyParams<double, float>& p, int nrhs, bool colloc, int epi,
                                         cudaStream_t s) {
   if (epi == EPI_RESID) return colloc ? launch_apply_t<double, float, true, EPI_RESID>(p, nrhs, s)
                                       : launch_apply_t<double, float, false, EPI_RESID>(p, nrhs, s);
-  if (epi == EPI_PLAIN) return colloc ? launch_apply_t<double, float, true, EPI_PLAIN>(p, nrhs, s)
-                                      : launch_apply_t<double, float, false, EPI_PLAIN>(p, nrhs, s);
   return cudaErrorInvalidValue;
 }
 
@@ -895,18 +829,7 @@ int apply_occupancy(bool colloc) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_v2<R, R, NY, W, false, EPI_DOT4, true>, 32 * W, 16 * 1024);
   return nb > 0 ? nb : 1;
 }
-template int apply_occupancy<float>(bool);
 template int apply_occupancy<double>(bool);
-
-template <int NR>
-static int cp_occ(int tab_n) {
-  constexpr int NY = CpNY<NR>::V;
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_cp<NY, NR, false, EPI_DOT4, false>, CP_THREADS(NY),
-                                                cp_smem_bytes(tab_n, NR, EPI_DOT4));
-  return nb > 0 ? nb : 1;
-}
-int cp_occupancy(int tab_n, int nr) { return nr == 1 ? cp_occ<1>(tab_n) : cp_occ<HZ_CP_NR>(tab_n); }
 
 template <typename R>
 cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s) {
@@ -925,8 +848,8 @@ template cudaError_t launch_record<double>(const ApplyParams<double>&, double*, 
 // =============================================================================================
 template <typename R>
 __global__ void eqerror_kernel(const typename Cx<R>::T* __restrict__ uref, const typename Cx<R>::T* __restrict__ u,
-                               int nx, int ny, int nzl, int z0, int nzg, long long xs, long long ys, long long zs,
-                               double h, int npml, double ball, double* __restrict__ partials) {
+                               int nx, int ny, int ldx, int nzl, int z0, int nzg, long long xs, long long ys,
+                               long long zs, double h, int npml, double ball, double* __restrict__ partials) {
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const long long plane = (long long)nx * ny;
   const long long n = (long long)nzl * plane;
@@ -940,7 +863,8 @@ __global__ void eqerror_kernel(const typename Cx<R>::T* __restrict__ uref, const
     const double d = sqrt(dx * dx + dy * dy + dz * dz);
     if (!(d > ball)) continue;
     const double W = h * d;
-    const typename Cx<R>::T a = uref[plane + idx], b = u[plane + idx];
+    const long long e = (long long)(zl + 1) * ny * ldx + (long long)y * ldx + x;
+    const typename Cx<R>::T a = uref[e], b = u[e];
     acc[0] += fabs(W * ((double)a.x - (double)b.x));
     acc[1] += fabs(W * ((double)a.y - (double)b.y));
     acc[2] += fabs(W * (double)a.x);
@@ -964,15 +888,16 @@ __global__ void eqerror_kernel(const typename Cx<R>::T* __restrict__ uref, const
 }
 
 template <typename R>
-cudaError_t launch_eqerror(const typename Cx<R>::T* uref, const typename Cx<R>::T* u, int nx, int ny, int nzl, int z0,
-                           int nzg, const long long* src, double h, int npml, double ball, double* partials, int nblocks,
-                           cudaStream_t s) {
-  eqerror_kernel<R><<<nblocks, 256, 0, s>>>(uref, u, nx, ny, nzl, z0, nzg, src[0], src[1], src[2], h, npml, ball, partials);
+cudaError_t launch_eqerror(const typename Cx<R>::T* uref, const typename Cx<R>::T* u, int nx, int ny, int ldx, int nzl,
+                           int z0, int nzg, const long long* src, double h, int npml, double ball, double* partials,
+                           int nblocks, cudaStream_t s) {
+  eqerror_kernel<R><<<nblocks, 256, 0, s>>>(uref, u, nx, ny, ldx, nzl, z0, nzg, src[0], src[1], src[2], h, npml, ball,
+                                            partials);
   return cudaGetLastError();
 }
-template cudaError_t launch_eqerror<float>(const float2*, const float2*, int, int, int, int, int, const long long*, double,
-                                           int, double, double*, int, cudaStream_t);
-template cudaError_t launch_eqerror<double>(const double2*, const double2*, int, int, int, int, int, const long long*,
+template cudaError_t launch_eqerror<float>(const float2*, const float2*, int, int, int, int, int, int, const long long*,
+                                           double, int, double, double*, int, cudaStream_t);
+template cudaError_t launch_eqerror<double>(const double2*, const double2*, int, int, int, int, int, int, const long long*,
                                             double, int, double, double*, int, cudaStream_t);
 
 // =============================================================================================
@@ -989,14 +914,12 @@ __global__ void matrix_kernel(ApplyParams<R> p, bool colloc, long long* __restri
   R* tab = reinterpret_cast<R*>(smem_raw);
   for (int i = threadIdx.x; i < p.n_g * TAB_STRIDE; i += blockDim.x) tab[i] = p.tab[i];
   __syncthreads();
-  const long long n = (long long)p.nzl * p.plane;
+  const long long n = (long long)p.nzl * p.ny * p.nx;
   const R ih2 = p.ih2;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (long long)gridDim.x * blockDim.x) {
-    const int zl = (int)(idx / p.plane);
-    const int rem = (int)(idx - (long long)zl * p.plane);
-    const int y = rem / p.nx, x = rem - y * p.nx;
+    int zl, y, x;
+    const long long e = st_elem(p, idx, zl, y, x);   // storage element of the row
     const int zg = p.z0 + zl;
-    const long long e = p.plane + idx;   // storage element of the row
     R t1, t2, mu0, mu1, mu2;
     if (p.gam != nullptr) {
       t1 = p.gam[e], t2 = p.gam[p.fstride + e], mu0 = p.gam[2 * p.fstride + e];
@@ -1027,7 +950,7 @@ __global__ void matrix_kernel(ApplyParams<R> p, bool colloc, long long* __restri
         continue;
       }
       const int cls = (dx != 0) + (dy != 0) + (dz != 0);
-      const R wnb = colloc ? wn : p.w[e + (long long)dz * p.plane + (long long)dy * p.nx + dx];
+      const R wnb = colloc ? wn : p.w[e + (long long)dz * p.plane + (long long)dy * p.ldx + dx];
       C v = make_cx(p.w2 * mu[cls] * wnb, R(0));
       const int dd[3] = {dx, dy, dz};
 #pragma unroll
@@ -1108,13 +1031,32 @@ template cudaError_t launch_sources<double>(const ApplyParams<double>&, int, con
                                             double, double2*, cudaStream_t);
 
 template <typename R>
-cudaError_t launch_vstats(const R* v, long long n, R inv_fh, R g_min, R g_max, unsigned long long* out, cudaStream_t s) {
-  vstats_kernel<R><<<592, 256, 0, s>>>(v, n, inv_fh, g_min, g_max, out);
+cudaError_t launch_vstats(const R* v, long long n, int nx, int ldx, R inv_fh, R g_min, R g_max, unsigned long long* out,
+                          cudaStream_t s) {
+  vstats_kernel<R><<<592, 256, 0, s>>>(v, n, nx, ldx, inv_fh, g_min, g_max, out);
   return cudaGetLastError();
 }
-template cudaError_t launch_vstats<float>(const float*, long long, float, float, float, unsigned long long*, cudaStream_t);
-template cudaError_t launch_vstats<double>(const double*, long long, double, double, double, unsigned long long*,
+template cudaError_t launch_vstats<float>(const float*, long long, int, int, float, float, float, unsigned long long*,
+                                          cudaStream_t);
+template cudaError_t launch_vstats<double>(const double*, long long, int, int, double, double, double, unsigned long long*,
                                            cudaStream_t);
+
+// =============================================================================================
+// loopback communicator (P slabs in one process on one device): out[i] = op over the P ranks' buffers
+// in rank order (sum or max) — the device half of its allreduce
+// =============================================================================================
+__global__ void loop_reduce_kernel(LoopPtrs ptrs, int np, double* __restrict__ out, long long n, int op) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double a = ptrs.p[0][i];
+    for (int q = 1; q < np; q++) a = op == 0 ? a + ptrs.p[q][i] : fmax(a, ptrs.p[q][i]);
+    out[i] = a;
+  }
+}
+cudaError_t launch_loop_reduce(const LoopPtrs& ptrs, int np, double* out, long long n, int op, cudaStream_t s) {
+  const int nb = (int)std::min<long long>(148, (n + 255) / 256);
+  loop_reduce_kernel<<<nb > 0 ? nb : 1, 256, 0, s>>>(ptrs, np, out, n, op);
+  return cudaGetLastError();
+}
 
 constexpr int VEC_NT = 256;
 
@@ -1151,15 +1093,15 @@ template cudaError_t launch_bicgl<float>(int, const VecParams<float>&, int, cuda
 template cudaError_t launch_bicgl<double>(int, const VecParams<double>&, int, cudaStream_t);
 
 template <typename R>
-cudaError_t launch_norm2(const typename Cx<R>::T* f, long long fstride, long long plane, long long n, int nrhs,
-                         int nblocks, double* partials, double* out, unsigned int* tickets, cudaStream_t s) {
+cudaError_t launch_norm2(const typename Cx<R>::T* f, long long fstride, long long plane, long long n, int nx, int ldx,
+                         int nrhs, int nblocks, double* partials, double* out, unsigned int* tickets, cudaStream_t s) {
   dim3 grid((unsigned)nblocks, (unsigned)nrhs);
-  norm2_kernel<R, VEC_NT><<<grid, VEC_NT, 0, s>>>(f, fstride, plane, n, partials, out, tickets);
+  norm2_kernel<R, VEC_NT><<<grid, VEC_NT, 0, s>>>(f, fstride, plane, n, nx, ldx, partials, out, tickets);
   return cudaGetLastError();
 }
-template cudaError_t launch_norm2<float>(const float2*, long long, long long, long long, int, int, double*, double*,
-                                         unsigned int*, cudaStream_t);
-template cudaError_t launch_norm2<double>(const double2*, long long, long long, long long, int, int, double*, double*,
-                                          unsigned int*, cudaStream_t);
+template cudaError_t launch_norm2<float>(const float2*, long long, long long, long long, int, int, int, int, double*,
+                                         double*, unsigned int*, cudaStream_t);
+template cudaError_t launch_norm2<double>(const double2*, long long, long long, long long, int, int, int, int, double*,
+                                          double*, unsigned int*, cudaStream_t);
 
 }  // namespace hz

@@ -4,7 +4,7 @@
 
 #include "apply.cuh"
 #include "apply27.cuh"
-#include "apply27_cp.cuh"
+#include "apply27_tm.cuh"
 
 namespace hz {
 
@@ -21,7 +21,7 @@ struct SolverState {
 template <typename R>
 struct VecParams {
   typedef typename Cx<R>::T C;
-  long long n;        // owned points per RHS (nzl*plane)
+  long long n;        // owned storage elements per RHS (nzl*plane, pad columns included: they stay 0)
   long long plane;    // halo-plane offset
   long long fstride;  // per-RHS stride
   int nblocks;        // CTAs per RHS
@@ -43,29 +43,41 @@ enum { BICG_INIT = 0, BICG_S = 1, BICG_UPDATE = 2, BICG_RHO_RESET = 3 };
 // BCL_D, apply (DOT4), BCL_E
 enum { BCL_INIT = 0, BCL_A = 1, BCL_B = 2, BCL_C = 3, BCL_D = 4, BCL_E = 5 };
 
-template <typename R> int apply_ny();
-template <typename R> int apply_warps();
+int apply_last_launches();   // kernels launched by the last apply launch on this thread (1 or 2)
+// register path (R = double): complex128 and the fp64 residual of the complex64 solver
 template <typename R> int apply_occupancy(bool colloc);
-int apply_last_launches();   // kernels launched by the last launch_apply on this thread (1 or 2)
 template <typename R> long long apply_nblocks_x(int nx, int ny);   // CTAs along x of one z-chunk
 template <typename R, typename S> long long apply_plan(ApplyParams<R, S>& p);   // CTAs per RHS, both launches
-template <typename R, typename S> long long apply_slots(ApplyParams<R, S>& p);  // dot partial slots per RHS
-int cp_group(int nrhs);                                                           // RHS per CTA (complex64)
-int cp_occupancy(int tab_n, int nr);
-int cp_rows(int nr);   // rows per thread (NY) of the complex64 apply for NR RHS per CTA
-   // CTAs/SM of the complex64 apply (NR RHS per CTA, 4 dots)
 template <typename R, typename S>
 cudaError_t launch_apply(const ApplyParams<R, S>& p, int nrhs, bool colloc, int epi, cudaStream_t s);
 template <>
+cudaError_t launch_apply<double, double>(const ApplyParams<double, double>& p, int nrhs, bool colloc, int epi,
+                                         cudaStream_t s);
+template <>
 cudaError_t launch_apply<double, float>(const ApplyParams<double, float>& p, int nrhs, bool colloc, int epi,
                                         cudaStream_t s);
+// complex64 tensor-map apply (apply27_tm): the two tensor maps of the launch (w, and u of this call)
+struct TmLaunch {
+  const CUtensorMap* w;
+  const CUtensorMap* u;
+};
+int tm_group(int nrhs, int epi);         // RHS per CTA
+int tm_occupancy(int tab_n, int tx, int ty, int nr);   // resident CTAs per SM
+cudaError_t launch_apply_tm(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, bool colloc, int epi,
+                            cudaStream_t s);
+// loopback communicator: the ranks' buffers (same device), reduced in rank order; op 0 = sum, 1 = max
+constexpr int LOOP_MAX_RANKS = 16;
+struct LoopPtrs {
+  const double* p[LOOP_MAX_RANKS];
+};
+cudaError_t launch_loop_reduce(const LoopPtrs& ptrs, int np, double* out, long long n, int op, cudaStream_t s);
 template <typename R> cudaError_t launch_winv(const R* v, R* w, long long n, cudaStream_t s);
 template <typename R> cudaError_t launch_record(const ApplyParams<R>& p, R* rec, cudaStream_t s);
 template <typename R> cudaError_t launch_gam_field(const ApplyParams<R>& p, R* out, int radius, cudaStream_t s);
 template <typename R>
-cudaError_t launch_eqerror(const typename Cx<R>::T* uref, const typename Cx<R>::T* u, int nx, int ny, int nzl, int z0,
-                           int nzg, const long long* src, double h, int npml, double ball, double* partials, int nblocks,
-                           cudaStream_t s);
+cudaError_t launch_eqerror(const typename Cx<R>::T* uref, const typename Cx<R>::T* u, int nx, int ny, int ldx, int nzl,
+                           int z0, int nzg, const long long* src, double h, int npml, double ball, double* partials,
+                           int nblocks, cudaStream_t s);
 template <typename R>
 cudaError_t launch_matrix(const ApplyParams<R>& p, bool colloc, long long* cols, typename Cx<R>::T* vals, cudaStream_t s);
 cudaError_t launch_dispersion(const double* w7, const double* G, int nG, const double* theta, const double* phi, int nang,
@@ -74,11 +86,12 @@ template <typename R>
 cudaError_t launch_sources(const ApplyParams<R>& p, int nsrc, const long long* nodes, const double* amps,
                            int consistent, R ih3, typename Cx<R>::T* b, cudaStream_t s);
 template <typename R>
-cudaError_t launch_vstats(const R* v, long long n, R inv_fh, R g_min, R g_max, unsigned long long* out, cudaStream_t s);
+cudaError_t launch_vstats(const R* v, long long n, int nx, int ldx, R inv_fh, R g_min, R g_max, unsigned long long* out,
+                          cudaStream_t s);
 template <typename R> cudaError_t launch_bicg(int which, const VecParams<R>& q, int nrhs, cudaStream_t s);
 template <typename R> cudaError_t launch_bicgl(int which, const VecParams<R>& q, int nrhs, cudaStream_t s);
 template <typename R>
-cudaError_t launch_norm2(const typename Cx<R>::T* f, long long fstride, long long plane, long long n, int nrhs,
-                         int nblocks, double* partials, double* out, unsigned int* tickets, cudaStream_t s);
+cudaError_t launch_norm2(const typename Cx<R>::T* f, long long fstride, long long plane, long long n, int nx, int ldx,
+                         int nrhs, int nblocks, double* partials, double* out, unsigned int* tickets, cudaStream_t s);
 
 }  // namespace hz

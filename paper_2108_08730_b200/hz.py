@@ -69,6 +69,9 @@ _P = ct.POINTER
 _sigs = {
     "hz_last_error": (ct.c_char_p, []),
     "hz_version": (ct.c_char_p, []),
+    "hz_field_ldx": (ct.c_int, [ct.c_int]),
+    "hz_ctx_create_loopback": (ct.c_int, [ct.c_int, ct.c_int, _P(_vp)]),
+    "hz_solve_opts_default": (hz_solve_opts, []),
     "hz_kernel_launch_count": (ct.c_longlong, []),
     "hz_trim_memory": (None, []),
     "hz_get_unique_id": (ct.c_int, [ct.c_char_p]),
@@ -121,6 +124,30 @@ def _ptr(a):
     raise TypeError(type(a))
 
 
+def _strides_elems(a):
+    if hasattr(a, "data_ptr"):
+        return tuple(a.stride()), a.shape
+    return tuple(st // a.itemsize for st in a.strides), a.shape
+
+
+def _fptr(c, a, what="field"):
+    """Address of a field buffer in the ABI layout [nrhs][nz_local+2][ny][ldx] (include/hz.h): the
+    [..][nx] view that Coeffs.alloc_field returns, or a dense tensor / array whose last dim is ldx."""
+    if a is None:
+        return None
+    g = c.grid
+    ldx = c.ldx
+    st, shp = _strides_elems(a)
+    if len(shp) not in (3, 4) or tuple(shp[-3:-1]) != (g.nz_local + 2, g.ny) or shp[-1] not in (g.nx, ldx):
+        raise ValueError(f"{what}: shape {tuple(shp)} is not [nrhs][{g.nz_local + 2}][{g.ny}][{g.nx} or {ldx}]")
+    fstride = ldx * g.ny * (g.nz_local + 2)
+    ok = tuple(st[-3:]) == (ldx * g.ny, ldx, 1) and (len(shp) == 3 or shp[0] == 1 or st[0] == fstride)
+    if not ok:
+        raise ValueError(f"{what}: strides {tuple(st)} are not the padded field layout (row pitch {ldx}); "
+                         "allocate it with Coeffs.alloc_field")
+    return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+
 def _stream_ptr(stream):
     if stream is None:
         return None
@@ -129,6 +156,11 @@ def _stream_ptr(stream):
 
 def hz_version() -> str:
     return _lib.hz_version().decode()
+
+
+def hz_field_ldx(nx: int) -> int:
+    """Row pitch of every field buffer (include/hz.h): nx rounded up to a multiple of 4."""
+    return int(_lib.hz_field_ldx(nx))
 
 
 def hz_kernel_launch_count() -> int:
@@ -163,6 +195,14 @@ def hz_ctx_create(device: int = 0, nranks: int = 1, rank: int = 0, uid: Optional
     h = _vp()
     _check(_lib.hz_ctx_create(device, nranks, rank, uid, ct.byref(h)), "hz_ctx_create")
     return Ctx(h)
+
+
+def hz_ctx_create_loopback(device: int, nranks: int):
+    """nranks contexts of one loopback group on one device (include/hz.h): call each rank's functions
+    from its own thread."""
+    arr = (_vp * nranks)()
+    _check(_lib.hz_ctx_create_loopback(device, nranks, arr), "hz_ctx_create_loopback")
+    return [Ctx(_vp(arr[r])) for r in range(nranks)]
 
 
 # ------------------------------------------------------------------------------------------------
@@ -237,14 +277,23 @@ class Coeffs:
             self._h = None
 
     @property
+    def ldx(self) -> int:
+        return hz_field_ldx(self.grid.nx)
+
+    @property
     def field_shape(self):
         g = self.grid
         return (g.nz_local + 2, g.ny, g.nx)
 
-    def alloc_field(self, nrhs: int, device="cuda"):
+    def alloc_field(self, nrhs: int, device="cuda", pin_memory: bool = False):
+        """Zeroed field buffer in the ABI layout [nrhs][nz_local+2][ny][ldx], returned as its
+        [nrhs][nz_local+2][ny][nx] view (the pad columns are not part of the field)."""
         import torch
         dt = torch.complex64 if self.dtype == HZ_C64 else torch.complex128
-        return torch.zeros((nrhs,) + self.field_shape, dtype=dt, device=device)
+        g = self.grid
+        full = torch.zeros((nrhs, g.nz_local + 2, g.ny, self.ldx), dtype=dt, device=device,
+                           pin_memory=pin_memory and str(device) == "cpu")
+        return full[..., :g.nx]
 
 
 def hz_assemble_coeffs(ctx: Ctx, nx: int, ny: int, nz_global: int, h: float, v, freq: float, table: Table,
@@ -270,11 +319,14 @@ def hz_coeffs_export(c: Coeffs, record=None, pml=None) -> None:
 def hz_apply_impedance(c: Coeffs, u, au, nrhs: Optional[int] = None, stream=None) -> None:
     if nrhs is None:
         nrhs = u.shape[0]
-    _check(_lib.hz_apply_impedance(c._h, _ptr(u), _ptr(au), nrhs, _stream_ptr(stream)), "hz_apply_impedance")
+    _check(_lib.hz_apply_impedance(c._h, _fptr(c, u, "u"), _fptr(c, au, "au"), nrhs, _stream_ptr(stream)),
+           "hz_apply_impedance")
 
 
 def hz_solve(c: Coeffs, b, x, nrhs: Optional[int] = None, rtol=1e-6, max_iter=20000, replace_every=50,
              check_every=10, timing=False, ell=1, stall_window=0, stream=None):
+    """Zero for rtol / max_iter / replace_every / check_every / ell / stall_window selects the default
+    (include/hz.h); replace_every < 0 turns residual replacement off."""
     """Returns (status, relres[nrhs], iters[nrhs], stats dict).  ell = 1: BiCGSTAB; 2: BiCGStab(2)."""
     if nrhs is None:
         nrhs = b.shape[0]
@@ -282,7 +334,7 @@ def hz_solve(c: Coeffs, b, x, nrhs: Optional[int] = None, rtol=1e-6, max_iter=20
     rel = (ct.c_double * nrhs)()
     its = (ct.c_int * nrhs)()
     stt = hz_solve_stats()
-    st = _check(_lib.hz_solve(c._h, _ptr(b), _ptr(x), nrhs, ct.byref(o), rel, its, ct.byref(stt),
+    st = _check(_lib.hz_solve(c._h, _fptr(c, b, "b"), _fptr(c, x, "x"), nrhs, ct.byref(o), rel, its, ct.byref(stt),
                               _stream_ptr(stream)), "hz_solve")
     stats = {k: getattr(stt, k) for k, _ in hz_solve_stats._fields_}
     return st, np.array(rel[:]), np.array(its[:]), stats
@@ -296,14 +348,15 @@ def hz_point_sources(c: Coeffs, nodes, b, amps=None, consistent=True, stream=Non
         a = np.ascontiguousarray(np.stack([av.real, av.imag], axis=1))
     _check(_lib.hz_point_sources(c._h, n.shape[0], n.ctypes.data_as(_P(ct.c_longlong)),
                                  a.ctypes.data_as(_P(ct.c_double)) if a is not None else None,
-                                 1 if consistent else 0, _ptr(b), _stream_ptr(stream)), "hz_point_sources")
+                                 1 if consistent else 0, _fptr(c, b, "b"), _stream_ptr(stream)), "hz_point_sources")
 
 
 def hz_eqerror(c: Coeffs, u_ref, u, src_xyz, npml_mask: int, ball_cells: float = 2.0, stream=None) -> float:
     """The paper's err (reading A20) between two slab wavefields (see include/hz.h)."""
     src = (ct.c_longlong * 3)(*[int(t) for t in src_xyz])
     out = ct.c_double()
-    _check(_lib.hz_eqerror(c._h, _ptr(u_ref), _ptr(u), src, npml_mask, ball_cells, ct.byref(out), _stream_ptr(stream)),
+    _check(_lib.hz_eqerror(c._h, _fptr(c, u_ref, "u_ref"), _fptr(c, u, "u"), src, npml_mask, ball_cells, ct.byref(out),
+                           _stream_ptr(stream)),
            "hz_eqerror")
     return out.value
 

@@ -15,6 +15,8 @@ from .configs import (  # noqa: F401
     get_config,
     velocity_model,
     velocity_slab,
+    crop_config,
+    CROP_SHAPE,
     source_nodes,
     random_field,
     rng_for,

@@ -181,6 +181,8 @@ def velocity_slab(cfg: Config, z0: int = 0, nz_local: Optional[int] = None,
     """
     if nz_local is None:
         nz_local = cfg.nz - z0
+    if "origin" in cfg.extra:
+        return _crop_slab(cfg, z0, nz_local, device)
     nx, ny, h, npml = cfg.nx, cfg.ny, cfg.h, cfg.npml
     k = np.arange(z0, z0 + nz_local, dtype=np.float64)
     if cfg.index == 1:
@@ -211,11 +213,55 @@ def velocity_slab(cfg: Config, z0: int = 0, nz_local: Optional[int] = None,
     raise ValueError(cfg.index)
 
 
-def _cfg4_eval(cfg: Config, draws, k) -> np.ndarray:
+# ----------------------------------------------------------------------------------------
+# seeded crops of configs 4-5 (SURVEY §8(d) "Oracle timing": solve parity of the large models on a
+# 201×201×101 window of the same generated model, with its own npml = 8 PML, same f and h, 1 source)
+# ----------------------------------------------------------------------------------------
+
+CROP_SHAPE = (101, 201, 201)   # (nz, ny, nx)
+
+
+def crop_config(ci: int, freq: Optional[float] = None) -> Config:
+    """The seeded 201×201×101 crop of config 4 or 5: a Config whose velocity is the parent model's
+    on the window at extra["origin"] = (x0, y0, z0) (global node indices), npml = 8, the parent's h
+    and frequency (config 4: 5 or 10 Hz), one source (see source_nodes)."""
+    parent = get_config(ci)
+    if ci not in (4, 5):
+        raise ValueError("crops are defined for configs 4 and 5")
+    nz, ny, nx = CROP_SHAPE
+    rng = rng_for(ci, counter=9001)
+    x0 = int(rng.integers(0, parent.nx - nx + 1))
+    y0 = int(rng.integers(0, parent.ny - ny + 1))
+    z0 = int(rng.integers(0, parent.nz - nz + 1))
+    f = parent.freq if freq is None else float(freq)
+    if f not in parent.freqs:
+        raise ValueError(f"config {ci} is defined at {parent.freqs} Hz")
+    return Config(ci, parent.name + "-crop", nx, ny, nz, parent.h, (f,), 8, "c64", 1,
+                  f"seeded {nx}x{ny}x{nz} crop of BASELINE config {ci} at origin {(x0, y0, z0)}, {f} Hz",
+                  extra={"origin": (x0, y0, z0), "parent": parent})
+
+
+def _crop_slab(cfg: Config, z0: int, nz_local: int, device=None) -> np.ndarray:
+    parent = cfg.extra["parent"]
+    gx0, gy0, gz0 = cfg.extra["origin"]
+    if cfg.index == 4:
+        draws = _cfg4_draws(parent)
+        k = np.arange(gz0 + z0, gz0 + z0 + nz_local, dtype=np.float64)
+        win = Config(**{**parent.__dict__, "nx": cfg.nx, "ny": cfg.ny})
+        out = np.empty((nz_local, cfg.ny, cfg.nx))
+        for a in range(0, nz_local, 8):
+            b = min(nz_local, a + 8)
+            out[a:b] = _cfg4_eval(win, draws, k[a:b], gx0, gy0)
+        return out
+    return _cfg5_slab(parent, gz0 + z0, nz_local, device, gx0, gy0, cfg.nx, cfg.ny)
+
+
+def _cfg4_eval(cfg: Config, draws, k, x0: int = 0, y0: int = 0) -> np.ndarray:
+    """Model at global planes k, columns x0 .. x0+cfg.nx-1, rows y0 .. y0+cfg.ny-1."""
     folds, zbar, vel, faults = draws
     nx, ny, h, npml = cfg.nx, cfg.ny, cfg.h, cfg.npml
-    x = (np.arange(nx) - npml) * h
-    y = (np.arange(ny) - npml) * h
+    x = (np.arange(x0, x0 + nx) - npml) * h
+    y = (np.arange(y0, y0 + ny) - npml) * h
     z = (np.asarray(k, dtype=np.float64) - npml) * h
     Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
     for (xf, yf, zf, strike, dip, throw) in faults:
@@ -236,15 +282,23 @@ def _cfg4_eval(cfg: Config, draws, k) -> np.ndarray:
     return vel[layer]
 
 
-def _cfg5_slab(cfg: Config, z0: int, nz_local: int, device=None) -> np.ndarray:
+def _cfg5_slab(cfg: Config, z0: int, nz_local: int, device=None, x0: int = 0, y0: int = 0,
+               nxw: Optional[int] = None, nyw: Optional[int] = None) -> np.ndarray:
+    """Config-5 model at global planes z0 .. z0+nz_local-1 over the window of nxw × nyw nodes at
+    (x0, y0) (default: the whole plane).  The noise of a plane is drawn for the whole grid (one
+    Philox stream per plane), so a window equals the same window of the full model."""
     nx, ny, h, npml = cfg.nx, cfg.ny, cfg.h, cfg.npml
+    nxw = nx if nxw is None else nxw
+    nyw = ny if nyw is None else nyw
     ker = _grf_kernel(h)
     half = (len(ker) - 1) // 2
     planes = list(range(z0 - half, z0 + nz_local + half))
-    noise = np.empty((len(planes), ny + 2 * half, nx + 2 * half), dtype=np.float32)
+    noise = np.empty((len(planes), nyw + 2 * half, nxw + 2 * half), dtype=np.float32)
     for n, p in enumerate(planes):
-        noise[n] = rng_for(5, counter=p + (1 << 40)).standard_normal(
+        full = rng_for(5, counter=p + (1 << 40)).standard_normal(
             (ny + 2 * half, nx + 2 * half), dtype=np.float32)
+        noise[n] = full[y0:y0 + nyw + 2 * half, x0:x0 + nxw + 2 * half]
+    nx, ny = nxw, nyw
     norm = float(np.sqrt(np.sum(ker ** 2)) ** 3)
     if device is not None:
         import torch
@@ -268,8 +322,8 @@ def _cfg5_slab(cfg: Config, z0: int, nz_local: int, device=None) -> np.ndarray:
         g = np.tensordot(sw(g, len(ker), axis=0), ker, axes=([3], [0]))
     g = g / norm
     v = 3000.0 + 600.0 * g
-    x = (np.arange(nx) - npml) * h
-    y = (np.arange(ny) - npml) * h
+    x = (np.arange(x0, x0 + nx) - npml) * h
+    y = (np.arange(y0, y0 + ny) - npml) * h
     z = (np.arange(z0, z0 + nz_local) - npml) * h
     for (zi, a, b, dv, xc, yc) in _cfg5_draws(cfg):
         surf = zi + a * (x[None, :] - xc) + b * (y[:, None] - yc)
@@ -284,6 +338,8 @@ def velocity_model(cfg: Config) -> np.ndarray:
 def source_nodes(cfg: Config) -> np.ndarray:
     """Global (x, y, z) node indices of the config's point sources, int64 [nsrc][3]."""
     n, npml = cfg.nx, cfg.npml
+    if "origin" in cfg.extra:   # crop: one source at the window's centre column, one node below its PML
+        return np.array([[cfg.nx // 2, cfg.ny // 2, npml + 1]], dtype=np.int64)
     if cfg.index == 1:
         return np.array([[cfg.nx // 2, cfg.ny // 2, cfg.nz // 2]], dtype=np.int64)
     if cfg.index == 2:

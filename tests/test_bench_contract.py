@@ -12,7 +12,7 @@ from conftest import ROOT
 def test_reference_arm_json_line():
     env = dict(os.environ, OMP_NUM_THREADS="1")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
-                          "--steps", "1", "--warmup", "0", "--ref-iters", "2"],
+                          "--steps", "1", "--warmup", "0", "--cpu-planes", "3"],
                          capture_output=True, text=True, cwd=ROOT, env=env, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]

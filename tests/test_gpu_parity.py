@@ -2,7 +2,6 @@
 coefficient record, PML arrays, operator apply (several tiles + ragged tails, both precisions, both
 mass formulations, batched RHS), decomposition invariance, point sources, and sampled rows at the
 full BASELINE sizes in the launch configuration bench.py times."""
-import os
 import zlib
 
 import numpy as np
@@ -248,9 +247,9 @@ def test_domain_errors(hz, ctx, table):
 
 @pytest.mark.parametrize("mass", ["eq8", "colloc"])
 def test_apply_tiled_launches(hz, ctx, table, ga_table, mass):
-    """complex64 tiled launches (x/y-PML tiles, z-PML tiles, PML-free tiles): odd nx (ragged tile width),
-    clamped overlapping last tiles in x and y, 3 RHS (one full RHS pair and a pair with one idle slot)
-    — full oracle comparison, every point individually."""
+    """complex64 tiled launch (x/y-PML tiles, z-PML chunks, PML-free chunks in one launch): odd nx (ragged
+    row and tile width), ragged last tiles in x and y, 3 RHS (one full RHS pair and a pair with one idle
+    slot) — full oracle comparison, every point individually."""
     rng = np.random.default_rng(77)
     nz, ny, nx, h, f, npml = 21, 27, 301, 20.0, 8.0, 4
     v = rng.uniform(1600.0, 4200.0, (nz, ny, nx))
@@ -266,23 +265,31 @@ def test_apply_tiled_launches(hz, ctx, table, ga_table, mass):
     assert err.max() <= 1e-4, np.unravel_index(err.argmax(), err.shape)
 
 
-def test_apply_reference_path_c64(hz, ctx, table, ga_table):
-    """HZ_NO_CP=1 (read at assemble) routes complex64 through the register-path / bulk-copy kernels kept
-    as the A/B reference: same oracle parity as the default RHS-fused launch."""
-    rng = np.random.default_rng(78)
-    nz, ny, nx, h, f, npml = 19, 23, 301, 20.0, 8.0, 4
+@pytest.mark.parametrize("nx", [63, 64, 65, 66, 129, 130])
+def test_apply_tile_edges_and_pads(hz, ctx, table, ga_table, nx):
+    """complex64 tensor-map tiles at every alignment of the row against the 32-byte pitch (nx mod 4) and
+    the tile width (one and several x tiles), several y tiles with a ragged last one, 3 RHS (a pair and a
+    pair with an idle slot): every point against the oracle, and the pad columns [nx, ldx) of the output
+    written as zeros (the Krylov dot products run over whole pitched rows)."""
+    rng = np.random.default_rng(nx)
+    nz, ny, h, f, npml = 9, 37, 20.0, 8.0, 3
     v = rng.uniform(1600.0, 4200.0, (nz, ny, nx))
-    u = synth.random_field((2, nz, ny, nx), seed=10)
-    os.environ["HZ_NO_CP"] = "1"
-    try:
-        C = assemble(hz, ctx, table, v, h, f, npml, "c64")
-    finally:
-        del os.environ["HZ_NO_CP"]
+    u = synth.random_field((3, nz, ny, nx), seed=nx)
+    C = assemble(hz, ctx, table, v, h, f, npml, "c64")
+    ud = C.alloc_field(3)
+    ud[:, 1:-1] = torch.from_numpy(u).cuda()
+    full = torch.full((3, nz + 2, ny, C.ldx), complex(7.0, -7.0), dtype=torch.complex64, device="cuda")
+    aud = full[..., :nx]
     l0 = hz.hz_kernel_launch_count()
-    got = gpu_apply(hz, C, u)
-    assert hz.hz_kernel_launch_count() - l0 == 2          # general + bulk-copy interior launches
+    hz.hz_apply_impedance(C, ud, aud)
+    torch.cuda.synchronize()
+    assert hz.hz_kernel_launch_count() - l0 == 1
+    got = aud[:, 1:-1].cpu().numpy()
     ref = op.apply(op.assemble(oracle_problem(v, h, f, npml, ga_table, "c64")), u)
-    assert rel(got, ref) <= TOL["c64"], rel(got, ref)
+    err = np.abs(got - ref) / (np.abs(ref) + 1e-3 * np.abs(ref).max())
+    assert rel(got, ref) <= TOL["c64"] and err.max() <= 1e-4, (rel(got, ref), np.unravel_index(err.argmax(), err.shape))
+    assert bool((full[:, 1:-1, :, nx:] == 0).all())
+    assert bool((full[:, 0] == complex(7.0, -7.0)).all())      # halo planes are not written
 
 
 @pytest.mark.parametrize("which", ["Gm", "G4"])

@@ -1,7 +1,10 @@
-"""CPU checks of the complex64 apply's tile planner (host logic in libhz, include/hz_debug.h): for many
-plane sizes and PML widths every point of the plane is stored by exactly one tile, every tile respects
-the kernel's shape limits, and a tile runs the x/y-PML body exactly when its stored points are PML points
-(a tile is wholly inside or outside the x/y-PML)."""
+"""CPU checks of the complex64 tensor-map apply's work-list planner (host logic in libhz,
+include/hz_debug.h): for many grid sizes and PML widths every (point, plane) of the slab — pad columns
+included — is computed by exactly one work item (tile x0 computes the columns [x0 − 1, x0 + tx − 1)),
+the tile shape respects the kernel's limits (tx a multiple of 4, ≤ 64, ty·tx/2 ≤ 256 threads), and the
+item's body matches the PML it
+touches: the PML-free body only on planes and tiles without PML points, the z-PML body
+only on tiles without x/y-PML points."""
 import ctypes
 
 import numpy as np
@@ -9,45 +12,61 @@ import pytest
 
 hz = pytest.importorskip("paper_2108_08730_b200.hz", reason="libhz.so not built")
 
-CP_HALO = 768
 
-
-def plan(nx, ny, lo_x, hi_x, lo_y, hi_y, ny_rows):
+def plan(nx, ny, nz, lo, hi, slots=296, ngroups=1):
     lib = ctypes.CDLL(hz._LIBPATH)
     f = lib.hz_debug_plan_tiles
     f.restype = ctypes.c_int
-    f.argtypes = [ctypes.c_int] * 7 + [ctypes.POINTER(ctypes.c_int), ctypes.c_int]
-    n = f(nx, ny, lo_x, hi_x, lo_y, hi_y, ny_rows, None, 0)
+    f.argtypes = [ctypes.c_int] * 11 + [ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    args = [nx, ny, nz, lo[0], hi[0], lo[1], hi[1], lo[2], hi[2], slots, ngroups]
+    n = f(*args, None, 0, None)
     assert n > 0
-    buf = (ctypes.c_int * (9 * n))()
-    assert f(nx, ny, lo_x, hi_x, lo_y, hi_y, ny_rows, buf, n) == n
-    return np.frombuffer(buf, dtype=np.int32).reshape(n, 9).copy()
+    buf = (ctypes.c_int * (5 * n))()
+    wh = (ctypes.c_int * 2)()
+    assert f(*args, buf, n, wh) == n
+    return np.frombuffer(buf, dtype=np.int32).reshape(n, 5).copy(), wh[0], wh[1]
 
 
-CASES = [(101, 101, 8), (41, 41, 8), (801, 801, 8), (201, 201, 10), (45, 21, 4), (301, 27, 4), (3, 3, 1),
-         (7, 5, 0), (64, 66, 0), (65, 3, 1), (130, 129, 2), (17, 250, 5), (5, 9, 3)]
+CASES = [(101, 101, 101, 8), (41, 41, 41, 8), (801, 801, 19, 8), (201, 201, 101, 10), (45, 21, 9, 4),
+         (301, 27, 12, 4), (3, 3, 3, 1), (7, 5, 4, 0), (64, 66, 5, 0), (65, 3, 3, 1), (130, 129, 7, 2),
+         (17, 250, 6, 5), (5, 9, 3, 3), (1201, 40, 6, 8)]
 
 
-@pytest.mark.parametrize("rows", [1, 2])
-@pytest.mark.parametrize("nx,ny,npml", CASES)
-def test_tiles_partition_the_plane(nx, ny, npml, rows):
-    # PML-free range of an axis as libhz derives it from the profile: (npml, n-1-npml) exclusive of the
-    # half-step stretch at the boundary node (lo = npml + 1, hi = n - 2 - npml); no PML: [0, n-1]
-    def rng(n):
-        if npml == 0:
-            return 0, n - 1
-        return npml + 1, n - 2 - npml
-    lo_x, hi_x = rng(nx)
-    lo_y, hi_y = rng(ny)
-    T = plan(nx, ny, lo_x, hi_x, lo_y, hi_y, rows)
-    count = np.zeros((ny, nx), np.int32)
-    in_pml_x = np.ones(nx, bool) if hi_x < lo_x else ~((np.arange(nx) >= lo_x) & (np.arange(nx) <= hi_x))
-    in_pml_y = np.ones(ny, bool) if hi_y < lo_y else ~((np.arange(ny) >= lo_y) & (np.arange(ny) <= hi_y))
-    for x0, y0, tx, ty, xs, ys, xe, ye, pml in T:
-        assert 1 <= tx <= 64 and ty >= 2 and ty % 2 == 0
-        assert tx * ty <= 256 * rows and (tx + 2) * (ty + 2) <= CP_HALO
-        assert 0 <= x0 <= xs < xe <= x0 + tx <= nx and 0 <= y0 <= ys < ye <= y0 + ty <= ny
-        count[ys:ye, xs:xe] += 1
-        stored_pml = in_pml_x[xs:xe][None, :] | in_pml_y[ys:ye][:, None]
-        assert stored_pml.all() if pml else not stored_pml.any()
-    assert (count == 1).all(), np.argwhere(count != 1)[:5]
+def pml_range(n, npml):
+    # PML-free range as libhz derives it from the profile: lo = npml + 1, hi = n - 2 - npml; no PML: [0, n-1]
+    if npml == 0:
+        return 0, n - 1
+    return npml + 1, n - 2 - npml
+
+
+@pytest.mark.parametrize("ngroups", [1, 3])
+@pytest.mark.parametrize("nx,ny,nz,npml", CASES)
+def test_items_partition_the_slab(nx, ny, nz, npml, ngroups):
+    lo, hi = zip(*[pml_range(n, npml) for n in (nx, ny, nz)])
+    items, tx, ty = plan(nx, ny, nz, lo, hi, ngroups=ngroups)
+    ldx = hz.hz_field_ldx(nx)
+    assert ldx % 4 == 0 and ldx >= nx > ldx - 4
+    assert tx % 4 == 0 and 4 <= tx <= 64 and ty == 256 // (tx // 2)
+    ntx = -(-(ldx + 1) // tx)
+    assert (ntx - 1) * tx - 1 < ldx                     # no tile wholly outside the pitched row
+    count = np.zeros((nz, ny, ntx * tx + 1), np.int32)  # column c + 1 ↔ x = c (x = −1 first)
+
+    def in_pml(n, a, b):
+        idx = np.arange(n)
+        return np.ones(n, bool) if b < a else ~((idx >= a) & (idx <= b))
+    px, py, pz = in_pml(nx, lo[0], hi[0]), in_pml(ny, lo[1], hi[1]), in_pml(nz, lo[2], hi[2])
+    for x0, y0, z0, z1, mode in items:
+        assert x0 % tx == 0 and y0 % ty == 0 and 0 <= z0 < z1 <= nz
+        count[z0:z1, y0:y0 + ty, x0:x0 + tx] += 1          # x ∈ [x0 − 1, x0 + tx − 1)
+        xs, ys = slice(max(x0 - 1, 0), min(x0 + tx - 1, nx)), slice(y0, min(y0 + ty, ny))
+        xy_pml = px[xs].any() or py[ys].any()
+        if mode == 2:
+            assert xy_pml
+        else:
+            assert not xy_pml
+            assert (mode == 1) == bool(pz[z0:z1].any())
+    assert (count[:, :ny, 1:ldx + 1] == 1).all()
+    # x/y-PML items first (heavier, scheduled first)
+    modes = items[:, 4]
+    if (modes == 2).any() and (modes != 2).any():
+        assert np.max(np.nonzero(modes == 2)) < np.min(np.nonzero(modes != 2))
