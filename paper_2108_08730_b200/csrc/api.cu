@@ -260,6 +260,7 @@ struct hz_coeffs {
   struct TmPlan {
     DBuf work;
     int n_items = 0;
+    int grid = 1;   // resident CTAs: SMs × CTAs per SM
   };
   std::map<int, std::unique_ptr<TmPlan>> tm_plans;
   std::unique_ptr<SolverWork> work;
@@ -626,13 +627,13 @@ hz_status tm_encoder() {
 }
 
 // Tile geometry: tile i computes the columns [i·tx − 1, (i+1)·tx − 1) (apply27_tm.cuh); ntx tiles of
-// tx ∈ {16, 32, 64} columns cover the pitched row (the pad columns too, which the apply writes as
-// zeros): the width with the fewest box columns ntx·(tx + 4) (halo included), the wider on a tie;
-// rows ty = 512/tx; the maps start at the slab's first in-grid storage plane (planes outside the
-// global grid read zeros).
+// tx ∈ {32, 64} columns cover the pitched row (the pad columns too, which the apply writes as zeros):
+// the width with the fewest box columns ntx·(tx + 4) (halo included), the wider on a tie; rows
+// ty = 768/tx; the maps start at the slab's first in-grid storage plane (planes outside the global
+// grid read zeros).
 int tm_tile_width(int ldx) {
   int best = TM_MAXTX, cost = INT_MAX;
-  for (int tx = TM_MAXTX; tx >= 16; tx /= 2) {
+  for (int tx = TM_MAXTX; tx >= 32; tx /= 2) {
     const int ntx = (ldx + 1 + tx - 1) / tx;
     if (ntx * (tx + 4) < cost) { cost = ntx * (tx + 4); best = tx; }
   }
@@ -736,6 +737,7 @@ const hz_coeffs::TmPlan* tm_plan(hz_coeffs* c, int ngroups, int nr) {
   tm_build_items(c->grid, c->ldx, c->tm_tx, c->tm_ty, c->lo, c->hi, slots, ngroups, items);
   std::unique_ptr<hz_coeffs::TmPlan> pl(new hz_coeffs::TmPlan);
   pl->n_items = (int)items.size();
+  pl->grid = std::max(1, slots / std::max(1, ngroups));
   if (pl->work.ensure(std::max<size_t>(1, items.size()) * sizeof(int4)) != cudaSuccess) return nullptr;
   if (!items.empty() && cudaMemcpy(pl->work.p, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice) != cudaSuccess)
     return nullptr;
@@ -785,11 +787,12 @@ hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int 
     const hz_coeffs::TmPlan* pl = tm_plan(c, ng, nr);
     if (!pl) { set_error("tm_plan: device allocation / copy failed"); return HZ_ERR_CUDA; }
     p.tm_work = pl->work.template as<int4>();
-    p.tm_nblocks = pl->n_items;
+    p.tm_nitems = pl->n_items;
+    p.tm_nblocks = std::max(1, std::min(pl->n_items, pl->grid));   // persistent CTAs
     L.w = &c->tmap_w;
     L.u = tm_umap(c, p.u, nrhs);
     if (!L.u) return HZ_ERR_CUDA;
-    nb = pl->n_items;
+    nb = p.tm_nblocks;
   } else {
     ApplyParams<R, S> pp = p;
     nb = apply_plan<R, S>(pp);

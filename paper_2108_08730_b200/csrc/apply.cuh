@@ -48,11 +48,12 @@ struct ApplyParams {
   // general launch work list per RHS: the boundary z-chunks (low, high) × all warps (nbx CTAs each),
   // then the interior z-chunks × the "frame" of warps outside the box (nbx_frame CTAs each)
   int nbound, nbx_frame, frame_warps, gen_blocks;
-  // complex64 tensor-map launch (apply27_tm): work items (tm_item), x/y-PML tiles first;
-  // tm_nblocks = items = dot partial slots per RHS; tiles of tm_tx × tm_ty points; tm_org = first
-  // storage plane covered by the tensor maps (planes outside the global grid are zero-filled)
+  // complex64 tensor-map launch (apply27_tm): tm_nitems work items (tm_item), x/y-PML tiles first,
+  // walked round-robin by a persistent grid of tm_nblocks CTAs (= dot partial slots per RHS); tiles
+  // of tm_tx × tm_ty points; tm_org = first storage plane covered by the tensor maps (planes outside
+  // the global grid are zero-filled)
   const int4* tm_work;
-  int tm_nblocks, tm_tx, tm_ty, tm_org;
+  int tm_nitems, tm_nblocks, tm_tx, tm_ty, tm_org;
   const S* v;                 // [nzl+2][ny][ldx] velocity incl. halo planes
   const S* w;                 // [nzl+2][ny][ldx] 1/v² incl. halo planes (apply input)
   const S* gam;               // GAm rule (A19): [5][nzl+2][ny][ldx] row weights (t1, t2, μ0, μ1, μ2)

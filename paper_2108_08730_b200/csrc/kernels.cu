@@ -720,60 +720,22 @@ static cudaError_t launch_one(const ApplyParams<R, S>& p, long long nb, cudaStre
 static thread_local int g_last_apply_launches = 0;
 int apply_last_launches() { return g_last_apply_launches; }
 
-// complex64 tensor-map launch: one launch over the work list (x/y-PML items, then the rest);
-// blockIdx.y = group of NR right-hand sides (1 for a single RHS, else 2).
-template <int NR, bool COLLOC, int EPI, bool GAM>
-static cudaError_t launch_tm_t(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
-  const int ngroups = (nrhs + NR - 1) / NR;
-  const int nitems = p.tm_nblocks;
-  g_last_apply_launches = nitems > 0 ? 1 : 0;
-  if (nitems <= 0) return cudaSuccess;
-  auto kern = apply27_tm<NR, COLLOC, EPI, GAM>;
-  const size_t smem = tm_smem_bytes(p.tab_n, p.tm_tx, p.tm_ty, NR);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  kern<<<dim3((unsigned)nitems, (unsigned)ngroups), TM_NTHR, smem, s>>>(*L.w, *L.u, p);
-  return cudaGetLastError();
-}
-template <int NR, bool COLLOC, int EPI>
-static cudaError_t launch_tm(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, cudaStream_t s) {
-  return p.gam != nullptr ? launch_tm_t<NR, COLLOC, EPI, true>(L, p, nrhs, s) : launch_tm_t<NR, COLLOC, EPI, false>(L, p, nrhs, s);
-}
-// RHS per CTA: two for a plain apply of several fields (the coefficients are built once for both);
-// one when a dot epilogue runs (its fp64 partials would not fit the register budget of two)
+// RHS per CTA of the complex64 tensor-map apply: two for a plain apply of several fields (the
+// coefficients are built once for both); one when a dot epilogue runs (its fp64 partials would not
+// fit the register budget of two)
 int tm_group(int nrhs, int epi) { return (nrhs > 1 && epi == EPI_PLAIN) ? 2 : 1; }
 
-template <bool COLLOC, int EPI>
-static cudaError_t launch_tm_epi(const TmLaunch& L, ApplyParams<float, float> p, int nrhs, cudaStream_t s) {
-  p.nrhs = nrhs;
-  if constexpr (EPI == EPI_PLAIN) {
-    if (tm_group(nrhs, EPI) == 2) return launch_tm<2, COLLOC, EPI>(L, p, nrhs, s);
-  }
-  return launch_tm<1, COLLOC, EPI>(L, p, nrhs, s);
-}
+// the tile-width instantiations live in their own translation units (tm64.cu, tm32.cu)
 cudaError_t launch_apply_tm(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, bool colloc, int epi,
                             cudaStream_t s) {
-  switch (epi) {
-    case EPI_PLAIN: return colloc ? launch_tm_epi<true, EPI_PLAIN>(L, p, nrhs, s) : launch_tm_epi<false, EPI_PLAIN>(L, p, nrhs, s);
-    case EPI_DOT1: return colloc ? launch_tm_epi<true, EPI_DOT1>(L, p, nrhs, s) : launch_tm_epi<false, EPI_DOT1>(L, p, nrhs, s);
-    case EPI_DOT4: return colloc ? launch_tm_epi<true, EPI_DOT4>(L, p, nrhs, s) : launch_tm_epi<false, EPI_DOT4>(L, p, nrhs, s);
-  }
+  g_last_apply_launches = p.tm_nitems > 0 ? 1 : 0;
+  if (p.tm_nitems <= 0) return cudaSuccess;
+  if (p.tm_tx == 64) return launch_apply_tm_tx<64>(L, p, nrhs, colloc, epi, s);
+  if (p.tm_tx == 32) return launch_apply_tm_tx<32>(L, p, nrhs, colloc, epi, s);
   return cudaErrorInvalidValue;
 }
-
 int tm_occupancy(int tab_n, int tx, int ty, int nr) {
-  int nb = 0;
-  if (nr == 1)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_tm<1, false, EPI_DOT4, false>, TM_NTHR,
-                                                  tm_smem_bytes(tab_n, tx, ty, 1));
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, apply27_tm<2, false, EPI_DOT4, false>, TM_NTHR,
-                                                  tm_smem_bytes(tab_n, tx, ty, 2));
-  return nb > 0 ? nb : 1;
+  return tx == 64 ? tm_occupancy_tx<64>(tab_n, nr) : tm_occupancy_tx<32>(tab_n, nr);
 }
 
 template <typename R, typename S, bool COLLOC, int EPI>

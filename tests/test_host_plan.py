@@ -1,7 +1,7 @@
 """CPU checks of the complex64 tensor-map apply's work-list planner (host logic in libhz,
 include/hz_debug.h): for many grid sizes and PML widths every (point, plane) of the slab — pad columns
 included — is computed by exactly one work item (tile x0 computes the columns [x0 − 1, x0 + tx − 1)),
-the tile shape respects the kernel's limits (tx a multiple of 4, ≤ 64, ty·tx/2 ≤ 256 threads), and the
+the tile shape respects the kernel's limits (tx ∈ {32, 64}, ty·tx/2 = 384 threads), and the
 item's body matches the PML it
 touches: the PML-free body only on planes and tiles without PML points, the z-PML body
 only on tiles without x/y-PML points."""
@@ -46,7 +46,7 @@ def test_items_partition_the_slab(nx, ny, nz, npml, ngroups):
     items, tx, ty = plan(nx, ny, nz, lo, hi, ngroups=ngroups)
     ldx = hz.hz_field_ldx(nx)
     assert ldx % 4 == 0 and ldx >= nx > ldx - 4
-    assert tx % 4 == 0 and 4 <= tx <= 64 and ty == 256 // (tx // 2)
+    assert tx in (32, 64) and ty == 384 // (tx // 2)
     ntx = -(-(ldx + 1) // tx)
     assert (ntx - 1) * tx - 1 < ldx                     # no tile wholly outside the pitched row
     count = np.zeros((nz, ny, ntx * tx + 1), np.int32)  # column c + 1 ↔ x = c (x = −1 first)
