@@ -6,6 +6,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <atomic>
 #include <climits>
 #include <condition_variable>
@@ -710,10 +711,17 @@ void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], 
   const int nin = std::max(1, (int)std::lround((double)nch * (zh - zl) / std::max(1, nzl)));
   const int nxy = std::max(1, std::min(std::max(1, nzl / 2), (int)std::lround(nch * 1.5)));
   out.clear();
-  for (int k = 0; k < nxy; k++) {   // chunk-major: concurrently running CTAs share z-planes in L2
-    const int a = (int)((long long)nzl * k / nxy), b = (int)((long long)nzl * (k + 1) / nxy);
-    if (b > a)
-      for (auto& t : xy) out.push_back(tm_item(t.first, t.second, a, b, TM_PMLXY));
+  // x/y-PML tiles: nxy chunks, also cut at the z-PML boundaries so that each chunk's mode is exact
+  std::vector<int> cuts;
+  for (int k = 0; k <= nxy; k++) cuts.push_back((int)((long long)nzl * k / nxy));
+  cuts.push_back(zl);
+  cuts.push_back(zh);
+  std::sort(cuts.begin(), cuts.end());
+  cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+  for (size_t k = 0; k + 1 < cuts.size(); k++) {   // chunk-major: concurrently running CTAs share z-planes in L2
+    const int a = cuts[k], b = cuts[k + 1];
+    const int mode = TM_PMLXY | ((a < zl || b > zh) ? TM_PMLZ : 0);
+    for (auto& t : xy) out.push_back(tm_item(t.first, t.second, a, b, mode));
   }
   for (auto& t : in) {
     if (zl > 0) out.push_back(tm_item(t.first, t.second, 0, zl, TM_PMLZ));

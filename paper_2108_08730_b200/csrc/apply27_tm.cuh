@@ -45,7 +45,8 @@ namespace hz {
 constexpr int TM_NTHR = 384;     // threads per CTA (12 warps, one CTA per SM, ≤ 168 registers)
 constexpr int TM_MAXTX = 64;     // widest tile
 
-// PML mode of a work item: 0 none, 1 z-PML planes only, 2 x/y-PML columns/rows (+ z)
+// PML mode bits of a work item: TM_PMLZ the chunk holds z-PML planes, TM_PMLXY the tile holds x/y-PML
+// columns / rows; TM_LEAN neither
 enum { TM_LEAN = 0, TM_PMLZ = 1, TM_PMLXY = 2 };
 
 // work item {x0 | y0 << 16, z0 | z1 << 16, mode, 0}: tile origin (x0, y0), local planes [z0, z1)
@@ -315,11 +316,12 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
 #pragma unroll
     for (int k = 0; k < KK; k++) part[r][k] = 0.0;
 
-  // ---- one work item with body PM (TM_LEAN / TM_PMLZ / TM_PMLXY)
+  // ---- one work item with body PM (mode bits TM_PMLZ | TM_PMLXY)
   auto run_item = [&](auto PMc, const int4 item) {
     constexpr int PM = decltype(PMc)::value;
     constexpr bool PML = PM != TM_LEAN;
-    constexpr bool PXY = PM == TM_PMLXY;
+    constexpr bool PXY = (PM & TM_PMLXY) != 0;
+    constexpr bool PZ = (PM & TM_PMLZ) != 0;
     const int X0 = item.x & 0xffff, Y0 = item.x >> 16;
     const int zc0 = item.y & 0xffff, zc1 = item.y >> 16;
     const int nplanes = zc1 - zc0 + 2;   // input planes zc0-1 .. zc1
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
       const float* sw = reinterpret_cast<const float*>(st) + sbw;
       const int zg = p.z0 + pl;
       bool zp_prev = false, zp_cur = false, zp_next = false, zcorr = false;
-      if (PML) {
+      if (PZ) {
         zp_prev = do_prev && (zg - 1 < zlo || zg - 1 > zhi);
         zp_cur = (pl >= zc0 && pl < zc1) && (zg < zlo || zg > zhi);
         zp_next = do_next && (zg + 1 < zlo || zg + 1 > zhi);
@@ -445,7 +447,7 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
         if (GAM && pl + 2 < zc1) gam_load(pl + 3);   // the next call's rows
       }
       C dzp = z2, dzc = z2, dzn = z2;
-      if (PML && zcorr) {
+      if (PZ && zcorr) {
         if (zp_prev) dzp = p.dp[2][zg - 1];
         if (zp_cur) {
           const C dz = cadd(p.dm[2][zg], p.dp[2][zg]);
@@ -484,6 +486,15 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
 #pragma unroll
         for (int eb = 0; eb < 2; eb += EP) {
         C u0[2], P1[2], P2[2], Q0[2], Q1[2], Q2[2], L1[2], L2[2], Xc[2];
+        C dmx = z2, dpx = z2, dmy = z2, dpy = z2;   // this point's δ∓ (x) and the row's δ∓ (y), read once a plane
+        if (PXY && gen_x) {
+          dmx = __ldg(p.dm[0] + (eb ? xe1 : xe0));
+          dpx = __ldg(p.dp[0] + (eb ? xe1 : xe0));
+        }
+        if (PXY && gen_y) {
+          dmy = __ldg(p.dm[1] + ye);
+          dpy = __ldg(p.dp[1] + ye);
+        }
 #pragma unroll
         for (int kk = 0; kk < 3; kk++) {
           const int k = PXY ? (kk == 0 ? 1 : (kk == 1 ? 0 : 2)) : kk;   // halo row: 0 below, 1 centre, 2 above
@@ -522,9 +533,8 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
                 L1[e] = z2;
                 L2[e] = z2;
                 if (gen_x) {   // δx(u)
-                  const C dm = __ldg(p.dm[0] + (e ? xe1 : xe0)), dp = __ldg(p.dp[0] + (e ? xe1 : xe0));
-                  L1[e] = zfma_c(dm, zneg_sw(dm), csub(U[e], U[e + 1]), L1[e]);
-                  L1[e] = zfma_c(dp, zneg_sw(dp), csub(U[e + 2], U[e + 1]), L1[e]);
+                  L1[e] = zfma_c(dmx, zneg_sw(dmx), csub(U[e], U[e + 1]), L1[e]);
+                  L1[e] = zfma_c(dpx, zneg_sw(dpx), csub(U[e + 2], U[e + 1]), L1[e]);
                 }
               }
             } else {   // row below / above: a face (centre column), 2 corners (x-neighbours)
@@ -536,12 +546,11 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
               }
               if (PXY && gen_col) {
                 if (gen_x) {   // δx(Y): this row's part
-                  const C dm = __ldg(p.dm[0] + (e ? xe1 : xe0)), dp = __ldg(p.dp[0] + (e ? xe1 : xe0));
-                  L2[e] = zfma_c(dm, zneg_sw(dm), csub(U[e], U[e + 1]), L2[e]);
-                  L2[e] = zfma_c(dp, zneg_sw(dp), csub(U[e + 2], U[e + 1]), L2[e]);
+                  L2[e] = zfma_c(dmx, zneg_sw(dmx), csub(U[e], U[e + 1]), L2[e]);
+                  L2[e] = zfma_c(dpx, zneg_sw(dpx), csub(U[e + 2], U[e + 1]), L2[e]);
                 }
                 if (gen_y) {   // δy(u), δy(X): this row's part
-                  const C d = __ldg((k == 0 ? p.dm[1] : p.dp[1]) + ye);
+                  const C d = k == 0 ? dmy : dpy;
                   L1[e] = zfma_c(d, zneg_sw(d), csub(U[e + 1], u0[e]), L1[e]);
                   L2[e] = zfma_c(d, zneg_sw(d), csub(X, Xc[e]), L2[e]);
                 }
@@ -593,7 +602,7 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
               c = cfma(nt1, L1[e], c);
               c = cfma(nt2, L2[e], c);
             }
-            if (zcorr) {   // δz · (t0 P0 + t1 P1 + t2 P2) of each output plane
+            if (PZ && zcorr) {   // δz · (t0 P0 + t1 P1 + t2 P2) of each output plane
               if (zp_prev) {
                 C B3 = cscale(fma(cp.c1, i1h, R(4) * pt1), c0u);
                 B3 = cfma(pt1, p1, B3);
@@ -690,7 +699,7 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
     // points run the x/y-PML body (a point is always computed by the same warp of the same tile, so its
     // operation sequence stays fixed); the others run the z-PML or the PML-free body
     bool xyw = false;
-    if (item.z == TM_PMLXY) {
+    if (item.z & TM_PMLXY) {
       const int X0 = item.x & 0xffff, Y0 = item.x >> 16;
       const int x = X0 - 1 + 2 * c_, y = Y0 + rg;
       bool xp = false;
@@ -699,12 +708,14 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
       const bool yp = y < ny && (y < p.lo[1] || y > p.hi[1]);
       xyw = __any_sync(FULL, (xp || yp) && y < ny);
     }
-    if (xyw)
-      run_item(std::integral_constant<int, TM_PMLXY>(), item);
-    else if (item.z != TM_LEAN)
+    const bool zm = (item.z & TM_PMLZ) != 0;
+    if (xyw) {   // (one x/y body handles its chunk's z-PML planes too: a fourth body costs spills)
+      run_item(std::integral_constant<int, TM_PMLXY | TM_PMLZ>(), item);
+    } else if (zm) {
       run_item(std::integral_constant<int, TM_PMLZ>(), item);
-    else
+    } else {
       run_item(std::integral_constant<int, TM_LEAN>(), item);
+    }
   }
 
   if constexpr (K > 0) tm_reduce<NR, K, TM_NTHR>(part, act, p, rhs0, blockIdx.x);

@@ -2,9 +2,9 @@
 include/hz_debug.h): for many grid sizes and PML widths every (point, plane) of the slab — pad columns
 included — is computed by exactly one work item (tile x0 computes the columns [x0 − 1, x0 + tx − 1)),
 the tile shape respects the kernel's limits (tx ∈ {32, 64}, ty·tx/2 = 384 threads), and the
-item's body matches the PML it
-touches: the PML-free body only on planes and tiles without PML points, the z-PML body
-only on tiles without x/y-PML points."""
+item's mode bits match the PML it
+touches: TM_PMLXY exactly on tiles holding x/y-PML points, TM_PMLZ exactly on chunks
+holding z-PML planes."""
 import ctypes
 
 import numpy as np
@@ -60,13 +60,10 @@ def test_items_partition_the_slab(nx, ny, nz, npml, ngroups):
         count[z0:z1, y0:y0 + ty, x0:x0 + tx] += 1          # x ∈ [x0 − 1, x0 + tx − 1)
         xs, ys = slice(max(x0 - 1, 0), min(x0 + tx - 1, nx)), slice(y0, min(y0 + ty, ny))
         xy_pml = px[xs].any() or py[ys].any()
-        if mode == 2:
-            assert xy_pml
-        else:
-            assert not xy_pml
-            assert (mode == 1) == bool(pz[z0:z1].any())
+        assert bool(mode & 2) == xy_pml                       # TM_PMLXY: the tile holds x/y-PML points
+        assert bool(mode & 1) == bool(pz[z0:z1].any())       # TM_PMLZ: the chunk holds z-PML planes
     assert (count[:, :ny, 1:ldx + 1] == 1).all()
-    # x/y-PML items first (heavier, scheduled first)
-    modes = items[:, 4]
-    if (modes == 2).any() and (modes != 2).any():
-        assert np.max(np.nonzero(modes == 2)) < np.min(np.nonzero(modes != 2))
+    # x/y-PML tiles first (heavier, scheduled first)
+    xyi = (items[:, 4] & 2) != 0
+    if xyi.any() and (~xyi).any():
+        assert np.max(np.nonzero(xyi)) < np.min(np.nonzero(~xyi))
