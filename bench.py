@@ -34,7 +34,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -112,52 +111,54 @@ def read_traffic(key):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every 5 ms on a host thread
+    during the timed region (nvidia-smi's query, without its 100 ms+ polling floor)."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.path = os.path.join("/tmp", f"hz_clocks_{os.getpid()}.csv")
+        self.th = None
+        self.err = None
 
     def start(self):
+        import threading
         try:
-            self.f = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=self.f, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.dev = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.dev, pynvml.NVML_CLOCK_SM)
+        except Exception as e:   # noqa: BLE001
+            self.err = f"NVML unavailable: {e}"
+            return
+        self.sm, self.mask, self.stop_ev = [], 0, threading.Event()
+
+        def run():
+            nv = self.nv
+            while not self.stop_ev.is_set():
+                try:
+                    self.sm.append(nv.nvmlDeviceGetClockInfo(self.dev, nv.NVML_CLOCK_SM))
+                    self.mask |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.dev)
+                except Exception:   # noqa: BLE001
+                    pass
+                self.stop_ev.wait(0.005)
+        self.th = threading.Thread(target=run, daemon=True)
+        self.th.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.f.close()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax.append(float(parts[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        load = [x for x in sm if sm and x >= 0.5 * max(sm)] or sm
-        return {"sm_mhz": statistics.median(load) if load else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self.th is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "not sampled"], "samples": 0}
+        self.stop_ev.set()
+        self.th.join()
+        reasons = sorted(n for n, attr in self.REASONS if self.mask & getattr(self.nv, attr, 0))
+        sm = self.sm
+        load = [x for x in sm if x >= 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": self.smax,
+                "reasons": reasons, "samples": len(sm), "source": "NVML, 5 ms period"}
 
 
 # ------------------------------------------------------------------------------------------------
@@ -341,7 +342,8 @@ def run_hz(args):
             (tmax,) = parallel.rank_max([e0.elapsed_time(e1)], dev)
             it = int(stt["iterations"])
             solve[name] = {"solver": "BiCGSTAB" if ell == 1 else "BiCGStab(2)", "status": hz.STATUS_NAMES.get(st, st),
-                           "converged": bool(st == hz.HZ_OK), "iterations": it, "relres_max": float(np.max(rel)),
+                           "converged": bool(st == hz.HZ_OK), "iterations": it,
+                           "iterations_per_rhs": [int(i) for i in np.atleast_1d(its)], "relres_max": float(np.max(rel)),
                            "s": tmax * 1e-3, "s_per_rhs": tmax * 1e-3 / len(sn),
                            "ms_per_iteration": tmax / max(1, it),
                            "apply_ms_share": stt["apply_ms_total"] / tmax if tmax > 0 else None,

@@ -264,6 +264,34 @@ struct hz_coeffs {
     int grid = 1;   // resident CTAs: SMs × CTAs per SM
   };
   std::map<int, std::unique_ptr<TmPlan>> tm_plans;
+  // host-buffer applies: two copy streams and double-buffered device staging, so that the H2D copy of
+  // one RHS group, the apply of the previous one and the D2H copy of the one before overlap
+  struct HostIO {
+    cudaStream_t in = nullptr, out = nullptr;
+    cudaEvent_t start = nullptr, e_in[2] = {}, e_comp[2] = {}, e_out[2] = {};
+    DBuf bin, bout;
+    bool ok = false;
+    cudaError_t init() {
+      if (ok) return cudaSuccess;
+      cudaError_t e = cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+      for (int k = 0; k < 2 && e == cudaSuccess; k++) {
+        e = cudaEventCreateWithFlags(&e_in[k], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&e_comp[k], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&e_out[k], cudaEventDisableTiming);
+      }
+      ok = e == cudaSuccess;
+      return e;
+    }
+    ~HostIO() {
+      if (in) cudaStreamDestroy(in);
+      if (out) cudaStreamDestroy(out);
+      for (cudaEvent_t ev : {start, e_in[0], e_in[1], e_comp[0], e_comp[1], e_out[0], e_out[1]})
+        if (ev) cudaEventDestroy(ev);
+    }
+  };
+  HostIO hio;
   std::unique_ptr<SolverWork> work;
   size_t esz() const { return dtype == HZ_C64 ? 4 : 8; }   // real element size
   long long plane() const { return (long long)ldx * grid.ny; }
@@ -1147,26 +1175,56 @@ hz_status hz_coeffs_export(const hz_coeffs* c, void* record, void* pml_host, int
 // (3) apply
 // ---------------------------------------------------------------------------------------------
 template <typename R>
-static hz_status apply_t(const hz_coeffs* c, void* u, void* au, int nrhs, cudaStream_t s) {
+static hz_status apply_t(const hz_coeffs* cc, void* u, void* au, int nrhs, cudaStream_t s) {
   typedef typename Cx<R>::T C;
-  const size_t fb = (size_t)c->fstride() * nrhs * sizeof(C);
+  hz_coeffs* c = const_cast<hz_coeffs*>(cc);
+  const size_t fsb = (size_t)c->fstride() * sizeof(C);   // bytes of one field
   const bool du = is_device_ptr(u), da = is_device_ptr(au);
-  DBuf tu, ta;
-  void* ud = u;
-  void* ad = au;
-  if (!du) { HZ_CUDA(tu.ensure(fb)); HZ_CUDA(cudaMemcpyAsync(tu.p, u, fb, cudaMemcpyHostToDevice, s)); ud = tu.p; }
-  if (!da) { HZ_CUDA(ta.ensure(fb)); ad = ta.p; }
-  HZ_TRY(halo_exchange(c, ud, nrhs, sizeof(C), s));
-  ApplyParams<R> p = make_params<R>(c);
-  p.u = reinterpret_cast<const C*>(ud);
-  p.au = reinterpret_cast<C*>(ad);
-  HZ_TRY(apply_launch<R>(c, p, nrhs, EPI_PLAIN, s));
-  if (!da) {
-    HZ_CUDA(cudaMemcpyAsync(au, ad, fb, cudaMemcpyDeviceToHost, s));
-    HZ_CUDA(cudaStreamSynchronize(s));
-  } else if (!du) {
-    HZ_CUDA(cudaStreamSynchronize(s));
+  if (du && da) {
+    HZ_TRY(halo_exchange(c, u, nrhs, sizeof(C), s));
+    ApplyParams<R> p = make_params<R>(c);
+    p.u = reinterpret_cast<const C*>(u);
+    p.au = reinterpret_cast<C*>(au);
+    return apply_launch<R>(c, p, nrhs, EPI_PLAIN, s);
   }
+  // host u and / or Au: RHS groups of g fields through two staging slots; group k's H2D copy (stream
+  // in), apply (s) and D2H copy (stream out) overlap with the neighbouring groups'
+  auto& io = c->hio;
+  HZ_CUDA(io.init());
+  const int g = std::min(nrhs, 2);
+  if (!du) HZ_CUDA(io.bin.ensure(2 * g * fsb));
+  if (!da) HZ_CUDA(io.bout.ensure(2 * g * fsb));
+  HZ_CUDA(cudaEventRecord(io.start, s));   // the copies follow the caller's earlier work on s
+  HZ_CUDA(cudaStreamWaitEvent(io.in, io.start, 0));
+  HZ_CUDA(cudaStreamWaitEvent(io.out, io.start, 0));
+  const int ng = (nrhs + g - 1) / g;
+  for (int k = 0; k < ng; k++) {
+    const int slot = k & 1, r0 = k * g, n = std::min(g, nrhs - r0);
+    const size_t off = (size_t)r0 * fsb, bytes = (size_t)n * fsb;
+    char* src = du ? static_cast<char*>(u) + off : io.bin.as<char>() + (size_t)slot * g * fsb;
+    char* dst = da ? static_cast<char*>(au) + off : io.bout.as<char>() + (size_t)slot * g * fsb;
+    if (!du) {
+      if (k >= 2) HZ_CUDA(cudaStreamWaitEvent(io.in, io.e_comp[slot], 0));   // group k-2 has read the slot
+      HZ_CUDA(cudaMemcpyAsync(src, static_cast<const char*>(u) + off, bytes, cudaMemcpyHostToDevice, io.in));
+      HZ_CUDA(cudaEventRecord(io.e_in[slot], io.in));
+      HZ_CUDA(cudaStreamWaitEvent(s, io.e_in[slot], 0));
+    }
+    if (!da && k >= 2) HZ_CUDA(cudaStreamWaitEvent(s, io.e_out[slot], 0));   // group k-2's result copied out
+    HZ_TRY(halo_exchange(c, src, n, sizeof(C), s));
+    ApplyParams<R> p = make_params<R>(c);
+    p.u = reinterpret_cast<const C*>(src);
+    p.au = reinterpret_cast<C*>(dst);
+    HZ_TRY(apply_launch<R>(c, p, n, EPI_PLAIN, s));
+    HZ_CUDA(cudaEventRecord(io.e_comp[slot], s));
+    if (!da) {
+      HZ_CUDA(cudaStreamWaitEvent(io.out, io.e_comp[slot], 0));
+      HZ_CUDA(cudaMemcpyAsync(static_cast<char*>(au) + off, dst, bytes, cudaMemcpyDeviceToHost, io.out));
+      HZ_CUDA(cudaEventRecord(io.e_out[slot], io.out));
+    }
+  }
+  if (!da)
+    for (int k = 0; k < std::min(ng, 2); k++) HZ_CUDA(cudaStreamWaitEvent(s, io.e_out[k], 0));
+  HZ_CUDA(cudaStreamSynchronize(s));
   return HZ_OK;
 }
 

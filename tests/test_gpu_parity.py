@@ -463,3 +463,31 @@ def test_apply_ga_record_mode(hz, ctx, table, ga_table, dtype):
     got = gpu_apply(hz, C, u)
     ref = op.apply(op.assemble(oracle_problem(v, h, f, npml, ga_table, dtype)), u)
     assert rel(got, ref) <= TOL[dtype], rel(got, ref)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("nrhs", [1, 3, 6])
+def test_apply_host_buffers_pipelined(hz, ctx, table, dtype, nrhs):
+    """hz_apply_impedance with HOST u and / or Au (pinned or pageable): the RHS groups stream through
+    the library's double-buffered staging (H2D, apply, D2H on three streams) and the result is BITWISE
+    the device-buffer apply, for every combination and an odd group count."""
+    rng = np.random.default_rng(77 + nrhs)
+    nz, ny, nx, h, f, npml = 13, 19, 37, 25.0, 7.0, 3
+    v = rng.uniform(1500.0, 4500.0, (nz, ny, nx))
+    C = assemble(hz, ctx, table, v, h, f, npml, dtype)
+    u = synth.random_field((nrhs, nz, ny, nx), seed=9)
+    ref = C.alloc_field(nrhs)
+    ud = C.alloc_field(nrhs)
+    ud[:, 1:-1] = torch.from_numpy(u.astype(cdt(dtype))).cuda()
+    hz.hz_apply_impedance(C, ud, ref)
+    torch.cuda.synchronize()
+    ref = ref.cpu()
+    for pin in (True, False):
+        uh = C.alloc_field(nrhs, device="cpu", pin_memory=pin)
+        uh.copy_(ud.cpu())
+        for src, host_out in ((uh, True), (ud, True), (uh, False)):
+            out = C.alloc_field(nrhs, device="cpu", pin_memory=pin) if host_out else C.alloc_field(nrhs)
+            out.fill_(complex(7.0, -7.0))
+            hz.hz_apply_impedance(C, src, out)
+            torch.cuda.synchronize()
+            assert torch.equal(out[:, 1:-1].cpu(), ref[:, 1:-1]), (pin, src.device, out.device)
