@@ -10,6 +10,13 @@ Follows PAPER.md §2.1 and the adaptive rule of P:36/P:51/P:273/P:446
 
 with κ = v² (ρ = 1; reading A17) and the PML stretching ∂x̃ = ξx⁻¹ ∂x, ξ = 1 + iγ/ω.
 
+Visco-acoustic, variable density (NEXT-2; Eqs. 1.1-1.4 and 2): Problem(b=…, Q=…) gives
+  ω²/κ p + Σ_a ∂_a b ∂_a p = s,   κ = v_c²/b,  v_c = v (1 − i/(2Q))            (reading A24)
+with the per-axis D_a b-weighted at the staggered midpoints: on the stencil line through the
+transverse neighbour (p, q) of row n the edge buoyancy is the mean of the row line's and that line's
+edge values, each the mean of its two end nodes (reading A25).  b = None, Q = None is the ρ = 1
+elastic operator above, computed by the original expressions.
+
 Readings (DESIGN.md §Readings): A4 (Eq. 8's p0 is p0/κ0), A5 (Eq. 8 is the default mass;
 Eq. "10" collocation mass available as mass="colloc"), A6 (stiffness in per-axis form
 S = Σ_a D2_a ⊗ T_a with t0 = ws1 + ⅔ws2 + ½ws3, t1 = ws2/12, t2 = ws3/8 — the unique
@@ -139,6 +146,8 @@ class Problem:
     v_pml: Optional[float] = None     # None → max(v) (reading A7)
     mass: str = "eq8"                 # "eq8" (default A5) | "colloc"
     rule: str = "GA"                  # "GA" (row's own weights) | "GAm" (27-point mean, A19)
+    b: Optional[np.ndarray] = None    # buoyancy 1/ρ per node (Eq. 2), None → 1 (A17)
+    Q: Optional[object] = None        # quality factor per node or scalar (visco-acoustic κ, A24), None → ∞
 
     @property
     def omega(self):
@@ -150,6 +159,18 @@ class Problem:
 
     def coefficients(self) -> PointCoefficients:
         return point_coefficients(self.v, self.freq, self.h, self.table, self.rule)
+
+    def kappa(self):
+        """Bulk modulus per node: v² (b = None, Q = None: the ρ = 1 operator, A17), else
+        κ = v_c²/b with the complex velocity v_c = v (1 − i/(2Q)) (reading A24; e^{−iωt}, so
+        Im k = Im(ω/v_c) > 0 attenuates)."""
+        if self.b is None and self.Q is None:
+            return self.v ** 2
+        vc = self.v if self.Q is None else self.v * (1.0 - 0.5j / np.asarray(self.Q, dtype=np.float64))
+        kap = vc ** 2 / (1.0 if self.b is None else self.b)
+        if np.iscomplexobj(kap) and not np.any(kap.imag):   # Q = ∞ everywhere: κ is real
+            kap = kap.real
+        return kap
 
     def pml(self):
         vp = float(np.max(self.v)) if self.v_pml is None else float(self.v_pml)
@@ -177,16 +198,56 @@ def _entry(prob: Problem, coef: PointCoefficients, pml, K, J, I, d):
     c = mass_class(d)
     kk_c, jj_c, ii_c = np.clip(kk, 0, nz - 1), np.clip(jj, 0, ny - 1), np.clip(ii, 0, nx - 1)
     w2 = prob.omega ** 2
+    kap = prob.kappa()
     if prob.mass == "eq8":
-        mass = w2 * coef.mu[..., c] / v[kk_c, jj_c, ii_c] ** 2
+        mass = w2 * coef.mu[..., c] / kap[kk_c, jj_c, ii_c]
     elif prob.mass == "colloc":
-        mass = w2 * coef.mu[..., c] / v[K, J, I] ** 2          # Eq. "10", κ0 for all 27
+        mass = w2 * coef.mu[..., c] / kap[K, J, I]          # Eq. "10", κ0 for all 27
     else:
         raise ValueError(prob.mass)
-    stiff = (Dx[dx][I] * T_weight(dy, dz, coef.t0, coef.t1, coef.t2)
-             + Dy[dy][J] * T_weight(dx, dz, coef.t0, coef.t1, coef.t2)
-             + Dz[dz][K] * T_weight(dx, dy, coef.t0, coef.t1, coef.t2))
+    if prob.b is None:
+        stiff = (Dx[dx][I] * T_weight(dy, dz, coef.t0, coef.t1, coef.t2)
+                 + Dy[dy][J] * T_weight(dx, dz, coef.t0, coef.t1, coef.t2)
+                 + Dz[dz][K] * T_weight(dx, dy, coef.t0, coef.t1, coef.t2))
+    else:
+        bz = _b_weighted(prob, K, J, I, dz, (dz, dy, dx), 0, amz, apz)
+        by = _b_weighted(prob, K, J, I, dy, (dz, dy, dx), 1, amy, apy)
+        bx = _b_weighted(prob, K, J, I, dx, (dz, dy, dx), 2, amx, apx)
+        stiff = (bx * T_weight(dy, dz, coef.t0, coef.t1, coef.t2)
+                 + by * T_weight(dx, dz, coef.t0, coef.t1, coef.t2)
+                 + bz * T_weight(dx, dy, coef.t0, coef.t1, coef.t2))
     return mass + stiff, ok, (kk, jj, ii)
+
+
+def _b_at(b, K, J, I):
+    """b at nodes (K, J, I), indices clamped into the grid (out-of-grid buoyancy = the nearest
+    node's; only the centre coefficients of lines at the grid edge use it, reading A25)."""
+    nz, ny, nx = b.shape
+    return b[np.clip(K, 0, nz - 1), np.clip(J, 0, ny - 1), np.clip(I, 0, nx - 1)]
+
+
+def _b_weighted(prob, K, J, I, da, d, axis, am, ap):
+    """D_a(n, d_a) of the b-weighted second difference along axis a (0 = z, 1 = y, 2 = x) on the
+    stencil line through the transverse neighbour n + d⊥ of row n (reading A25, Eq. 2):
+        edge buoyancy of a line at node m:  b±(m) = (b(m) + b(m ± e_a)) / 2   (staggered midpoint)
+        β± = (b±(n) + b±(n + d⊥)) / 2        (row line and transverse line averaged: A symmetric)
+        D_a(n, −1) = β⁻ a⁻_a(n_a),  D_a(n, +1) = β⁺ a⁺_a(n_a),  D_a(n, 0) = −(β⁻ a⁻ + β⁺ a⁺)."""
+    b = prob.b
+    e = [0, 0, 0]
+    e[axis] = 1
+    t = list(d)
+    t[axis] = 0                                        # transverse neighbour offset d⊥
+    n_a = (K, J, I)[axis]
+
+    def edge(sign, k, j, i):
+        return 0.5 * (_b_at(b, k, j, i) + _b_at(b, k + sign * e[0], j + sign * e[1], i + sign * e[2]))
+    beta_p = 0.5 * (edge(+1, K, J, I) + edge(+1, K + t[0], J + t[1], I + t[2]))
+    beta_m = 0.5 * (edge(-1, K, J, I) + edge(-1, K + t[0], J + t[1], I + t[2]))
+    if da == 1:
+        return beta_p * ap[n_a]
+    if da == -1:
+        return beta_m * am[n_a]
+    return -(beta_m * am[n_a] + beta_p * ap[n_a])
 
 
 def assemble(prob: Problem, coef: Optional[PointCoefficients] = None) -> sp.csr_matrix:

@@ -101,11 +101,12 @@ def test_gradient_analytic_reduced(ga_table):
     assert _gradient_case(61, ga_table) <= 0.02
 
 
-@pytest.mark.slow
 def test_gradient_ordering_ga_gm(ga_table):
-    """Paper's Linear row ordering GA < Gm (Table 2) on the reduced analog."""
+    """Paper's Linear row ordering GA < Gm (Table 2), shrunk to a 31³ analog of config 2 (same
+    h, f and v(z)) so that it runs in the default suite (~25 s): measured err 2.5e-3 (GA) vs 1.3e-2
+    (Gm); the margin asserted is 3×."""
     gm = weights.WeightTable(4.0, 0.1, np.array([4.0]), weights.gm_weights()[None], 0)
-    assert _gradient_case(61, ga_table) < _gradient_case(61, gm)
+    assert 3.0 * _gradient_case(31, ga_table) < _gradient_case(31, gm)
 
 
 def _small_helmholtz(ga_table, seed=5, n=(12, 11, 10)):

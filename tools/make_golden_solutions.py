@@ -5,8 +5,9 @@ solve.  Calls only oracle/ and synth/ (task rule: a stored expected value is wri
 script that calls only the oracle).
 
 Configs 4-5 are solved on their seeded 201x201x101 crops (synth.crop_config): keys
-"4c5", "4c10" (config 4 at 5 / 10 Hz) and "5c10", solved with the oracle's BiCGStab(2) (BiCGSTAB stagnates
-on the full config-4 model, reading A23).
+"4c5", "4c10" (config 4 at 5 / 10 Hz) and "5c10".  Config 3 and the crops are solved with the oracle's
+BiCGStab(2): complex128 BiCGSTAB stagnates above 1e-10 on these sharp-contrast models (DESIGN.md
+reading A23; a config-3 BiCGSTAB run did not finish in 3.7 h).
 
 Usage: python tools/make_golden_solutions.py [key ...]     (each RHS solve runs in its own process)
 """
@@ -61,7 +62,7 @@ def solve_one(args):
     A = op.assemble(P)
     nodes = synth.source_nodes(cfg)
     b = op.point_sources(P, nodes[r:r + 1])[0].ravel()
-    if isinstance(ci, str):   # crops of the large models: BiCGStab(2) (BiCGSTAB stagnates there)
+    if isinstance(ci, str) or ci == 3:   # blocky config 3, crops of 4-5: BiCGStab(2) (BiCGSTAB stagnates, A23)
         x, rel, it = solvers.bicgstab_l(A, b, ell=2, rtol=RTOL, max_iter=16000)
     else:
         x, rel, it = solvers.bicgstab(A, b, rtol=RTOL)
