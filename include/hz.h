@@ -161,6 +161,23 @@ hz_status hz_assemble_coeffs(hz_ctx* ctx, const hz_grid* grid, hz_dtype dtype, c
 hz_status hz_coeffs_export(const hz_coeffs* c, void* record, void* pml_host, int nmax);
 void hz_coeffs_destroy(hz_coeffs* c);
 
+/* Visco-acoustic, variable-density medium (NEXT-2; Eqs. 1.1-1.4 and 2; DESIGN.md readings
+ * A24, A25).  Attaches buoyancy b = 1/rho and the quality factor Q to an assembled operator, which
+ * then reads
+ *   (Au)_n = omega^2 sum_d mu_{|d|}(w_n) u_{n+d} / kappa_{n+d}        kappa = v_c^2 / b,
+ *                                                                    v_c = v (1 - i/(2Q))   (A24)
+ *          + sum_a sum_{p,q} T(p,q; w_n) [beta+ a+_a (u_+ - u_0) + beta- a-_a (u_- - u_0)]_{line p,q}
+ *   beta+- = (b+-(n) + b+-(n + d_perp))/2,  b+-(m) = (b_m + b_{m +- e_a})/2              (A25)
+ * (the weights w_n still come from G = v/(f h)).  b, q: real arrays of the coeffs' real type
+ * (float for HZ_C64, double for HZ_C128) in v's layout ([nz_local][ny][nx], or [nz_local+2][ny][nx]
+ * when grid.v_halo), host or device, copied (the caller keeps ownership); NULL b means b = 1, NULL q
+ * means Q = infinity; both NULL restores the rho = 1 elastic operator.  Halo planes come from the
+ * neighbour ranks as for v.  Every later apply / solve / residual of c uses the medium; the kernel
+ * is apply_medium.cu (a gather kernel: correctness first).  Errors:
+ * HZ_ERR_DOMAIN if a b is not positive and finite or a Q not > 0 (each rank checks its slab),
+ * HZ_ERR_CUDA on allocation / copy failures.  Synchronous on `stream`. */
+hz_status hz_coeffs_set_medium(hz_coeffs* c, const void* b, const void* q, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * (3) apply_impedance — Au = [M + S] u for nrhs fields, matrix-free, asynchronous on
  * `stream`.  u and au: [nrhs][nz_local+2][ny][ldx] complex of the coeffs' dtype.  u's halo planes

@@ -292,6 +292,10 @@ struct hz_coeffs {
     }
   };
   HostIO hio;
+  // visco-acoustic / variable-density medium (hz_coeffs_set_medium; readings A24, A25): every apply
+  // goes through apply_medium.cu with b and κ⁻¹ = b/(v²(1 − i/(2Q))²), [nzl+2][ny][ldx] with halos
+  bool medium = false;
+  DBuf bmed, kinv;
   std::unique_ptr<SolverWork> work;
   size_t esz() const { return dtype == HZ_C64 ? 4 : 8; }   // real element size
   long long plane() const { return (long long)ldx * grid.ny; }
@@ -815,6 +819,27 @@ template <typename R, typename S>
 hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int epi, cudaStream_t s) {
   hz_coeffs* c = const_cast<hz_coeffs*>(cc);
   const int K = epi_k(epi);
+  if (c->medium) {   // visco-acoustic / variable density: the b-weighted gather kernel (apply_medium.cu)
+    typedef typename Cx<S>::T CS;
+    const S* bm = c->bmed.template as<S>();
+    const CS* ki = c->kinv.template as<CS>();
+    const bool colloc = c->mass == HZ_MASS_COLLOC;
+    const long long nb = launch_apply_medium<R, S>(p, bm, ki, nrhs, colloc, epi, s, nullptr);
+    if (K > 0) {
+      HZ_CUDA(c->partials.ensure(sizeof(double) * (size_t)nb * K * nrhs));
+      if (c->tickets.n < sizeof(unsigned) * (size_t)nrhs) {
+        HZ_CUDA(c->tickets.ensure(sizeof(unsigned) * (size_t)nrhs));
+        HZ_CUDA(cudaMemsetAsync(c->tickets.p, 0, c->tickets.n, s));
+      }
+      p.partials = c->partials.as<double>();
+      p.tickets = c->tickets.as<unsigned>();
+    }
+    cudaError_t e = cudaSuccess;
+    launch_apply_medium<R, S>(p, bm, ki, nrhs, colloc, epi, s, &e);
+    HZ_CUDA(e);
+    count_launch();
+    return HZ_OK;
+  }
   constexpr bool TM = sizeof(R) == 4 && sizeof(S) == 4;
   TmLaunch L{nullptr, nullptr};
   long long nb = 0;
@@ -1226,6 +1251,68 @@ static hz_status apply_t(const hz_coeffs* cc, void* u, void* au, int nrhs, cudaS
     for (int k = 0; k < std::min(ng, 2); k++) HZ_CUDA(cudaStreamWaitEvent(s, io.e_out[k], 0));
   HZ_CUDA(cudaStreamSynchronize(s));
   return HZ_OK;
+}
+
+template <typename R>
+static hz_status set_medium_t(hz_coeffs* c, const void* b, const void* q, cudaStream_t s) {
+  const hz_grid* g = &c->grid;
+  const long long plane = c->plane(), n = (long long)(g->nz_local + 2) * plane;
+  DBuf qd;
+  auto load = [&](DBuf& dst, const void* src, R fill) -> hz_status {
+    HZ_CUDA(dst.ensure((size_t)n * sizeof(R)));
+    HZ_CUDA(launch_medium_fill<R>(dst.as<R>(), n, fill, s));
+    count_launch();
+    if (src == nullptr) return HZ_OK;
+    const cudaMemcpyKind kind = is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const R* in = reinterpret_cast<const R*>(src);
+    const size_t rowb = (size_t)g->nx * sizeof(R), pitch = (size_t)c->ldx * sizeof(R);
+    const size_t vplane = (size_t)g->nx * g->ny;
+    auto copy_planes = [&](int dst_plane, const R* sp, int np) {
+      return cudaMemcpy2DAsync(dst.as<R>() + (size_t)dst_plane * plane, pitch, sp, rowb, rowb, (size_t)np * g->ny, kind, s);
+    };
+    if (g->v_halo) {   // the same layout as v (include/hz.h hz_grid.v_halo)
+      HZ_CUDA(copy_planes(1, in + vplane, g->nz_local));
+      if (g->z0 > 0) HZ_CUDA(copy_planes(0, in, 1));
+      if (g->z0 + g->nz_local < g->nz_global) HZ_CUDA(copy_planes(g->nz_local + 1, in + (size_t)(g->nz_local + 1) * vplane, 1));
+    } else {
+      HZ_CUDA(copy_planes(1, in, g->nz_local));
+      HZ_TRY(halo_exchange(c, dst.p, 1, sizeof(R), s));
+    }
+    return HZ_OK;
+  };
+  HZ_TRY(load(c->bmed, b, R(1)));
+  if (q) HZ_TRY(load(qd, q, R(0)));
+  DBuf bad;
+  HZ_CUDA(bad.ensure(sizeof(unsigned long long)));
+  HZ_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
+  HZ_CUDA(launch_medium_check<R>(c->bmed.as<R>() + plane, q ? qd.as<R>() + plane : nullptr, (long long)g->nz_local * plane,
+                                 g->nx, c->ldx, bad.as<unsigned long long>(), s));
+  count_launch();
+  unsigned long long nbad = 0;
+  HZ_CUDA(cudaMemcpyAsync(&nbad, bad.p, sizeof(nbad), cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  if (nbad > 0) {
+    set_error("hz_coeffs_set_medium: " + std::to_string(nbad) + " buoyancy / Q values are not positive and finite");
+    return HZ_ERR_DOMAIN;
+  }
+  typedef typename Cx<R>::T C;
+  HZ_CUDA(c->kinv.ensure((size_t)n * sizeof(C)));
+  HZ_CUDA(launch_medium_kinv<R>(c->v.as<R>(), c->bmed.as<R>(), q ? qd.as<R>() : nullptr, c->kinv.as<C>(), n, s));
+  count_launch();
+  HZ_CUDA(cudaStreamSynchronize(s));
+  c->medium = true;
+  return HZ_OK;
+}
+
+extern "C" hz_status hz_coeffs_set_medium(hz_coeffs* c, const void* b, const void* q, void* stream) {
+  if (!c) { set_error("hz_coeffs_set_medium: NULL coeffs"); return HZ_ERR_INVALID_ARG; }
+  HZ_TRY(set_device(c->ctx));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!b && !q) {   // ρ = 1, Q = ∞: back to the class-sum kernels
+    c->medium = false;
+    return HZ_OK;
+  }
+  return c->dtype == HZ_C64 ? set_medium_t<float>(c, b, q, s) : set_medium_t<double>(c, b, q, s);
 }
 
 extern "C" hz_status hz_apply_impedance(const hz_coeffs* c, void* u, void* au, int nrhs, void* stream) {

@@ -69,6 +69,18 @@ template <int TX> int tm_occupancy_tx(int tab_n, int nr);
 int tm_occupancy(int tab_n, int tx, int ty, int nr);   // resident CTAs per SM
 cudaError_t launch_apply_tm(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, bool colloc, int epi,
                             cudaStream_t s);
+// visco-acoustic / variable-density apply (apply_medium.cu; NEXT-2, readings A24, A25): bmed = b,
+// kinv = κ⁻¹ = b/(v²(1 − i/(2Q))²), both [nzl+2][ny][ldx] with halo planes.  err == nullptr: no
+// launch, returns the CTAs per RHS (partial slots); else launches and returns the same count.
+template <typename R, typename S>
+long long launch_apply_medium(const ApplyParams<R, S>& p, const S* bmed, const typename Cx<S>::T* kinv, int nrhs,
+                              bool colloc, int epi, cudaStream_t s, cudaError_t* err);
+template <typename S>
+cudaError_t launch_medium_kinv(const S* v, const S* b, const S* q, typename Cx<S>::T* out, long long n, cudaStream_t s);
+template <typename S> cudaError_t launch_medium_fill(S* out, long long n, S val, cudaStream_t s);
+template <typename S>
+cudaError_t launch_medium_check(const S* b, const S* q, long long n, int nx, int ldx, unsigned long long* bad,
+                                cudaStream_t s);
 // loopback communicator: the ranks' buffers (same device), reduced in rank order; op 0 = sum, 1 = max
 constexpr int LOOP_MAX_RANKS = 16;
 struct LoopPtrs {

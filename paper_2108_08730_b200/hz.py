@@ -86,6 +86,7 @@ _sigs = {
                                       ct.c_int, ct.c_int, _P(_vp), _P(ct.c_longlong)]),
     "hz_coeffs_export": (ct.c_int, [_vp, _vp, _vp, ct.c_int]),
     "hz_coeffs_destroy": (None, [_vp]),
+    "hz_coeffs_set_medium": (ct.c_int, [_vp, _vp, _vp, _vp]),
     "hz_apply_impedance": (ct.c_int, [_vp, _vp, _vp, ct.c_int, _vp]),
     "hz_solve": (ct.c_int, [_vp, _vp, _vp, ct.c_int, _P(hz_solve_opts), _P(ct.c_double),
                             _P(ct.c_int), _P(hz_solve_stats), _vp]),
@@ -314,6 +315,12 @@ def hz_assemble_coeffs(ctx: Ctx, nx: int, ny: int, nz_global: int, h: float, v, 
 def hz_coeffs_export(c: Coeffs, record=None, pml=None) -> None:
     nmax = 0 if pml is None else pml.shape[-1]
     _check(_lib.hz_coeffs_export(c._h, _ptr(record), _ptr(pml), nmax), "hz_coeffs_export")
+
+
+def hz_coeffs_set_medium(c: Coeffs, b=None, q=None, stream=None) -> None:
+    """Buoyancy b = 1/ρ and quality factor Q (arrays of the coeffs' real dtype in v's layout, or None
+    for b = 1 / Q = ∞) for every later apply and solve of c (include/hz.h)."""
+    _check(_lib.hz_coeffs_set_medium(c._h, _ptr(b), _ptr(q), _stream_ptr(stream)), "hz_coeffs_set_medium")
 
 
 def hz_apply_impedance(c: Coeffs, u, au, nrhs: Optional[int] = None, stream=None) -> None:
