@@ -247,6 +247,7 @@ struct hz_coeffs {
   DBuf w;                      // [nzl+2][ny][ldx] R: 1/v² (the apply's model input)
   DBuf tab_f, tab_d;           // [n_g_dev][TAB_STRIDE] float / double rows (float only for C64)
   DBuf ctab_f, ctab_d;         // [n_g_dev][CTAB_STRIDE] pre-scaled class coefficients (apply)
+  DBuf ctm_f;                  // [n_g_dev][TMTAB_STRIDE] the same with c0, m0 (complex64 tensor-map apply)
   DBuf pml_f[6], pml_d[6];     // dm x,y,z ; dp x,y,z (complex float / complex double)
   int lo[3], hi[3];
   int tab_lo = 0, tab_n = 2;   // table rows covering the model's G range (staged in smem by the apply)
@@ -263,7 +264,8 @@ struct hz_coeffs {
     int n_items = 0;
     int grid = 1;   // resident CTAs: SMs × CTAs per SM
   };
-  std::map<int, std::unique_ptr<TmPlan>> tm_plans;
+  std::map<int, std::unique_ptr<TmPlan>> tm_plans;   // per RHS count
+  DBuf tm_ctr;                 // apply27_tm work counter + CTA ticket
   // host-buffer applies: two copy streams and double-buffered device staging, so that the H2D copy of
   // one RHS group, the apply of the previous one and the D2H copy of the one before overlap
   struct HostIO {
@@ -515,6 +517,7 @@ ApplyParams<R, S> make_params(const hz_coeffs* c) {
   p.gam = c->rule != HZ_RULE_GA ? c->gam.as<S>() : nullptr;
   p.tab = sizeof(R) == 4 ? c->tab_f.as<R>() : c->tab_d.as<R>();
   p.ctab = sizeof(R) == 4 ? c->ctab_f.as<R>() : c->ctab_d.as<R>();
+  p.ctm = sizeof(R) == 4 ? c->ctm_f.as<float>() : nullptr;
   p.tab_lo = c->tab_lo;
   p.tab_n = c->tab_n;
   p.invih2 = (R)(c->h * c->h);
@@ -662,8 +665,8 @@ hz_status tm_encoder() {
 // Tile geometry: tile i computes the columns [i·tx − 1, (i+1)·tx − 1) (apply27_tm.cuh); ntx tiles of
 // tx ∈ {32, 64} columns cover the pitched row (the pad columns too, which the apply writes as zeros):
 // the width with the fewest box columns ntx·(tx + 4) (halo included), the wider on a tie; rows
-// ty = 768/tx; the maps start at the slab's first in-grid storage plane (planes outside the global
-// grid read zeros).
+// ty = tm_rows(tx); the maps start at the slab's first in-grid storage plane (planes outside the
+// global grid read zeros).
 int tm_tile_width(int ldx) {
   int best = TM_MAXTX, cost = INT_MAX;
   for (int tx = TM_MAXTX; tx >= 32; tx /= 2) {
@@ -712,12 +715,13 @@ const CUtensorMap* tm_umap(hz_coeffs* c, const void* u, int nrhs) {
   return &(c->tmap_u[key] = m);
 }
 
-// Work list for ngroups RHS groups of nr RHS per CTA: each tile of the ntx × nty grid marches the
-// slab in z-chunks whose count balances the launch over whole waves of resident CTAs against the 2
-// halo planes a chunk re-reads; tiles with x/y-PML points run the x/y-PML body (cut into 1.5× more
-// chunks: they cost more per point), the others run the z-PML body on the chunks [0, zl) and
-// [zh, nzl) that touch the z-PML and the PML-free body in between.  x/y-PML items come first.
-void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], const int hi[3], int slots, int ngroups,
+// Work list: the ntx × nty tiles, each marching the slab in z-chunks (every item is run once per RHS,
+// handed out dynamically).  The chunk count balances the tail of the dynamic schedule (about half an
+// item per CTA) against the 2 halo planes a chunk re-reads; tiles with x/y-PML points run the x/y
+// corrections and are cut at the z-PML boundaries too; the other tiles run the PML-free planes
+// [zl, zh) and the z-PML chunks [0, zl), [zh, nzl) as separate items.  x/y-PML items come first
+// (they cost more per point, so they do not end up in the tail).
+void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], const int hi[3], int slots, int nrhs,
                     std::vector<int4>& out) {
   const int nzl = g.nz_local;
   const int ntx = (ldx + 1 + tx - 1) / tx, nty = (g.ny + ty - 1) / ty;
@@ -729,23 +733,21 @@ void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], 
       const bool pml = xa < lo[0] || x1 > hi[0] || y0 < lo[1] || y1 > hi[1] || hi[0] < lo[0] || hi[1] < lo[1];
       (pml ? xy : in).push_back({x0, y0});
     }
-  const double nt = (double)(xy.size() + in.size());
+  const double nt = (double)(xy.size() + in.size()) * std::max(1, nrhs);
   int nch = 1;
   double best = -1;
-  for (int n = 1; n <= std::max(1, nzl / 4); n++) {
-    const double waves = nt * n * ngroups / std::max(1, slots);
+  for (int n = 1; n <= std::max(1, nzl / 8); n++) {
+    const double per_cta = nt * n / std::max(1, slots);   // items per CTA
     const double L = (double)nzl / n;
-    const double eff = waves / std::ceil(waves) * L / (L + 2.0);
+    const double eff = per_cta / (per_cta + 0.5) * L / (L + 2.0);
     if (eff > best + 1e-9) { best = eff; nch = n; }
   }
   const int zl = std::min(std::max(lo[2] - g.z0, 0), nzl);
   const int zh = std::min(std::max(hi[2] - g.z0 + 1, zl), nzl);
   const int nin = std::max(1, (int)std::lround((double)nch * (zh - zl) / std::max(1, nzl)));
-  const int nxy = std::max(1, std::min(std::max(1, nzl / 2), (int)std::lround(nch * 1.5)));
   out.clear();
-  // x/y-PML tiles: nxy chunks, also cut at the z-PML boundaries so that each chunk's mode is exact
   std::vector<int> cuts;
-  for (int k = 0; k <= nxy; k++) cuts.push_back((int)((long long)nzl * k / nxy));
+  for (int k = 0; k <= nch; k++) cuts.push_back((int)((long long)nzl * k / nch));
   cuts.push_back(zl);
   cuts.push_back(zh);
   std::sort(cuts.begin(), cuts.end());
@@ -766,23 +768,21 @@ void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], 
   }
 }
 
-const hz_coeffs::TmPlan* tm_plan(hz_coeffs* c, int ngroups, int nr) {
-  const int key = ngroups * 8 + nr;
-  auto it = c->tm_plans.find(key);
+const hz_coeffs::TmPlan* tm_plan(hz_coeffs* c, int nrhs) {
+  auto it = c->tm_plans.find(nrhs);
   if (it != c->tm_plans.end()) return it->second.get();
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->ctx->device);
-  const int slots = sms * tm_occupancy(c->tab_n, c->tm_tx, c->tm_ty, nr);
   std::vector<int4> items;
-  tm_build_items(c->grid, c->ldx, c->tm_tx, c->tm_ty, c->lo, c->hi, slots, ngroups, items);
+  tm_build_items(c->grid, c->ldx, c->tm_tx, c->tm_ty, c->lo, c->hi, sms, nrhs, items);
   std::unique_ptr<hz_coeffs::TmPlan> pl(new hz_coeffs::TmPlan);
   pl->n_items = (int)items.size();
-  pl->grid = std::max(1, slots / std::max(1, ngroups));
+  pl->grid = sms;   // one persistent CTA per SM
   if (pl->work.ensure(std::max<size_t>(1, items.size()) * sizeof(int4)) != cudaSuccess) return nullptr;
   if (!items.empty() && cudaMemcpy(pl->work.p, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice) != cudaSuccess)
     return nullptr;
   auto* raw = pl.get();
-  c->tm_plans[key] = std::move(pl);
+  c->tm_plans[nrhs] = std::move(pl);
   return raw;
 }
 
@@ -790,8 +790,8 @@ const hz_coeffs::TmPlan* tm_plan(hz_coeffs* c, int ngroups, int nr) {
 
 // test hook (include/hz_debug.h): the tensor-map apply's work list for a single slab
 extern "C" int hz_debug_plan_tiles(int nx, int ny, int nz, int lo_x, int hi_x, int lo_y, int hi_y, int lo_z, int hi_z,
-                                   int slots, int ngroups, int* out, int max_items, int* tile_wh) {
-  if (nx < 3 || ny < 3 || nz < 1 || nx > 65535 || ny > 65535 || nz > 65535 || slots < 1 || ngroups < 1 ||
+                                   int slots, int nrhs, int* out, int max_items, int* tile_wh) {
+  if (nx < 3 || ny < 3 || nz < 1 || nx > 65535 || ny > 65535 || nz > 65535 || slots < 1 || nrhs < 1 ||
       (max_items > 0 && out == nullptr))
     return -1;
   hz_grid g{nx, ny, nz, 0, nz, 1.0, 0};
@@ -800,7 +800,7 @@ extern "C" int hz_debug_plan_tiles(int nx, int ny, int nz, int lo_x, int hi_x, i
   const int ty = tm_rows(tx);
   const int lo[3] = {lo_x, lo_y, lo_z}, hi[3] = {hi_x, hi_y, hi_z};
   std::vector<int4> items;
-  tm_build_items(g, ldx, tx, ty, lo, hi, slots, ngroups, items);
+  tm_build_items(g, ldx, tx, ty, lo, hi, slots, nrhs, items);
   for (int n = 0; n < (int)items.size() && n < max_items; n++) {
     const int4 t = items[n];
     int* o = out + 5 * n;
@@ -844,16 +844,20 @@ hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int 
   TmLaunch L{nullptr, nullptr};
   long long nb = 0;
   if constexpr (TM) {
-    const int nr = tm_group(nrhs, epi), ng = (nrhs + nr - 1) / nr;
-    const hz_coeffs::TmPlan* pl = tm_plan(c, ng, nr);
+    const hz_coeffs::TmPlan* pl = tm_plan(c, nrhs);
     if (!pl) { set_error("tm_plan: device allocation / copy failed"); return HZ_ERR_CUDA; }
+    if (c->tm_ctr.n == 0) {   // work counter + finished-CTA ticket, zero between launches
+      HZ_CUDA(c->tm_ctr.ensure(2 * sizeof(unsigned)));
+      HZ_CUDA(cudaMemsetAsync(c->tm_ctr.p, 0, 2 * sizeof(unsigned), s));
+    }
     p.tm_work = pl->work.template as<int4>();
+    p.tm_ctr = c->tm_ctr.template as<unsigned>();
     p.tm_nitems = pl->n_items;
-    p.tm_nblocks = std::max(1, std::min(pl->n_items, pl->grid));   // persistent CTAs
+    p.tm_nblocks = std::max(1, std::min(pl->n_items * nrhs, pl->grid));   // persistent CTAs
     L.w = &c->tmap_w;
     L.u = tm_umap(c, p.u, nrhs);
     if (!L.u) return HZ_ERR_CUDA;
-    nb = p.tm_nblocks;
+    nb = (long long)pl->n_items;   // one dot partial slot per item and RHS
   } else {
     ApplyParams<R, S> pp = p;
     nb = apply_plan<R, S>(pp);
@@ -956,11 +960,37 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
     }
     std::vector<float> cr_f(cr.size());
     for (size_t i = 0; i < cr.size(); i++) cr_f[i] = (float)cr[i];
+    // complex64 tensor-map apply: the centre coefficients tabulated too (c0 = −(6c1 + 12c2 + 8c3),
+    // m0 = ω² − 6m1 − 12m2 − 8m3, evaluated in fp64), rows of TMTAB_STRIDE floats
+    // [c0 c1 c2 c3 | m0 m1 m2 m3 | differences of the same eight]
+    std::vector<float> ct_f((size_t)ng * TMTAB_STRIDE, 0.f);
+    {
+      std::vector<double> v8((size_t)ng * 8);
+      for (int i = 0; i < ng; i++) {
+        const double* o = &v6[(size_t)i * 6];
+        double* q = &v8[(size_t)i * 8];
+        q[0] = -(6.0 * o[0] + 12.0 * o[1] + 8.0 * o[2]);
+        q[1] = o[0];
+        q[2] = o[1];
+        q[3] = o[2];
+        q[4] = w2d - (6.0 * o[3] + 12.0 * o[4] + 8.0 * o[5]);
+        q[5] = o[3];
+        q[6] = o[4];
+        q[7] = o[5];
+      }
+      for (int i = 0; i < ng; i++)
+        for (int k = 0; k < 8; k++) {
+          ct_f[(size_t)i * TMTAB_STRIDE + k] = (float)v8[(size_t)i * 8 + k];
+          ct_f[(size_t)i * TMTAB_STRIDE + 8 + k] = (i + 1 < ng) ? (float)(v8[(size_t)(i + 1) * 8 + k] - v8[(size_t)i * 8 + k]) : 0.f;
+        }
+    }
     HZ_CUDA(c->ctab_d.ensure(cr.size() * sizeof(double)));
     HZ_CUDA(cudaMemcpy(c->ctab_d.p, cr.data(), cr.size() * sizeof(double), cudaMemcpyHostToDevice));
     if (sizeof(R) == 4) {
       HZ_CUDA(c->ctab_f.ensure(cr_f.size() * sizeof(float)));
       HZ_CUDA(cudaMemcpy(c->ctab_f.p, cr_f.data(), cr_f.size() * sizeof(float), cudaMemcpyHostToDevice));
+      HZ_CUDA(c->ctm_f.ensure(ct_f.size() * sizeof(float)));
+      HZ_CUDA(cudaMemcpy(c->ctm_f.p, ct_f.data(), ct_f.size() * sizeof(float), cudaMemcpyHostToDevice));
     }
     c->n_g_dev = ng;
     c->g_min = T.g_min;

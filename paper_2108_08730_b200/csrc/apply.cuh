@@ -25,6 +25,7 @@ enum { EPI_PLAIN = 0, EPI_DOT1 = 1, EPI_DOT4 = 2, EPI_RESID = 3 };
 __host__ __device__ constexpr int epi_k(int epi) { return epi == 1 ? 2 : (epi == 2 ? 7 : (epi == 3 ? 3 : 0)); }
 
 constexpr int TAB_STRIDE = 12;   // table row: t1 t2 mu0 mu1 mu2 | dt1 dt2 dmu0 dmu1 dmu2 | pad pad
+constexpr int TMTAB_STRIDE = 16;   // apply27_tm table row: c0..c3 m0..m3 | their differences
 
 // R: arithmetic type; S: storage type of the fields and the velocity (S = R except the
 // mixed-precision residual of the complex64 solver, which reads c64 storage and computes in fp64).
@@ -48,17 +49,20 @@ struct ApplyParams {
   // general launch work list per RHS: the boundary z-chunks (low, high) × all warps (nbx CTAs each),
   // then the interior z-chunks × the "frame" of warps outside the box (nbx_frame CTAs each)
   int nbound, nbx_frame, frame_warps, gen_blocks;
-  // complex64 tensor-map launch (apply27_tm): tm_nitems work items (tm_item), x/y-PML tiles first,
-  // walked round-robin by a persistent grid of tm_nblocks CTAs (= dot partial slots per RHS); tiles
-  // of tm_tx × tm_ty points; tm_org = first storage plane covered by the tensor maps (planes outside
-  // the global grid are zero-filled)
+  // complex64 tensor-map launch (apply27_tm): tm_nitems work items (tm_item: tile × z-chunk, x/y-PML
+  // tiles first), each run once per RHS, handed out by the counter tm_ctr[0] to a persistent grid of
+  // tm_nblocks CTAs (tm_ctr[1]: finished CTAs; both zero between launches); tiles of tm_tx × tm_ty
+  // points; tm_org = first storage plane covered by the tensor maps (planes outside the global grid
+  // are zero-filled)
   const int4* tm_work;
+  unsigned int* tm_ctr;
   int tm_nitems, tm_nblocks, tm_tx, tm_ty, tm_org;
   const S* v;                 // [nzl+2][ny][ldx] velocity incl. halo planes
   const S* w;                 // [nzl+2][ny][ldx] 1/v² incl. halo planes (apply input)
   const S* gam;               // GAm rule (A19): [5][nzl+2][ny][ldx] row weights (t1, t2, μ0, μ1, μ2)
                               // averaged over the 27 stencil nodes (stride fstride), or null (GA)
   const R* ctab;              // [n_g][CTAB_STRIDE] pre-scaled class coefficients + differences
+  const float* ctm;           // [n_g][TMTAB_STRIDE] complex64 tensor-map apply: c0..c3, m0..m3 + differences
   int tab_lo, tab_n;          // rows [tab_lo, tab_lo + tab_n) cover every G of the model (staged in smem)
   const CS* u;                // [nrhs][nzl+2][ny][ldx]
   const CS* ulo;              // optional low part of u (mixed-precision residual of the c64 solver:

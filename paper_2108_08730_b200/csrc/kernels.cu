@@ -720,11 +720,6 @@ static cudaError_t launch_one(const ApplyParams<R, S>& p, long long nb, cudaStre
 static thread_local int g_last_apply_launches = 0;
 int apply_last_launches() { return g_last_apply_launches; }
 
-// RHS per CTA of the complex64 tensor-map apply: two for a plain apply of several fields (the
-// coefficients are built once for both); one when a dot epilogue runs (its fp64 partials would not
-// fit the register budget of two)
-int tm_group(int nrhs, int epi) { return (nrhs > 1 && epi == EPI_PLAIN) ? 2 : 1; }
-
 // the tile-width instantiations live in their own translation units (tm64.cu, tm32.cu)
 cudaError_t launch_apply_tm(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, bool colloc, int epi,
                             cudaStream_t s) {
@@ -733,9 +728,6 @@ cudaError_t launch_apply_tm(const TmLaunch& L, const ApplyParams<float, float>& 
   if (p.tm_tx == 64) return launch_apply_tm_tx<64>(L, p, nrhs, colloc, epi, s);
   if (p.tm_tx == 32) return launch_apply_tm_tx<32>(L, p, nrhs, colloc, epi, s);
   return cudaErrorInvalidValue;
-}
-int tm_occupancy(int tab_n, int tx, int ty, int nr) {
-  return tx == 64 ? tm_occupancy_tx<64>(tab_n, nr) : tm_occupancy_tx<32>(tab_n, nr);
 }
 
 template <typename R, typename S, bool COLLOC, int EPI>

@@ -61,12 +61,9 @@ struct TmLaunch {
   const CUtensorMap* w;
   const CUtensorMap* u;
 };
-int tm_group(int nrhs, int epi);         // RHS per CTA
 template <int TX>
 cudaError_t launch_apply_tm_tx(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, bool colloc, int epi,
                                cudaStream_t s);
-template <int TX> int tm_occupancy_tx(int tab_n, int nr);
-int tm_occupancy(int tab_n, int tx, int ty, int nr);   // resident CTAs per SM
 cudaError_t launch_apply_tm(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, bool colloc, int epi,
                             cudaStream_t s);
 // visco-acoustic / variable-density apply (apply_medium.cu; NEXT-2, readings A24, A25): bmed = b,

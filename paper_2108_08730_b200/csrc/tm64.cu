@@ -3,5 +3,4 @@
 
 namespace hz {
 template cudaError_t launch_apply_tm_tx<64>(const TmLaunch&, const ApplyParams<float, float>&, int, bool, int, cudaStream_t);
-template int tm_occupancy_tx<64>(int, int);
 }  // namespace hz

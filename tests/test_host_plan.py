@@ -1,7 +1,7 @@
 """CPU checks of the complex64 tensor-map apply's work-list planner (host logic in libhz,
 include/hz_debug.h): for many grid sizes and PML widths every (point, plane) of the slab — pad columns
 included — is computed by exactly one work item (tile x0 computes the columns [x0 − 1, x0 + tx − 1)),
-the tile shape respects the kernel's limits (tx ∈ {32, 64}, ty·tx/2 = 384 threads), and the
+the tile shape respects the kernel's limits (tx ∈ {32, 64}, ty·tx/2 = 352 consumer threads), and the
 item's mode bits match the PML it
 touches: TM_PMLXY exactly on tiles holding x/y-PML points, TM_PMLZ exactly on chunks
 holding z-PML planes."""
@@ -13,12 +13,12 @@ import pytest
 hz = pytest.importorskip("paper_2108_08730_b200.hz", reason="libhz.so not built")
 
 
-def plan(nx, ny, nz, lo, hi, slots=296, ngroups=1):
+def plan(nx, ny, nz, lo, hi, slots=148, nrhs=1):
     lib = ctypes.CDLL(hz._LIBPATH)
     f = lib.hz_debug_plan_tiles
     f.restype = ctypes.c_int
     f.argtypes = [ctypes.c_int] * 11 + [ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
-    args = [nx, ny, nz, lo[0], hi[0], lo[1], hi[1], lo[2], hi[2], slots, ngroups]
+    args = [nx, ny, nz, lo[0], hi[0], lo[1], hi[1], lo[2], hi[2], slots, nrhs]
     n = f(*args, None, 0, None)
     assert n > 0
     buf = (ctypes.c_int * (5 * n))()
@@ -39,14 +39,14 @@ def pml_range(n, npml):
     return npml + 1, n - 2 - npml
 
 
-@pytest.mark.parametrize("ngroups", [1, 3])
+@pytest.mark.parametrize("nrhs", [1, 3])
 @pytest.mark.parametrize("nx,ny,nz,npml", CASES)
-def test_items_partition_the_slab(nx, ny, nz, npml, ngroups):
+def test_items_partition_the_slab(nx, ny, nz, npml, nrhs):
     lo, hi = zip(*[pml_range(n, npml) for n in (nx, ny, nz)])
-    items, tx, ty = plan(nx, ny, nz, lo, hi, ngroups=ngroups)
+    items, tx, ty = plan(nx, ny, nz, lo, hi, nrhs=nrhs)
     ldx = hz.hz_field_ldx(nx)
     assert ldx % 4 == 0 and ldx >= nx > ldx - 4
-    assert tx in (32, 64) and ty == 384 // (tx // 2)
+    assert tx in (32, 64) and ty * (tx // 2) == 352     # 11 consumer warps of whole tile rows
     ntx = -(-(ldx + 1) // tx)
     assert (ntx - 1) * tx - 1 < ldx                     # no tile wholly outside the pitched row
     count = np.zeros((nz, ny, ntx * tx + 1), np.int32)  # column c + 1 ↔ x = c (x = −1 first)
