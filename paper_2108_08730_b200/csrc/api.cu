@@ -11,6 +11,7 @@
 #include <climits>
 #include <condition_variable>
 #include <map>
+#include <queue>
 #include <mutex>
 #include <cmath>
 #include <complex>
@@ -715,12 +716,14 @@ const CUtensorMap* tm_umap(hz_coeffs* c, const void* u, int nrhs) {
   return &(c->tmap_u[key] = m);
 }
 
-// Work list: the ntx × nty tiles, each marching the slab in z-chunks (every item is run once per RHS,
-// handed out dynamically).  The chunk count balances the tail of the dynamic schedule (about half an
-// item per CTA) against the 2 halo planes a chunk re-reads; tiles with x/y-PML points run the x/y
-// corrections and are cut at the z-PML boundaries too; the other tiles run the PML-free planes
-// [zl, zh) and the z-PML chunks [0, zl), [zh, nzl) as separate items.  x/y-PML items come first
-// (they cost more per point, so they do not end up in the tail).
+// Work list: the ntx × nty tiles, each marching the slab in z-chunks; every item runs once per RHS,
+// handed out dynamically in list order.  A chunk re-reads 2 halo planes, and the schedule's makespan
+// depends on how the items pack onto the CTAs, so the planner simulates the greedy list schedule
+// (each item to the CTA that frees first; cost = planes read, x/y-PML tiles weighted 1.3) for n equal
+// chunks per tile and for one long + one short chunk per tile (short ones last), and keeps the split
+// with the shortest makespan.  Items of tiles holding x/y-PML points come first within a chunk;
+// TM_PMLZ marks chunks holding z-PML output planes (the kernel tests each plane).  Chunk-major order:
+// concurrently running CTAs work on neighbouring tiles at similar depths (halo rows shared in L2).
 void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], const int hi[3], int slots, int nrhs,
                     std::vector<int4>& out) {
   const int nzl = g.nz_local;
@@ -733,38 +736,48 @@ void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], 
       const bool pml = xa < lo[0] || x1 > hi[0] || y0 < lo[1] || y1 > hi[1] || hi[0] < lo[0] || hi[1] < lo[1];
       (pml ? xy : in).push_back({x0, y0});
     }
-  const double nt = (double)(xy.size() + in.size()) * std::max(1, nrhs);
-  int nch = 1;
-  double best = -1;
-  for (int n = 1; n <= std::max(1, nzl / 8); n++) {
-    const double per_cta = nt * n / std::max(1, slots);   // items per CTA
-    const double L = (double)nzl / n;
-    const double eff = per_cta / (per_cta + 0.5) * L / (L + 2.0);
-    if (eff > best + 1e-9) { best = eff; nch = n; }
+  const int rep = std::max(1, nrhs);
+  const int ncta = std::max(1, slots);
+  auto makespan = [&](const std::vector<int>& cuts) {
+    std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+    for (int k = 0; k < ncta; k++) q.push(0.0);
+    double mk = 0.0;
+    for (size_t k = 0; k + 1 < cuts.size(); k++) {
+      const double L = cuts[k + 1] - cuts[k] + 2.0;
+      for (int pass = 0; pass < 2; pass++) {
+        const size_t cnt = (pass == 0 ? xy.size() : in.size()) * rep;
+        const double cost = pass == 0 ? 1.3 * L : L;
+        for (size_t i = 0; i < cnt; i++) {
+          const double t = q.top() + cost;
+          q.pop();
+          q.push(t);
+          mk = std::max(mk, t);
+        }
+      }
+    }
+    return mk;
+  };
+  std::vector<int> best_cuts{0, nzl};
+  double best = makespan(best_cuts);
+  for (int n = 2; n <= std::max(1, nzl / 3); n++) {
+    std::vector<int> cuts;
+    for (int k = 0; k <= n; k++) cuts.push_back((int)((long long)nzl * k / n));
+    const double m = makespan(cuts);
+    if (m < best - 1e-9) { best = m; best_cuts = cuts; }
+  }
+  for (int t = 2; t <= nzl / 2; t++) {
+    const std::vector<int> cuts{0, nzl - t, nzl};
+    const double m = makespan(cuts);
+    if (m < best - 1e-9) { best = m; best_cuts = cuts; }
   }
   const int zl = std::min(std::max(lo[2] - g.z0, 0), nzl);
   const int zh = std::min(std::max(hi[2] - g.z0 + 1, zl), nzl);
-  const int nin = std::max(1, (int)std::lround((double)nch * (zh - zl) / std::max(1, nzl)));
   out.clear();
-  std::vector<int> cuts;
-  for (int k = 0; k <= nch; k++) cuts.push_back((int)((long long)nzl * k / nch));
-  cuts.push_back(zl);
-  cuts.push_back(zh);
-  std::sort(cuts.begin(), cuts.end());
-  cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
-  for (size_t k = 0; k + 1 < cuts.size(); k++) {   // chunk-major: concurrently running CTAs share z-planes in L2
-    const int a = cuts[k], b = cuts[k + 1];
-    const int mode = TM_PMLXY | ((a < zl || b > zh) ? TM_PMLZ : 0);
-    for (auto& t : xy) out.push_back(tm_item(t.first, t.second, a, b, mode));
-  }
-  for (auto& t : in) {
-    if (zl > 0) out.push_back(tm_item(t.first, t.second, 0, zl, TM_PMLZ));
-    if (zh < nzl) out.push_back(tm_item(t.first, t.second, zh, nzl, TM_PMLZ));
-  }
-  for (int k = 0; k < nin; k++) {
-    const int a = zl + (int)((long long)(zh - zl) * k / nin), b = zl + (int)((long long)(zh - zl) * (k + 1) / nin);
-    if (b > a)
-      for (auto& t : in) out.push_back(tm_item(t.first, t.second, a, b, TM_LEAN));
+  for (size_t k = 0; k + 1 < best_cuts.size(); k++) {
+    const int a = best_cuts[k], b = best_cuts[k + 1];
+    const int zm = (a < zl || b > zh) ? TM_PMLZ : 0;
+    for (auto& t : xy) out.push_back(tm_item(t.first, t.second, a, b, TM_PMLXY | zm));
+    for (auto& t : in) out.push_back(tm_item(t.first, t.second, a, b, zm));
   }
 }
 

@@ -45,7 +45,7 @@ namespace hz {
 constexpr int TM_NCW = 11;                    // consumer warps per CTA (+ producer: 12 warps, 3 per SMSP → ≤ 168 registers)
 constexpr int TM_NTHR = 32 * (TM_NCW + 1);    // + one producer warp (one CTA per SM)
 constexpr int TM_MAXTX = 64;                  // widest tile
-constexpr int TM_STAGES = 12;                 // ring depth (planes in flight per CTA)
+constexpr int TM_STAGES = 18;                 // ring depth (planes in flight per CTA)
 
 // PML mode bits of a work item: TM_PMLZ the chunk holds z-PML output planes, TM_PMLXY the tile holds
 // x/y-PML columns / rows; TM_LEAN neither
@@ -172,7 +172,10 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_tm);
   const uint32_t full0 = sbase, empty0 = sbase + 8u * S;
   volatile int* meta = reinterpret_cast<volatile int*>(smem_tm + 16 * S);        // item id per stage
-  double* red = reinterpret_cast<double*>(smem_tm + 256);                         // [TM_NCW][KK]
+  // header: full[S], empty[S] mbarriers, meta[S], then the item reduction scratch [TM_NCW][KK]
+  constexpr uint32_t RED_OFF = (20u * S + 7u) & ~7u;
+  static_assert(RED_OFF + 8u * TM_NCW * KK <= TM_HDR, "apply27_tm: shared header overflow");
+  double* red = reinterpret_cast<double*>(smem_tm + RED_OFF);
   unsigned char* ring = smem_tm + TM_HDR;
   const uint32_t ring_s = sbase + TM_HDR;
   float* stab = reinterpret_cast<float*>(smem_tm + tm_ring_end(TX, ty));

@@ -63,7 +63,9 @@ def test_items_partition_the_slab(nx, ny, nz, npml, nrhs):
         assert bool(mode & 2) == xy_pml                       # TM_PMLXY: the tile holds x/y-PML points
         assert bool(mode & 1) == bool(pz[z0:z1].any())       # TM_PMLZ: the chunk holds z-PML planes
     assert (count[:, :ny, 1:ldx + 1] == 1).all()
-    # x/y-PML tiles first (heavier, scheduled first)
-    xyi = (items[:, 4] & 2) != 0
-    if xyi.any() and (~xyi).any():
-        assert np.max(np.nonzero(xyi)) < np.min(np.nonzero(~xyi))
+    # within a z-chunk, x/y-PML tiles first (heavier, scheduled first)
+    for z0 in np.unique(items[:, 2]):
+        sel = items[items[:, 2] == z0]
+        xyi = (sel[:, 4] & 2) != 0
+        if xyi.any() and (~xyi).any():
+            assert np.max(np.nonzero(xyi)) < np.min(np.nonzero(~xyi))
