@@ -105,6 +105,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (n > (1u << 30)) __trap();
   }
 }
+// the producer's wait for a free stage: back off between polls (its spinning would take issue slots
+// from the consumer warps of its SM sub-partition)
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  for (uint32_t n = 0;; n++) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred P1;\n mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (n > (1u << 28)) __trap();
+    __nanosleep(64);
+  }
+}
 __device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
@@ -209,7 +224,7 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
         const int c2 = (it.y & 0xffff) - p.tm_org;   // map coordinate of input plane 0 (storage plane z0)
         const int n = (it.y >> 16) - (it.y & 0xffff) + 2;
         for (int j = 0; j < n; j++) {
-          mbar_wait(empty0 + 8u * s, ph ^ 1u);
+          mbar_wait_sleep(empty0 + 8u * s, ph ^ 1u);
           if (j == 0) meta[s] = g;
           const uint32_t bar = full0 + 8u * s, dst = ring_s + (uint32_t)s * stB;
           mbar_expect_tx(bar, txB);
@@ -246,9 +261,13 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
   int s = 0;          // stage of the next plane to wait for
   uint32_t ph = 0;    // its phase parity
   int rs = 0;         // next stage to release
+  // release the oldest held stage: lane 0 arrives (predicated, no branch) once the warp is done with it
+  const uint32_t lead = lane == 0 ? 1u : 0u;
   auto release = [&]() {
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8u * rs);
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %0, 0;\n @p mbarrier.arrive.shared::cta.b64 _, [%1];\n}\n" ::"r"(lead),
+                 "r"(empty0 + 8u * rs)
+                 : "memory");
     if (++rs == S) rs = 0;
   };
 
