@@ -45,7 +45,13 @@ namespace hz {
 constexpr int TM_NCW = 11;                    // consumer warps per CTA (+ producer: 12 warps, 3 per SMSP → ≤ 168 registers)
 constexpr int TM_NTHR = 32 * (TM_NCW + 1);    // + one producer warp (one CTA per SM)
 constexpr int TM_MAXTX = 64;                  // widest tile
-constexpr int TM_STAGES = 18;                 // ring depth (planes in flight per CTA)
+#ifndef HZ_TM_STAGES
+#define HZ_TM_STAGES 10
+#endif
+#ifndef HZ_TM_SLEEP_NS
+#define HZ_TM_SLEEP_NS 64
+#endif
+constexpr int TM_STAGES = HZ_TM_STAGES;       // ring depth (planes in flight per CTA)
 
 // PML mode bits of a work item: TM_PMLZ the chunk holds z-PML output planes, TM_PMLXY the tile holds
 // x/y-PML columns / rows; TM_LEAN neither
@@ -117,7 +123,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
         : "memory");
     if (done) return;
     if (n > (1u << 28)) __trap();
-    __nanosleep(64);
+    __nanosleep(HZ_TM_SLEEP_NS);
   }
 }
 __device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2) {
