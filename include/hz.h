@@ -289,6 +289,45 @@ long long hz_kernel_launch_count(void);
  * (re-assembling and re-solving every step then allocates nothing); this returns the cache to CUDA. */
 void hz_trim_memory(void);
 
+
+/* ---- NEXT-3: convergent Born series (CBS) reference wavefield ------------------------------------
+ * hz_cbs_solve: the paper's heterogeneous-model reference ("highly-accurate Convergent Born
+ * Series (CBS) method", iteration stopped at a backward error of 1e-12), restated in DESIGN.md reading A26
+ * and oracle/cbs.py.  Solves (∇² + k²) u = s, k = 2πf/v, with the spectral Laplacian on the model
+ * embedded in a periodic box padded by opts.pad cells per side (velocity of the nearest model node plus
+ * an absorbing term i·absorb·k0²·Σ_axes (d/pad)²), by the preconditioned Born iteration
+ *   u ← u − γ[u − G(V u − s)],  V = k² − k0² − iε,  γ = (i/ε)V,  G = 1/(|p|² − k0² − iε) (cuFFT Z2Z),
+ * k0² = mid-range Re k², ε = 1.05·max|k² − k0²|, until ‖(∇² + k²)u − s‖/‖s‖ ≤ opts.tol (checked every
+ * opts.check_every iterations).  complex128 throughout, one GPU (the context's device).
+ *   v        [nz][ny][nx] float64 velocities (m/s), dense (no pitch, no halo), host or device
+ *   src_xyz  nsrc × (x, y, z) node indices (host); s = amp/h³ at each node
+ *   amps     nsrc × (re, im) (host) or NULL (unit amplitudes)
+ *   u        [nz][ny][nx] interleaved complex128 (host or device, caller-owned): the model region
+ *   stats    may be NULL: iterations, final backward error, k0², ε, box dims, pad, seconds
+ * opts == NULL: hz_cbs_opts_default() (pad = -1: two of the longest wavelengths; absorb 1; tol 1e-12;
+ * max_iter 200000; check_every 20).  Returns HZ_OK, HZ_NOT_CONVERGED (max_iter reached; u = last
+ * iterate), HZ_ERR_INVALID_ARG (sizes, sources outside the model, options), HZ_ERR_DOMAIN (v ≤ 0 or
+ * non-finite, h or f ≤ 0), HZ_ERR_OOM / HZ_ERR_CUDA.  Synchronous on `stream`. */
+typedef struct {
+  int pad;            /* padding cells per side (< 0: two of the longest wavelengths)     */
+  double absorb;      /* absorbing strength a (α = a·k0²·Σ (d/pad)²)                      */
+  double tol;         /* backward-error tolerance (1e-12)                           */
+  int max_iter;
+  int check_every;    /* iterations between backward-error evaluations                    */
+} hz_cbs_opts;
+typedef struct {
+  int iterations;
+  double backward_error;
+  double k0sq, eps;
+  int box[3];         /* Nx, Ny, Nz of the FFT box */
+  int pad;
+  double seconds;
+} hz_cbs_stats;
+hz_cbs_opts hz_cbs_opts_default(void);
+hz_status hz_cbs_solve(hz_ctx* ctx, int nx, int ny, int nz, double h, const double* v, double freq, int nsrc,
+                       const long long* src_xyz, const double* amps, const hz_cbs_opts* opts, double* u,
+                       hz_cbs_stats* stats, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

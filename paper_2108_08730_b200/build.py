@@ -14,7 +14,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo"] + os.environ.get("HZ_EXTRA_NVCC", "").split() + ["-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I" + os.path.join(HERE, "..", "include")]
-SOURCES = ["kernels.cu", "tm64.cu", "tm32.cu", "apply_medium.cu", "api.cu", "table.cpp"]
+SOURCES = ["kernels.cu", "tm64.cu", "tm32.cu", "apply_medium.cu", "cbs.cu", "api.cu", "table.cpp"]
 
 
 def _newer(target, deps):
@@ -49,7 +49,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _newer(LIB, objs):
-        run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-ldl"])
+        run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-lcufft", "-ldl"])
     return LIB
 
 

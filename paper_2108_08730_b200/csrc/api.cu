@@ -305,6 +305,12 @@ struct hz_coeffs {
   long long fstride() const { return (long long)(grid.nz_local + 2) * plane(); }
   long long npoints() const { return (long long)grid.nx * grid.ny * grid.nz_local; }   // owned points
 };
+// internal helpers shared with the other translation units (hz_internal.h)
+namespace hz {
+void add_launches(long long n) { count_launch(n); }
+bool device_pointer(const void* p) { return is_device_ptr(p); }
+int ctx_device(const hz_ctx* c) { return c->device; }
+}  // namespace hz
 
 extern "C" {
 

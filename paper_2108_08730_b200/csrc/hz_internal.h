@@ -10,6 +10,9 @@
 namespace hz {
 
 void set_error(const std::string& msg);
+void add_launches(long long n);            // kernel launch counter (hz_kernel_launch_count)
+bool device_pointer(const void* p);         // p is device (or managed) memory
+int ctx_device(const hz_ctx* c);            // the context's CUDA device
 
 // Weight table (host copy, fp64).  rows5[i] = (ws1, ws2, mu0, mu1, mu2) at G_i = g_min + i*dg.
 struct Table {

@@ -64,6 +64,16 @@ class hz_solve_stats(ct.Structure):
                 ("stagnated", ct.c_int)]
 
 
+class hz_cbs_opts(ct.Structure):
+    _fields_ = [("pad", ct.c_int), ("absorb", ct.c_double), ("tol", ct.c_double), ("max_iter", ct.c_int),
+                ("check_every", ct.c_int)]
+
+
+class hz_cbs_stats(ct.Structure):
+    _fields_ = [("iterations", ct.c_int), ("backward_error", ct.c_double), ("k0sq", ct.c_double),
+                ("eps", ct.c_double), ("box", ct.c_int * 3), ("pad", ct.c_int), ("seconds", ct.c_double)]
+
+
 _vp = ct.c_void_p
 _P = ct.POINTER
 _sigs = {
@@ -95,6 +105,9 @@ _sigs = {
     "hz_eqerror": (ct.c_int, [_vp, _vp, _vp, _P(ct.c_longlong), ct.c_int, ct.c_double, _P(ct.c_double), _vp]),
     "hz_table_dispersion": (ct.c_int, [_vp, ct.c_int, _P(ct.c_double), ct.c_int, _P(ct.c_double), _P(ct.c_double),
                                        _P(ct.c_double), _vp]),
+    "hz_cbs_opts_default": (hz_cbs_opts, []),
+    "hz_cbs_solve": (ct.c_int, [_vp, ct.c_int, ct.c_int, ct.c_int, ct.c_double, _vp, ct.c_double, ct.c_int,
+                                _P(ct.c_longlong), _P(ct.c_double), _P(hz_cbs_opts), _vp, _P(hz_cbs_stats), _vp]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
@@ -366,6 +379,39 @@ def hz_eqerror(c: Coeffs, u_ref, u, src_xyz, npml_mask: int, ball_cells: float =
                            _stream_ptr(stream)),
            "hz_eqerror")
     return out.value
+
+
+def hz_cbs_solve(ctx: Ctx, v, h: float, freq: float, src_xyz, u, amps=None, pad=-1, absorb=1.0, tol=1e-12,
+                 max_iter=200000, check_every=20, stream=None):
+    """Convergent Born series reference (NEXT-3, see include/hz.h): v is a dense [nz][ny][nx] float64
+    array (numpy or torch, host or device), u a caller-owned complex128 [nz][ny][nx] array of the same
+    placement.  Returns (status, stats dict)."""
+    nz, ny, nx = (int(t) for t in v.shape)
+    if tuple(u.shape) != (nz, ny, nx):
+        raise ValueError("u must have the model's shape")
+    src = np.ascontiguousarray(src_xyz, dtype=np.int64).reshape(-1, 3)
+    a = None
+    if amps is not None:
+        av = np.asarray(amps, dtype=np.complex128).reshape(-1)
+        a = np.ascontiguousarray(np.stack([av.real, av.imag], axis=1))
+
+    def ptr(x, dt):
+        if hasattr(x, "data_ptr"):
+            if str(x.dtype) != dt or not x.is_contiguous():
+                raise ValueError(f"expected a contiguous {dt} tensor")
+            return ct.c_void_p(x.data_ptr())
+        if x.dtype != np.dtype(dt.replace("torch.", "")) or not x.flags.c_contiguous:
+            raise ValueError(f"expected a contiguous {dt} array")
+        return ct.c_void_p(x.ctypes.data)
+    o = hz_cbs_opts(pad, absorb, tol, max_iter, check_every)
+    st = hz_cbs_stats()
+    status = _check(_lib.hz_cbs_solve(ctx._h, nx, ny, nz, float(h), ptr(v, "torch.float64"), float(freq), src.shape[0],
+                                      src.ctypes.data_as(_P(ct.c_longlong)),
+                                      a.ctypes.data_as(_P(ct.c_double)) if a is not None else None, ct.byref(o),
+                                      ptr(u, "torch.complex128"), ct.byref(st), _stream_ptr(stream)), "hz_cbs_solve")
+    stats = {k: getattr(st, k) for k, _ in hz_cbs_stats._fields_}
+    stats["box"] = tuple(st.box)
+    return status, stats
 
 
 def hz_table_dispersion(table: Table, G, theta, phi, stream=None) -> np.ndarray:
