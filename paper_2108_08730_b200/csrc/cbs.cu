@@ -84,10 +84,17 @@ __device__ __forceinline__ void atomic_max_pos(unsigned long long* m, double x) 
 __global__ void cbs_vrange_kernel(const double* __restrict__ v, long long n, unsigned long long* out) {
   __shared__ double smin[256], smax[256];
   double lo = HUGE_VAL, hi = 0.0;
+  unsigned long long bad = 0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    lo = fmin(lo, v[i]);
-    hi = fmax(hi, v[i]);
+    const double x = v[i];
+    if (!(x > 0.0) || !isfinite(x)) {
+      bad++;
+      continue;
+    }
+    lo = fmin(lo, x);
+    hi = fmax(hi, x);
   }
+  if (bad) atomicAdd(out + 3, bad);
   smin[threadIdx.x] = lo;
   smax[threadIdx.x] = hi;
   __syncthreads();
@@ -307,7 +314,7 @@ extern "C" hz_status hz_cbs_solve(hz_ctx* ctx, int nx, int ny, int nz, double h,
     vd = tmp;
   }
   unsigned long long* red = nullptr;
-  CBS_CUDA(mem.get(&red, 3));
+  CBS_CUDA(mem.get(&red, 4));
   auto bits = [](double x) {
     unsigned long long b;
     std::memcpy(&b, &x, sizeof(b));
@@ -318,15 +325,15 @@ extern "C" hz_status hz_cbs_solve(hz_ctx* ctx, int nx, int ny, int nz, double h,
     std::memcpy(&x, &b, sizeof(x));
     return x;
   };
-  const unsigned long long init[3] = {bits(HUGE_VAL), 0ull, 0ull};
+  const unsigned long long init[4] = {bits(HUGE_VAL), 0ull, 0ull, 0ull};   // min v, max v, max|k²−k0²|, invalid v
   CBS_CUDA(cudaMemcpyAsync(red, init, sizeof(init), cudaMemcpyHostToDevice, s));
   cbs_vrange_kernel<<<296, 256, 0, s>>>(vd, nm, red);
   CBS_CUDA(cudaGetLastError());
-  unsigned long long hr[3];
+  unsigned long long hr[4];
   CBS_CUDA(cudaMemcpyAsync(hr, red, sizeof(hr), cudaMemcpyDeviceToHost, s));
   CBS_CUDA(cudaStreamSynchronize(s));
   const double vmin = dbl(hr[0]), vmax = dbl(hr[1]);
-  if (!(vmin > 0) || !std::isfinite(vmax)) {
+  if (hr[3] != 0 || !(vmin > 0) || !std::isfinite(vmax)) {
     set_error("hz_cbs_solve: velocities must be positive and finite");
     return HZ_ERR_DOMAIN;
   }
