@@ -223,6 +223,11 @@ typedef struct {
   int stall_window;  /* a RHS whose true residual has not dropped 10% within this many
                         iterations is retired (HZ_NOT_CONVERGED, stats.stagnated = 1);
                         0 = default max(20*replace_every, 1000); < 0 = never            */
+  int precond;       /* 0: none.  1: right preconditioning by one V-cycle of the complex
+                        shifted-Laplacian multigrid (∇² + (1 + 0.5i)ω²/v², damped Jacobi,
+                        DESIGN.md reading A27; NEXT-4, the iterative route of P:35).
+                        complex64, ell = 1, one rank, GA / Eq. 8 / Eq. "10" coefficients
+                        (not the visco-acoustic medium); otherwise HZ_ERR_INVALID_ARG. */
 } hz_solve_opts;
 
 typedef struct {

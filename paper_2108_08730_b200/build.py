@@ -14,7 +14,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo"] + os.environ.get("HZ_EXTRA_NVCC", "").split() + ["-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I" + os.path.join(HERE, "..", "include")]
-SOURCES = ["kernels.cu", "tm64.cu", "tm32.cu", "apply_medium.cu", "cbs.cu", "api.cu", "table.cpp"]
+SOURCES = ["kernels.cu", "tm64.cu", "tm32.cu", "apply_medium.cu", "cbs.cu", "mg.cu", "api.cu", "table.cpp"]
 
 
 def _newer(target, deps):

@@ -22,6 +22,10 @@
 #include <vector>
 
 #include "hz_debug.h"
+
+#ifndef HZ_MG_BETA
+#define HZ_MG_BETA 0.5   // complex shift of the multigrid preconditioner (reading A27)
+#endif
 #include "hz_internal.h"
 #include "kernels.h"
 
@@ -228,6 +232,11 @@ struct SolverWork {
   DBuf state, active;
   DBuf partials, tickets;
   DBuf hb, hx;                  // staging for host b / x
+  DBuf ph, sh;                  // right preconditioning: M⁻¹p, M⁻¹s
+  struct MgDel {
+    void operator()(MgHierarchy* m) const { mg_destroy(m); }
+  };
+  std::unique_ptr<MgHierarchy, MgDel> mg;   // complex shifted-Laplacian multigrid (precond = 1)
 };
 
 struct hz_coeffs {
@@ -240,6 +249,7 @@ struct hz_coeffs {
   DBuf gam;                    // GAm: [5][nzl+2][ny][ldx] 27-node mean weights (t1, t2, mu0, mu1, mu2)
   double freq = 0, omega = 0, h = 0;
   double v_pml = 0;
+  double vmin = 0, vmax = 0;   // the model's velocity range (all ranks)
   hz_pml pml{};
   Table table;                 // host copy actually used (rank 0's on all ranks)
   int n_g_dev = 0;             // rows uploaded (>= 2)
@@ -1101,6 +1111,8 @@ hz_status assemble_t(hz_ctx* ctx, const hz_grid* g, const void* v_in, double fre
     c->tab_n = hi_r - lo_r + 1;
   }
   // ---- PML (host, double) → device deltas δ± = a± − 1/h²
+  c->vmin = vmin;
+  c->vmax = vmax;
   c->v_pml = (c->pml.v_pml > 0) ? c->pml.v_pml : vmax;
   const int ns[3] = {g->nx, g->ny, g->nz_global};
   const double ih2 = 1.0 / (g->h * g->h);
@@ -1594,9 +1606,14 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
     HZ_CUDA(w.dotG.ensure(sizeof(double) * nrhs));
   }
   if (sizeof(R) == 4) HZ_CUDA(w.xlo.ensure(fb));
+  const bool pre = o.precond == 1 && sizeof(R) == 4;
+  if (pre) {
+    HZ_CUDA(w.ph.ensure(fb));
+    HZ_CUDA(w.sh.ensure(fb));
+  }
   // the workspace starts at zero: pad columns stay 0 in every Krylov vector (the applies write
   // zeros there, the fp64 residual does not touch them), so the flat dot products see only points
-  for (DBuf* d : {&w.rhat, &w.p, &w.v, &w.t, &w.r, &w.r1, &w.r2, &w.xlo})
+  for (DBuf* d : {&w.rhat, &w.p, &w.v, &w.t, &w.r, &w.r1, &w.r2, &w.xlo, &w.ph, &w.sh})
     if (d->p && d->n >= fb) HZ_CUDA(cudaMemsetAsync(d->p, 0, fb, s));
   HZ_CUDA(w.dotA.ensure(sizeof(double) * 2 * nrhs));
   HZ_CUDA(w.dotB.ensure(sizeof(double) * 7 * nrhs));
@@ -1670,6 +1687,35 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   q.tickets = w.tickets.as<unsigned>();
   q.state = w.state.as<SolverState>();
   q.active = w.active.as<int>();
+  if constexpr (sizeof(R) == 4) {
+    if (pre) {
+      if (!w.mg) {
+        MgSpec sp;
+        sp.nx = c->grid.nx;
+        sp.ny = c->grid.ny;
+        sp.nz = c->grid.nz_local;
+        sp.ldx = c->ldx;
+        sp.plane = c->plane();
+        sp.fstride = c->fstride();
+        sp.w = c->w.as<float>();
+        sp.h = c->h;
+        sp.omega = c->omega;
+        sp.beta = HZ_MG_BETA;
+        sp.vmin = c->vmin;
+        sp.vmax = c->vmax;
+        sp.v_pml = c->v_pml;
+        sp.r_coeff = c->pml.r_coeff;
+        sp.npml = c->pml.npml;
+        sp.nrhs = nrhs;
+        sp.max_levels = 12;
+        MgHierarchy* m = nullptr;
+        HZ_CUDA(mg_create(sp, &m));
+        w.mg.reset(m);
+      }
+      q.ph = w.ph.as<C>();
+      q.sh = w.sh.as<C>();
+    }
+  }
 
   // r = b − A x (RESID epilogue; writes r, ‖r‖², (r̂0, r)).  For complex64 the residual is
   // computed in fp64 arithmetic on the c64 storage (reading A21): the fp32 apply's rounding
@@ -1784,12 +1830,13 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
   };
 
   // one operator apply with a dot epilogue (+ the ranks' sum of its dots)
-  auto apply_dots = [&](DBuf& in, DBuf& out, int epi, const C* rh, DBuf& dots, int ndots) -> hz_status {
+  auto apply_dots = [&](DBuf& in, DBuf& out, int epi, const C* rh, DBuf& dots, int ndots, const C* sdot = nullptr) -> hz_status {
     HZ_TRY(halo_exchange(c, in.p, nrhs, sizeof(C), s));
     ApplyParams<R> p = base;
     p.u = in.as<C>();
     p.au = out.as<C>();
     p.rhat = rh;
+    p.bvec = sdot;   // DOT4 operand s when it is not the input (right preconditioning)
     p.dots = dots.as<double>();
     timer.mark(s);
     HZ_TRY(apply_launch<R, R>(c, p, nrhs, epi, s));
@@ -1809,7 +1856,21 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
 
   while (n_active() > 0 && it < o.max_iter) {
     int inc = 1;
-    if (!ell2) {
+    if (!ell2 && pre) {   // right preconditioning (A27): v = A M⁻¹p, t = A M⁻¹s, x += α M⁻¹p + ω M⁻¹s
+      if constexpr (sizeof(R) == 4) {
+        long long nl = 0;
+        HZ_CUDA(mg_vcycle(w.mg.get(), w.p.as<float2>(), w.ph.as<float2>(), nrhs, w.active.as<int>(), s, &nl));
+        count_launch(nl);
+        HZ_TRY(apply_dots(w.ph, w.v, EPI_DOT1, rh, w.dotA, 2));
+        HZ_TRY(vec(BICG_S));
+        nl = 0;
+        HZ_CUDA(mg_vcycle(w.mg.get(), w.r.as<float2>(), w.sh.as<float2>(), nrhs, w.active.as<int>(), s, &nl));
+        count_launch(nl);
+        HZ_TRY(apply_dots(w.sh, w.t, EPI_DOT4, rh, w.dotB, 7, w.r.as<C>()));   // (t,s) with s, not M⁻¹s
+        HZ_TRY(vec(BICG_UPDATE));
+      }
+      HZ_TRY(allreduce_sum(c, w.dotR.as<double>(), 3 * (size_t)nrhs, s));
+    } else if (!ell2) {
       HZ_TRY(apply_dots(w.p, w.v, EPI_DOT1, rh, w.dotA, 2));   // v = A p, (r̂0, v)
       HZ_TRY(vec(BICG_S));                                      // s = r − α v (in r)
       HZ_TRY(apply_dots(w.r, w.t, EPI_DOT4, rh, w.dotB, 7));   // t = A s, (t,s), (t,t), (r̂0,s), (r̂0,t)
@@ -1944,6 +2005,11 @@ extern "C" hz_status hz_solve(const hz_coeffs* c, const void* b, void* x, int nr
   if (o.check_every < 1) { set_error("hz_solve: check_every must be >= 0"); return HZ_ERR_INVALID_ARG; }
   if (o.ell == 0) o.ell = 1;
   if (o.ell != 1 && o.ell != 2) { set_error("hz_solve: ell must be 1 (BiCGSTAB) or 2 (BiCGStab(2))"); return HZ_ERR_INVALID_ARG; }
+  if (o.precond != 0 && o.precond != 1) { set_error("hz_solve: precond must be 0 or 1"); return HZ_ERR_INVALID_ARG; }
+  if (o.precond == 1 && (c->dtype != HZ_C64 || o.ell != 1 || c->ctx->nranks != 1 || c->medium || c->grid.nz_local != c->grid.nz_global)) {
+    set_error("hz_solve: the multigrid preconditioner needs complex64, ell = 1, one rank and the acoustic (rho = 1) operator");
+    return HZ_ERR_INVALID_ARG;
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return c->dtype == HZ_C64 ? solve_t<float>(c, b, x, nrhs, o, relres_out, iters_out, stats, s)
                             : solve_t<double>(c, b, x, nrhs, o, relres_out, iters_out, stats, s);

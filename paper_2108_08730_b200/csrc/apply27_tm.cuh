@@ -496,7 +496,8 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
           if (EPI == EPI_DOT1) {
             tm_cdot(pp[0], pp[1], rh[e], a);
           } else if (EPI == EPI_DOT4) {
-            const C sv = in_[e] ? B.u0[e] : z2;
+            // s = the apply's input, or (right-preconditioned solve: the input is M⁻¹s) p.bvec
+            const C sv = in_[e] ? (p.bvec != nullptr ? __ldg(p.bvec + oel + (uint32_t)e) : B.u0[e]) : z2;
             tm_cdot(pp[0], pp[1], a, sv);
             tm_norm(pp[2], a);
             tm_cdot(pp[3], pp[4], rh[e], sv);

@@ -366,8 +366,10 @@ __global__ void __launch_bounds__(NT) bicg_update_kernel(VecParams<R> q) {
     C xx = X_[k];
     // x += α p + ω s; with q.xlo the iterate is the double-word x + xlo (compensated update)
     C dx;
-    dx.x = (a.x * pp.x - a.y * pp.y) + (w.x * s.x - w.y * s.y);
-    dx.y = (a.x * pp.y + a.y * pp.x) + (w.x * s.y + w.y * s.x);
+    const C dp_ = q.ph != nullptr ? q.ph[off + i] : pp;   // right preconditioning: M⁻¹p, M⁻¹s
+    const C ds_ = q.sh != nullptr ? q.sh[off + i] : s;
+    dx.x = (a.x * dp_.x - a.y * dp_.y) + (w.x * ds_.x - w.y * ds_.y);
+    dx.y = (a.x * dp_.y + a.y * dp_.x) + (w.x * ds_.y + w.y * ds_.x);
     if (q.xlo != nullptr) {
       C lo = L_[k];
       two_sum(xx.x, dx.x + lo.x, xx.x, lo.x);

@@ -28,6 +28,7 @@ struct VecParams {
   C *x, *r, *rhat, *p, *v, *t;
   C* xlo;              // compensation term of the iterate (complex64 solver) or null
   C *r1, *r2;          // BiCGStab(2) only: A-images of r0 (= r) within one outer step
+  const C *ph, *sh;    // right-preconditioned BiCGSTAB: x += α M⁻¹p + ω M⁻¹s (null: x += α p + ω s)
   const double* dotA;  // [nrhs][2]
   const double* dotB;  // [nrhs][7]
   double* dotR;        // [nrhs][3]
@@ -106,5 +107,20 @@ template <typename R> cudaError_t launch_bicgl(int which, const VecParams<R>& q,
 template <typename R>
 cudaError_t launch_norm2(const typename Cx<R>::T* f, long long fstride, long long plane, long long n, int nx, int ldx,
                          int nrhs, int nblocks, double* partials, double* out, unsigned int* tickets, cudaStream_t s);
+
+// complex shifted-Laplacian multigrid preconditioner (mg.cu; hz_solve_opts.precond = 1)
+struct MgSpec {
+  int nx, ny, nz;                 // the slab (single rank)
+  long long ldx, plane, fstride;  // field layout ([nrhs][nz+2][ny][ldx])
+  const float* w;                 // 1/v² in the field layout (first field)
+  double h, omega, beta, vmin, vmax, v_pml, r_coeff;
+  int npml, nrhs, max_levels;
+};
+struct MgHierarchy;
+cudaError_t mg_create(const MgSpec& spec, MgHierarchy** out);
+void mg_destroy(MgHierarchy* m);
+int mg_levels(const MgHierarchy* m);
+cudaError_t mg_vcycle(MgHierarchy* m, const float2* f, float2* e, int nrhs, const int* active, cudaStream_t s,
+                      long long* launches);
 
 }  // namespace hz

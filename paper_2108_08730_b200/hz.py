@@ -53,7 +53,7 @@ class hz_pml(ct.Structure):
 class hz_solve_opts(ct.Structure):
     _fields_ = [("rtol", ct.c_double), ("max_iter", ct.c_int), ("replace_every", ct.c_int),
                 ("check_every", ct.c_int), ("timing", ct.c_int), ("ell", ct.c_int),
-                ("stall_window", ct.c_int)]
+                ("stall_window", ct.c_int), ("precond", ct.c_int)]
 
 
 class hz_solve_stats(ct.Structure):
@@ -344,13 +344,13 @@ def hz_apply_impedance(c: Coeffs, u, au, nrhs: Optional[int] = None, stream=None
 
 
 def hz_solve(c: Coeffs, b, x, nrhs: Optional[int] = None, rtol=1e-6, max_iter=20000, replace_every=50,
-             check_every=10, timing=False, ell=1, stall_window=0, stream=None):
+             check_every=10, timing=False, ell=1, stall_window=0, precond=0, stream=None):
     """Zero for rtol / max_iter / replace_every / check_every / ell / stall_window selects the default
     (include/hz.h); replace_every < 0 turns residual replacement off."""
     """Returns (status, relres[nrhs], iters[nrhs], stats dict).  ell = 1: BiCGSTAB; 2: BiCGStab(2)."""
     if nrhs is None:
         nrhs = b.shape[0]
-    o = hz_solve_opts(rtol, max_iter, replace_every, check_every, 1 if timing else 0, ell, stall_window)
+    o = hz_solve_opts(rtol, max_iter, replace_every, check_every, 1 if timing else 0, ell, stall_window, precond)
     rel = (ct.c_double * nrhs)()
     its = (ct.c_int * nrhs)()
     stt = hz_solve_stats()

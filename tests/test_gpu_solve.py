@@ -250,3 +250,38 @@ def test_stall_window(hz, ctx, table, ell):
     st, rel, its, stats = hz.hz_solve(C, b, x, rtol=1e-14, max_iter=20000, stall_window=100, ell=ell)
     assert st == hz.HZ_NOT_CONVERGED and stats["stagnated"] == 1 and its[0] < 20000, (st, its, stats)
     assert rel[0] <= 1e-6
+
+
+@pytest.mark.parametrize("key", [1, "crop4_5hz"])
+def test_multigrid_preconditioned_solve(hz, ctx, table, ga_table, key):
+    """NEXT-4 (opt-in, reading A27): right preconditioning by one complex shifted-Laplacian multigrid
+    V-cycle.  Where it converges (config 1, the config-4 crop at 5 Hz) the wavefield equals the oracle's
+    within the north star's 1e-4, with fewer iterations than the unpreconditioned BiCGSTAB."""
+    cfg = synth.get_config(1) if key == 1 else synth.crop_config(4, 5.0)
+    v, C = setup(hz, ctx, table, cfg, "c64")
+    nodes = synth.source_nodes(cfg)[:1]
+    b = C.alloc_field(1)
+    hz.hz_point_sources(C, nodes, b)
+    x = C.alloc_field(1)
+    st, relres, its, _ = hz.hz_solve(C, b, x, rtol=1e-6, max_iter=20000, precond=1)
+    assert st == hz.HZ_OK and relres[0] <= 1e-6, (st, relres, its)
+    x0 = C.alloc_field(1)
+    st0, _, its0, _ = hz.hz_solve(C, b, x0, rtol=1e-6, max_iter=20000)
+    assert its[0] < its0[0], (its, its0)
+    G = golden(key)
+    u = x[0, 1:-1, :, :cfg.nx].cpu().numpy().astype(np.complex128).ravel()
+    assert rel(u[G["idx"]], G["values"][0]) <= 1e-4
+
+
+def test_multigrid_preconditioner_rejects_unsupported(hz, ctx, table):
+    cfg = synth.get_config(1)
+    v, C = setup(hz, ctx, table, cfg, "c128")
+    b = C.alloc_field(1)
+    x = C.alloc_field(1)
+    with pytest.raises(hz.HzError):
+        hz.hz_solve(C, b, x, precond=1)      # complex128
+    v, C = setup(hz, ctx, table, cfg, "c64")
+    b = C.alloc_field(1)
+    x = C.alloc_field(1)
+    with pytest.raises(hz.HzError):
+        hz.hz_solve(C, b, x, precond=1, ell=2)
