@@ -273,6 +273,7 @@ struct hz_coeffs {
   struct TmPlan {
     DBuf work;
     int n_items = 0;
+    int n_int = 0;  // halo-overlapped apply (nranks > 1): items [0, n_int) need no halo plane
     int grid = 1;   // resident CTAs: SMs × CTAs per SM
   };
   std::map<int, std::unique_ptr<TmPlan>> tm_plans;   // per RHS count
@@ -305,6 +306,25 @@ struct hz_coeffs {
     }
   };
   HostIO hio;
+  // halo-overlapped apply (nranks > 1): the exchange runs on `cs` while the interior items run on the
+  // caller's stream; `join` orders the boundary items after it
+  struct Overlap {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaError_t init() {
+      if (cs) return cudaSuccess;
+      cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+      return e;
+    }
+    ~Overlap() {
+      if (cs) cudaStreamDestroy(cs);
+      if (fork) cudaEventDestroy(fork);
+      if (join) cudaEventDestroy(join);
+    }
+  };
+  Overlap ovl;
   // visco-acoustic / variable-density medium (hz_coeffs_set_medium; readings A24, A25): every apply
   // goes through apply_medium.cu with b and κ⁻¹ = b/(v²(1 − i/(2Q))²), [nzl+2][ny][ldx] with halos
   bool medium = false;
@@ -740,11 +760,10 @@ const CUtensorMap* tm_umap(hz_coeffs* c, const void* u, int nrhs) {
 // with the shortest makespan.  Items of tiles holding x/y-PML points come first within a chunk;
 // TM_PMLZ marks chunks holding z-PML output planes (the kernel tests each plane).  Chunk-major order:
 // concurrently running CTAs work on neighbouring tiles at similar depths (halo rows shared in L2).
-void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], const int hi[3], int slots, int nrhs,
-                    std::vector<int4>& out) {
-  const int nzl = g.nz_local;
+// the tiles of a plane: those holding x/y-PML points (xy) and the others (in)
+void tm_tiles(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], const int hi[3],
+              std::vector<std::pair<int, int>>& xy, std::vector<std::pair<int, int>>& in) {
   const int ntx = (ldx + 1 + tx - 1) / tx, nty = (g.ny + ty - 1) / ty;
-  std::vector<std::pair<int, int>> xy, in;
   for (int j = 0; j < nty; j++)
     for (int i = 0; i < ntx; i++) {
       const int x0 = i * tx, y0 = j * ty;   // computes columns [x0 − 1, x0 + tx − 1)
@@ -752,6 +771,19 @@ void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], 
       const bool pml = xa < lo[0] || x1 > hi[0] || y0 < lo[1] || y1 > hi[1] || hi[0] < lo[0] || hi[1] < lo[1];
       (pml ? xy : in).push_back({x0, y0});
     }
+}
+// TM_PMLZ if the local output planes [a, b) of the slab hold z-PML planes
+int tm_zmode(const hz_grid& g, const int lo[3], const int hi[3], int a, int b) {
+  const int nzl = g.nz_local;
+  const int zl = std::min(std::max(lo[2] - g.z0, 0), nzl);
+  const int zh = std::min(std::max(hi[2] - g.z0 + 1, zl), nzl);
+  return (a < zl || b > zh) ? TM_PMLZ : 0;
+}
+void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], const int hi[3], int slots, int nrhs,
+                    std::vector<int4>& out) {
+  const int nzl = g.nz_local;
+  std::vector<std::pair<int, int>> xy, in;
+  tm_tiles(g, ldx, tx, ty, lo, hi, xy, in);
   const int rep = std::max(1, nrhs);
   const int ncta = std::max(1, slots);
   auto makespan = [&](const std::vector<int>& cuts) {
@@ -786,12 +818,10 @@ void tm_build_items(const hz_grid& g, int ldx, int tx, int ty, const int lo[3], 
     const double m = makespan(cuts);
     if (m < best - 1e-9) { best = m; best_cuts = cuts; }
   }
-  const int zl = std::min(std::max(lo[2] - g.z0, 0), nzl);
-  const int zh = std::min(std::max(hi[2] - g.z0 + 1, zl), nzl);
   out.clear();
   for (size_t k = 0; k + 1 < best_cuts.size(); k++) {
     const int a = best_cuts[k], b = best_cuts[k + 1];
-    const int zm = (a < zl || b > zh) ? TM_PMLZ : 0;
+    const int zm = tm_zmode(g, lo, hi, a, b);
     for (auto& t : xy) out.push_back(tm_item(t.first, t.second, a, b, TM_PMLXY | zm));
     for (auto& t : in) out.push_back(tm_item(t.first, t.second, a, b, zm));
   }
@@ -803,9 +833,38 @@ const hz_coeffs::TmPlan* tm_plan(hz_coeffs* c, int nrhs) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->ctx->device);
   std::vector<int4> items;
-  tm_build_items(c->grid, c->ldx, c->tm_tx, c->tm_ty, c->lo, c->hi, sms, nrhs, items);
+  // several slabs: the output planes next to an exchanged halo (local 0 below a lower neighbour,
+  // nzl − 1 below an upper one) become one-plane items at the end of the list, so that the items
+  // before them can run while the halo planes move (apply_launch)
+  const hz_grid& g = c->grid;
+  const int ia = (c->ctx->nranks > 1 && c->ctx->rank > 0) ? 1 : 0;
+  const int ib = g.nz_local - ((c->ctx->nranks > 1 && c->ctx->rank < c->ctx->nranks - 1) ? 1 : 0);
+  int n_int;
+  if (c->ctx->nranks > 1 && ib - ia >= 2) {
+    hz_grid gi = g;   // the interior planes [ia, ib) as a slab of their own
+    gi.z0 += ia;
+    gi.nz_local = ib - ia;
+    tm_build_items(gi, c->ldx, c->tm_tx, c->tm_ty, c->lo, c->hi, sms, nrhs, items);
+    for (int4& t : items) {
+      const int a = (t.y & 0xffff) + ia, b = (t.y >> 16) + ia;
+      t.y = a | (b << 16);
+    }
+    n_int = (int)items.size();
+    std::vector<std::pair<int, int>> xy, in;
+    tm_tiles(g, c->ldx, c->tm_tx, c->tm_ty, c->lo, c->hi, xy, in);
+    for (int z : {0, g.nz_local - 1}) {
+      if ((z == 0 && ia == 0) || (z == g.nz_local - 1 && ib == g.nz_local)) continue;
+      const int zm = tm_zmode(g, c->lo, c->hi, z, z + 1);
+      for (auto& t : xy) items.push_back(tm_item(t.first, t.second, z, z + 1, TM_PMLXY | zm));
+      for (auto& t : in) items.push_back(tm_item(t.first, t.second, z, z + 1, zm));
+    }
+  } else {
+    tm_build_items(g, c->ldx, c->tm_tx, c->tm_ty, c->lo, c->hi, sms, nrhs, items);
+    n_int = c->ctx->nranks > 1 ? 0 : (int)items.size();   // thin slab: everything after the exchange
+  }
   std::unique_ptr<hz_coeffs::TmPlan> pl(new hz_coeffs::TmPlan);
   pl->n_items = (int)items.size();
+  pl->n_int = n_int;
   pl->grid = sms;   // one persistent CTA per SM
   if (pl->work.ensure(std::max<size_t>(1, items.size()) * sizeof(int4)) != cudaSuccess) return nullptr;
   if (!items.empty() && cudaMemcpy(pl->work.p, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice) != cudaSuccess)
@@ -844,10 +903,19 @@ namespace {
 // One operator apply: complex64 (arithmetic and storage) through the tensor-map kernel, everything
 // else (complex128, the fp64 residual of the complex64 solver) through the register path.  Dot
 // epilogues get their partial / ticket scratch here.
+// exch: first exchange the halo planes of p.u with the z neighbours (nranks > 1).  The complex64
+// tensor-map apply overlaps that exchange with its interior items: they run on s while the halo
+// planes move on the overlap stream, then the one-plane boundary items (and the dot reduction over
+// the whole list) run after the join.  Every point is computed by the same operation sequence either
+// way, so the output is bitwise that of the exchange-then-apply order.
 template <typename R, typename S>
-hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int epi, cudaStream_t s) {
+hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int epi, cudaStream_t s, bool exch = false) {
   hz_coeffs* c = const_cast<hz_coeffs*>(cc);
+  typedef typename Cx<S>::T CU;
   const int K = epi_k(epi);
+  constexpr bool TM = sizeof(R) == 4 && sizeof(S) == 4;
+  const bool ovl = TM && exch && !c->medium && c->ctx->nranks > 1;
+  if (exch && !ovl) HZ_TRY(halo_exchange(c, const_cast<CU*>(p.u), nrhs, sizeof(CU), s));
   if (c->medium) {   // visco-acoustic / variable density: the b-weighted gather kernel (apply_medium.cu)
     typedef typename Cx<S>::T CS;
     const S* bm = c->bmed.template as<S>();
@@ -869,11 +937,11 @@ hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int 
     count_launch();
     return HZ_OK;
   }
-  constexpr bool TM = sizeof(R) == 4 && sizeof(S) == 4;
   TmLaunch L{nullptr, nullptr};
+  const hz_coeffs::TmPlan* pl = nullptr;
   long long nb = 0;
   if constexpr (TM) {
-    const hz_coeffs::TmPlan* pl = tm_plan(c, nrhs);
+    pl = tm_plan(c, nrhs);
     if (!pl) { set_error("tm_plan: device allocation / copy failed"); return HZ_ERR_CUDA; }
     if (c->tm_ctr.n == 0) {   // work counter + finished-CTA ticket, zero between launches
       HZ_CUDA(c->tm_ctr.ensure(2 * sizeof(unsigned)));
@@ -881,7 +949,9 @@ hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int 
     }
     p.tm_work = pl->work.template as<int4>();
     p.tm_ctr = c->tm_ctr.template as<unsigned>();
+    p.tm_item0 = 0;
     p.tm_nitems = pl->n_items;
+    p.tm_nred = pl->n_items;
     p.tm_nblocks = std::max(1, std::min(pl->n_items * nrhs, pl->grid));   // persistent CTAs
     L.w = &c->tmap_w;
     L.u = tm_umap(c, p.u, nrhs);
@@ -901,7 +971,31 @@ hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int 
     p.tickets = c->tickets.as<unsigned>();
   }
   if constexpr (TM) {
-    HZ_CUDA(launch_apply_tm(L, p, nrhs, c->mass == HZ_MASS_COLLOC, epi, s));
+    const bool colloc = c->mass == HZ_MASS_COLLOC;
+    if (ovl) {
+      HZ_CUDA(c->ovl.init());
+      HZ_CUDA(cudaEventRecord(c->ovl.fork, s));
+      if (pl->n_int > 0) {   // interior items: no halo plane read
+        ApplyParams<R, S> pi = p;
+        pi.tm_nitems = pl->n_int;
+        pi.tm_nred = 0;
+        // NCCL moves the planes with its own kernels: leave them a few SMs (the loopback group copies
+        // with the copy engines)
+        const int spare = c->ctx->loop ? 0 : 4;
+        pi.tm_nblocks = std::max(1, std::min(pl->n_int * nrhs, pl->grid - spare));
+        HZ_CUDA(launch_apply_tm(L, pi, nrhs, colloc, epi, s));
+        count_launch(apply_last_launches());
+      }
+      HZ_CUDA(cudaStreamWaitEvent(c->ovl.cs, c->ovl.fork, 0));
+      HZ_TRY(halo_exchange(c, const_cast<CU*>(p.u), nrhs, sizeof(CU), c->ovl.cs));
+      HZ_CUDA(cudaEventRecord(c->ovl.join, c->ovl.cs));
+      HZ_CUDA(cudaStreamWaitEvent(s, c->ovl.join, 0));
+      p.tm_item0 = pl->n_int;
+      p.tm_nitems = pl->n_items - pl->n_int;
+      p.tm_nblocks = std::max(1, std::min(p.tm_nitems * nrhs, pl->grid));
+      if (p.tm_nitems == 0) return HZ_OK;
+    }
+    HZ_CUDA(launch_apply_tm(L, p, nrhs, colloc, epi, s));
   } else {
     HZ_CUDA(launch_apply<R, S>(p, nrhs, c->mass == HZ_MASS_COLLOC, epi, s));
   }
@@ -1267,11 +1361,10 @@ static hz_status apply_t(const hz_coeffs* cc, void* u, void* au, int nrhs, cudaS
   const size_t fsb = (size_t)c->fstride() * sizeof(C);   // bytes of one field
   const bool du = is_device_ptr(u), da = is_device_ptr(au);
   if (du && da) {
-    HZ_TRY(halo_exchange(c, u, nrhs, sizeof(C), s));
     ApplyParams<R> p = make_params<R>(c);
     p.u = reinterpret_cast<const C*>(u);
     p.au = reinterpret_cast<C*>(au);
-    return apply_launch<R>(c, p, nrhs, EPI_PLAIN, s);
+    return apply_launch<R>(c, p, nrhs, EPI_PLAIN, s, true);
   }
   // host u and / or Au: RHS groups of g fields through two staging slots; group k's H2D copy (stream
   // in), apply (s) and D2H copy (stream out) overlap with the neighbouring groups'
@@ -1296,11 +1389,10 @@ static hz_status apply_t(const hz_coeffs* cc, void* u, void* au, int nrhs, cudaS
       HZ_CUDA(cudaStreamWaitEvent(s, io.e_in[slot], 0));
     }
     if (!da && k >= 2) HZ_CUDA(cudaStreamWaitEvent(s, io.e_out[slot], 0));   // group k-2's result copied out
-    HZ_TRY(halo_exchange(c, src, n, sizeof(C), s));
     ApplyParams<R> p = make_params<R>(c);
     p.u = reinterpret_cast<const C*>(src);
     p.au = reinterpret_cast<C*>(dst);
-    HZ_TRY(apply_launch<R>(c, p, n, EPI_PLAIN, s));
+    HZ_TRY(apply_launch<R>(c, p, n, EPI_PLAIN, s, true));
     HZ_CUDA(cudaEventRecord(io.e_comp[slot], s));
     if (!da) {
       HZ_CUDA(cudaStreamWaitEvent(io.out, io.e_comp[slot], 0));
@@ -1831,7 +1923,6 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
 
   // one operator apply with a dot epilogue (+ the ranks' sum of its dots)
   auto apply_dots = [&](DBuf& in, DBuf& out, int epi, const C* rh, DBuf& dots, int ndots, const C* sdot = nullptr) -> hz_status {
-    HZ_TRY(halo_exchange(c, in.p, nrhs, sizeof(C), s));
     ApplyParams<R> p = base;
     p.u = in.as<C>();
     p.au = out.as<C>();
@@ -1839,7 +1930,7 @@ hz_status solve_t(const hz_coeffs* cc, const void* b_in, void* x_in, int nrhs, c
     p.bvec = sdot;   // DOT4 operand s when it is not the input (right preconditioning)
     p.dots = dots.as<double>();
     timer.mark(s);
-    HZ_TRY(apply_launch<R, R>(c, p, nrhs, epi, s));
+    HZ_TRY(apply_launch<R, R>(c, p, nrhs, epi, s, true));   // halo exchange overlapped with the interior
     timer.mark(s);
     account(3);
     HZ_TRY(allreduce_sum(c, dots.as<double>(), (size_t)ndots * nrhs, s));

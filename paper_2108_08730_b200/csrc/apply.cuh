@@ -53,10 +53,13 @@ struct ApplyParams {
   // tiles first), each run once per RHS, handed out by the counter tm_ctr[0] to a persistent grid of
   // tm_nblocks CTAs (tm_ctr[1]: finished CTAs; both zero between launches); tiles of tm_tx × tm_ty
   // points; tm_org = first storage plane covered by the tensor maps (planes outside the global grid
-  // are zero-filled)
+  // are zero-filled).  A launch runs the items [tm_item0, tm_item0 + tm_nitems) of the list (dot
+  // partial slot = list index · nrhs + RHS); its last CTA reduces the partials of list items
+  // [0, tm_nred) into dots (tm_nred = 0: no reduction — the interior half of a halo-overlapped apply)
   const int4* tm_work;
   unsigned int* tm_ctr;
   int tm_nitems, tm_nblocks, tm_tx, tm_ty, tm_org;
+  int tm_item0, tm_nred;
   const S* v;                 // [nzl+2][ny][ldx] velocity incl. halo planes
   const S* w;                 // [nzl+2][ny][ldx] 1/v² incl. halo planes (apply input)
   const S* gam;               // GAm rule (A19): [5][nzl+2][ny][ldx] row weights (t1, t2, μ0, μ1, μ2)

@@ -225,13 +225,13 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
       if (g < total) {
         const int r = g % nrhs;
         if (p.active != nullptr && p.active[r] == 0) continue;   // converged RHS: no work
-        const int4 it = p.tm_work[g / nrhs];
+        const int4 it = p.tm_work[p.tm_item0 + g / nrhs];
         const int x0 = it.x & 0xffff, y0 = it.x >> 16;
         const int c2 = (it.y & 0xffff) - p.tm_org;   // map coordinate of input plane 0 (storage plane z0)
         const int n = (it.y >> 16) - (it.y & 0xffff) + 2;
         for (int j = 0; j < n; j++) {
           mbar_wait_sleep(empty0 + 8u * s, ph ^ 1u);
-          if (j == 0) meta[s] = g;
+          if (j == 0) meta[s] = g + p.tm_item0 * nrhs;   // list-wide id: item = g / nrhs
           const uint32_t bar = full0 + 8u * s, dst = ring_s + (uint32_t)s * stB;
           mbar_expect_tx(bar, txB);
           tma_load3(dst, &tmw, bar, x0 - 4, y0 - 1, c2 + j);
@@ -578,8 +578,8 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
   if (!last) return;
   __threadfence();
   if constexpr (K > 0) {
-    const int nit = p.tm_nitems;
-    for (int q = cw; q < nrhs * K; q += TM_NCW) {
+    const int nit = p.tm_nred;
+    for (int q = nit > 0 ? cw : nrhs * K; q < nrhs * K; q += TM_NCW) {
       const int rq = q / K, k = q - rq * K;
       if (p.active != nullptr && p.active[rq] == 0) continue;
       const volatile double* pp = p.partials;

@@ -3,8 +3,10 @@ hz_ctx_create_loopback), one host thread per rank, going through the same halo-e
 broadcast call sites as the NCCL path (halo planes by cudaMemcpyAsync, dot products summed by a device
 kernel in rank order) — SURVEY §4 item 4, §8(e).
 
-  * apply: the slabs' halo planes come from the library's exchange (not from the caller): the gathered
-    result is bitwise the single-domain apply (per-point arithmetic identical, halos are copies);
+  * apply: the slabs' halo planes come from the library's exchange (not from the caller), overlapped
+    with the interior planes' items (the boundary planes' one-plane items run after the join; slabs
+    too thin for an interior run everything after the exchange, P = 16): the gathered result is
+    bitwise the single-domain apply (per-point arithmetic identical, halos are copies);
   * solve: decomposition invariance at P = 2, 4, 8 — wavefields within 1e-4 of the single-domain solve
     and iteration counts within a few percent (the dot products' summation order changes with P);
   * BiCGStab(2) and the complex64 compensated iterate (whose x_lo halo planes are exchanged too).
@@ -73,7 +75,7 @@ def slabs_assemble(hz, ctxs, table, v, P, r):
     return z0, nzl, C
 
 
-@pytest.mark.parametrize("P", [2, 3, 5])
+@pytest.mark.parametrize("P", [2, 3, 5, 16])
 def test_loopback_apply_is_bitwise_single_domain(hz, table, model, P):
     u = synth.random_field((3, NZ, NY, NX), seed=41)
     ctx1 = hz.hz_ctx_create(0)
