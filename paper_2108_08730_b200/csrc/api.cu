@@ -937,7 +937,8 @@ hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int 
     count_launch();
     return HZ_OK;
   }
-  TmLaunch L{nullptr, nullptr};
+  TmLaunch L{nullptr, nullptr, nullptr};
+  CUtensorMap map_u, map_r;   // copies: a later tm_umap call may evict the cached entries
   const hz_coeffs::TmPlan* pl = nullptr;
   long long nb = 0;
   if constexpr (TM) {
@@ -954,8 +955,17 @@ hz_status apply_launch(const hz_coeffs* cc, ApplyParams<R, S>& p, int nrhs, int 
     p.tm_nred = pl->n_items;
     p.tm_nblocks = std::max(1, std::min(pl->n_items * nrhs, pl->grid));   // persistent CTAs
     L.w = &c->tmap_w;
-    L.u = tm_umap(c, p.u, nrhs);
-    if (!L.u) return HZ_ERR_CUDA;
+    const CUtensorMap* mu = tm_umap(c, p.u, nrhs);
+    if (!mu) return HZ_ERR_CUDA;
+    map_u = *mu;
+    L.u = &map_u;
+    if (K > 0) {   // the dot epilogues stage r̂₀ through TMA as well
+      if (!p.rhat) { set_error("apply: dot epilogue without r-hat"); return HZ_ERR_INVALID_ARG; }
+      const CUtensorMap* mr = tm_umap(c, p.rhat, nrhs);
+      if (!mr) return HZ_ERR_CUDA;
+      map_r = *mr;
+      L.r = &map_r;
+    }
     nb = (long long)pl->n_items;   // one dot partial slot per item and RHS
   } else {
     ApplyParams<R, S> pp = p;

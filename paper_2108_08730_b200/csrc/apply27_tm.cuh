@@ -77,15 +77,18 @@ __host__ __device__ constexpr uint32_t tm_wbox(int tx, int ty) { return (uint32_
 __host__ __device__ constexpr uint32_t tm_ubox(int tx, int ty) { return (uint32_t)tm_bxu(tx) * (ty + 2) * 8u; }
 __host__ __device__ constexpr uint32_t tm_wbytes(int tx, int ty) { return tm_r128(tm_wbox(tx, ty)); }
 __host__ __device__ constexpr uint32_t tm_ubytes(int tx, int ty) { return tm_r128(tm_ubox(tx, ty)); }
-__host__ __device__ constexpr uint32_t tm_stage_bytes(int tx, int ty) { return tm_wbytes(tx, ty) + tm_ubytes(tx, ty); }
+// a stage: the w box, the u box, and (dot epilogues) an r̂₀ box of the u box's shape (rh)
+__host__ __device__ constexpr uint32_t tm_stage_bytes(int tx, int ty, bool rh = false) {
+  return tm_wbytes(tx, ty) + (rh ? 2u : 1u) * tm_ubytes(tx, ty);
+}
 // staged table rows: TM_TP floats apart (80 B: 8 consecutive rows start on distinct 16-byte bank groups)
 constexpr int TM_TP = 20;
 __host__ __device__ constexpr uint32_t tm_tab_bytes(int tab_n) { return tm_r128((uint32_t)tab_n * TM_TP * 4u); }
 // shared memory: header (full / empty mbarriers, per-stage item ids, the item reduction scratch),
 // the ring of stages, then the staged coefficient rows
 constexpr uint32_t TM_HDR = 1024;
-__host__ __device__ constexpr size_t tm_ring_end(int tx, int ty) { return TM_HDR + (size_t)TM_STAGES * tm_stage_bytes(tx, ty); }
-__host__ __device__ constexpr size_t tm_smem_bytes(int tab_n, int tx, int ty) { return tm_ring_end(tx, ty) + tm_tab_bytes(tab_n); }
+__host__ __device__ constexpr size_t tm_ring_end(int tx, int ty, bool rh) { return TM_HDR + (size_t)TM_STAGES * tm_stage_bytes(tx, ty, rh); }
+__host__ __device__ constexpr size_t tm_smem_bytes(int tab_n, int tx, int ty, bool rh) { return tm_ring_end(tx, ty, rh) + tm_tab_bytes(tab_n); }
 
 // ---- TMA / mbarrier / named-barrier primitives (PTX) -------------------------------------------
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -172,7 +175,8 @@ struct TmSlotX : TmSlot {
 // CTAs (the last one reduces the dot partials and resets both counters for the next launch).
 template <int TX, bool COLLOC, int EPI, bool GAM>
 __global__ void __launch_bounds__(TM_NTHR, 1)
-    apply27_tm(const __grid_constant__ CUtensorMap tmw, const __grid_constant__ CUtensorMap tmu, ApplyParams<float, float> p) {
+    apply27_tm(const __grid_constant__ CUtensorMap tmw, const __grid_constant__ CUtensorMap tmu,
+               const __grid_constant__ CUtensorMap tmr, ApplyParams<float, float> p) {
   typedef float R;
   typedef float2 C;
   constexpr int K = epi_k(EPI);
@@ -180,9 +184,12 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
   constexpr int S = TM_STAGES;
   constexpr int tx = TX, ty = tm_rows(TX);
   constexpr int bxu = tm_bxu(TX), bxw = tm_bxw(TX);
-  constexpr uint32_t wB = tm_wbytes(TX, ty);
-  constexpr uint32_t stB = tm_stage_bytes(TX, ty);
-  constexpr uint32_t txB = tm_wbox(tx, ty) + tm_ubox(tx, ty);   // transaction bytes per plane
+  // dot epilogues: r̂₀ at the output plane comes through the stage too (a TMA box, not a per-thread
+  // global load whose DRAM latency the 11 consumer warps cannot hide)
+  constexpr bool RH = K > 0;
+  constexpr uint32_t wB = tm_wbytes(TX, ty), uB = tm_ubytes(TX, ty);
+  constexpr uint32_t stB = tm_stage_bytes(TX, ty, RH);
+  constexpr uint32_t txB = tm_wbox(tx, ty) + (RH ? 2u : 1u) * tm_ubox(tx, ty);   // transaction bytes per plane
 
   const int nx = p.nx, ny = p.ny, ldx = p.ldx;
   const int plane = (int)p.plane;   // host: (nzl + 2)·plane < 2^31 (32-bit offsets within a field)
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
   double* red = reinterpret_cast<double*>(smem_tm + RED_OFF);
   unsigned char* ring = smem_tm + TM_HDR;
   const uint32_t ring_s = sbase + TM_HDR;
-  float* stab = reinterpret_cast<float*>(smem_tm + tm_ring_end(TX, ty));
+  float* stab = reinterpret_cast<float*>(smem_tm + tm_ring_end(TX, ty, RH));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -236,6 +243,9 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
           mbar_expect_tx(bar, txB);
           tma_load3(dst, &tmw, bar, x0 - 4, y0 - 1, c2 + j);
           tma_load4(dst + wB, &tmu, bar, x0 - 2, y0 - 1, c2 + j, r);
+          // r̂₀ of the output plane computed when input plane j arrives (storage plane z0 + j − 1; the
+          // first two input planes fetch a plane no output reads, outside the map's range for j = 0)
+          if (RH) tma_load4(dst + wB + uB, &tmr, bar, x0 - 2, y0 - 1, c2 + j - 1, r);
           if (++s == S) { s = 0; ph ^= 1u; }
         }
       } else {
@@ -294,7 +304,6 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
     const bool in_[2] = {sto[0] && x < nx, sto[1] && x + 1 < nx};
     // 32-bit element offsets (wrap back for the never-stored x = −1 of row 0)
     const uint32_t orow = (uint32_t)(y * ldx + x);
-    const float2* __restrict__ rh0 = p.rhat + (long long)r * p.fstride;
     float2* __restrict__ au0 = p.au + (long long)r * p.fstride;
     double part[KK];
 #pragma unroll
@@ -383,13 +392,13 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
     };
 
     // ---- output plane ol (local) from the slots of planes ol−1 (A), ol (B), ol+1 (N); st = stage of ol+1
-    auto output = [&](const Slot& A, const Slot& B, const Slot& N, int ol) {
+    auto output = [&](const Slot& A, const Slot& B, const Slot& N, int ol, int st) {
       const uint32_t oel = (uint32_t)((ol + 1) * plane) + orow;   // element in this RHS's field
       C rh[2] = {z2, z2};
-      if (K > 0) {
+      if (K > 0) {   // r̂₀ box of stage st: row rr + 1, columns 2c + 1, 2c + 2 (points x, x + 1)
+        const C* sr = reinterpret_cast<const C*>(ring + (size_t)st * stB + wB + uB) + sbu + bxu + 1;
 #pragma unroll
-        for (int e = 0; e < 2; e++)
-          if (in_[e]) rh[e] = __ldg(rh0 + oel + (uint32_t)e);
+        for (int e = 0; e < 2; e++) rh[e] = in_[e] ? sr[e] : z2;
       }
       const int zg = p.z0 + ol;
       const bool zpml = PZ && (zg < zlo || zg > zhi);
@@ -526,19 +535,19 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
       mbar_wait(full0 + 8u * s, ph);
       st = advance();
       step(S2, st);
-      output(S0, S1, S2, zc0 + j - 2);
+      output(S0, S1, S2, zc0 + j - 2, st);
       release();
       if (++j >= n) break;
       mbar_wait(full0 + 8u * s, ph);
       st = advance();
       step(S0, st);
-      output(S1, S2, S0, zc0 + j - 2);
+      output(S1, S2, S0, zc0 + j - 2, st);
       release();
       if (++j >= n) break;
       mbar_wait(full0 + 8u * s, ph);
       st = advance();
       step(S1, st);
-      output(S2, S0, S1, zc0 + j - 2);
+      output(S2, S0, S1, zc0 + j - 2, st);
       release();
       if (++j >= n) break;
     }

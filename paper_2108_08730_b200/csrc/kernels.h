@@ -57,10 +57,12 @@ cudaError_t launch_apply<double, double>(const ApplyParams<double, double>& p, i
 template <>
 cudaError_t launch_apply<double, float>(const ApplyParams<double, float>& p, int nrhs, bool colloc, int epi,
                                         cudaStream_t s);
-// complex64 tensor-map apply (apply27_tm): the two tensor maps of the launch (w, and u of this call)
+// complex64 tensor-map apply (apply27_tm): the tensor maps of the launch (w, u of this call, and r̂₀ of
+// the dot epilogues — null for the plain apply)
 struct TmLaunch {
   const CUtensorMap* w;
   const CUtensorMap* u;
+  const CUtensorMap* r;
 };
 template <int TX>
 cudaError_t launch_apply_tm_tx(const TmLaunch& L, const ApplyParams<float, float>& p, int nrhs, bool colloc, int epi,

@@ -8,14 +8,14 @@ namespace hz {
 template <int TX, bool COLLOC, int EPI, bool GAM>
 static cudaError_t tm_launch_variant(const TmLaunch& L, const ApplyParams<float, float>& p, cudaStream_t s) {
   auto kern = apply27_tm<TX, COLLOC, EPI, GAM>;
-  const size_t smem = tm_smem_bytes(p.tab_n, TX, tm_rows(TX));
+  const size_t smem = tm_smem_bytes(p.tab_n, TX, tm_rows(TX), epi_k(EPI) > 0);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  kern<<<(unsigned)p.tm_nblocks, TM_NTHR, smem, s>>>(*L.w, *L.u, p);
+  kern<<<(unsigned)p.tm_nblocks, TM_NTHR, smem, s>>>(*L.w, *L.u, L.r ? *L.r : *L.u, p);
   return cudaGetLastError();
 }
 
