@@ -42,16 +42,26 @@
 
 namespace hz {
 
-constexpr int TM_NCW = 11;                    // consumer warps per CTA (+ producer: 12 warps, 3 per SMSP → ≤ 168 registers)
+#ifndef HZ_TM_NCW
+#define HZ_TM_NCW 11
+#endif
+constexpr int TM_NCW = HZ_TM_NCW;                    // consumer warps per CTA (+ producer: 12 warps, 3 per SMSP → ≤ 168 registers)
 constexpr int TM_NTHR = 32 * (TM_NCW + 1);    // + one producer warp (one CTA per SM)
 constexpr int TM_MAXTX = 64;                  // widest tile
 #ifndef HZ_TM_STAGES
 #define HZ_TM_STAGES 10
 #endif
+#ifndef HZ_TM_QFMA
+#define HZ_TM_QFMA 0
+#endif
 #ifndef HZ_TM_SLEEP_NS
 #define HZ_TM_SLEEP_NS 64
 #endif
-constexpr int TM_STAGES = HZ_TM_STAGES;       // ring depth (planes in flight per CTA)
+#ifndef HZ_TM_STAGES_RH
+#define HZ_TM_STAGES_RH HZ_TM_STAGES
+#endif
+// ring depth (planes in flight per CTA); rh: the stages of the dot-epilogue kernels also hold an r̂₀ box
+__host__ __device__ constexpr int tm_stages(bool rh) { return rh ? HZ_TM_STAGES_RH : HZ_TM_STAGES; }
 
 // PML mode bits of a work item: TM_PMLZ the chunk holds z-PML output planes, TM_PMLXY the tile holds
 // x/y-PML columns / rows; TM_LEAN neither
@@ -86,8 +96,8 @@ constexpr int TM_TP = 20;
 __host__ __device__ constexpr uint32_t tm_tab_bytes(int tab_n) { return tm_r128((uint32_t)tab_n * TM_TP * 4u); }
 // shared memory: header (full / empty mbarriers, per-stage item ids, the item reduction scratch),
 // the ring of stages, then the staged coefficient rows
-constexpr uint32_t TM_HDR = 1024;
-__host__ __device__ constexpr size_t tm_ring_end(int tx, int ty, bool rh) { return TM_HDR + (size_t)TM_STAGES * tm_stage_bytes(tx, ty, rh); }
+constexpr uint32_t TM_HDR = TM_NCW > 11 ? 2048 : 1024;
+__host__ __device__ constexpr size_t tm_ring_end(int tx, int ty, bool rh) { return TM_HDR + (size_t)tm_stages(rh) * tm_stage_bytes(tx, ty, rh); }
 __host__ __device__ constexpr size_t tm_smem_bytes(int tab_n, int tx, int ty, bool rh) { return tm_ring_end(tx, ty, rh) + tm_tab_bytes(tab_n); }
 
 // ---- TMA / mbarrier / named-barrier primitives (PTX) -------------------------------------------
@@ -181,12 +191,12 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
   typedef float2 C;
   constexpr int K = epi_k(EPI);
   constexpr int KK = K > 0 ? K : 1;
-  constexpr int S = TM_STAGES;
   constexpr int tx = TX, ty = tm_rows(TX);
   constexpr int bxu = tm_bxu(TX), bxw = tm_bxw(TX);
   // dot epilogues: r̂₀ at the output plane comes through the stage too (a TMA box, not a per-thread
   // global load whose DRAM latency the 11 consumer warps cannot hide)
   constexpr bool RH = K > 0;
+  constexpr int S = tm_stages(RH);
   constexpr uint32_t wB = tm_wbytes(TX, ty), uB = tm_ubytes(TX, ty);
   constexpr uint32_t stB = tm_stage_bytes(TX, ty, RH);
   constexpr uint32_t txB = tm_wbox(tx, ty) + (RH ? 2u : 1u) * tm_ubox(tx, ty);   // transaction bytes per plane
@@ -344,8 +354,13 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
         }
         C q[4];
         if (!COLLOC) {
+#if HZ_TM_QFMA
+          q[1] = cscale(W[1], U[1]);
+          q[2] = cscale(W[2], U[2]);
+#else
 #pragma unroll
           for (int m = 0; m < 4; m++) q[m] = cscale(W[m], U[m]);
+#endif
         }
 #pragma unroll
         for (int e = 0; e < 2; e++) {
@@ -372,7 +387,12 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
               N.L2[e] = zfma(dpy, csub(hu, hr1[e]), N.L2[e]);
             }
           }
+#if HZ_TM_QFMA
+          // q(x−1) + q(x+1): the outer column's product folded into the add (one FFMA2 instead of two ops)
+          const C hq = COLLOC ? z2 : (e == 0 ? cfma(W[0], U[0], q[2]) : cfma(W[3], U[3], q[1]));
+#else
           const C hq = COLLOC ? z2 : cadd(q[e], q[e + 2]);
+#endif
           if (k == 0) {          // row below: a face (centre column), 2 corners
             N.u1[e] = U[e + 1];
             N.u2[e] = hu;
