@@ -42,26 +42,22 @@
 
 namespace hz {
 
-#ifndef HZ_TM_NCW
-#define HZ_TM_NCW 11
-#endif
-constexpr int TM_NCW = HZ_TM_NCW;                    // consumer warps per CTA (+ producer: 12 warps, 3 per SMSP → ≤ 168 registers)
+constexpr int TM_NCW = 11;                    // consumer warps per CTA (+ producer: 12 warps, 3 per SMSP → ≤ 168 registers)
 constexpr int TM_NTHR = 32 * (TM_NCW + 1);    // + one producer warp (one CTA per SM)
 constexpr int TM_MAXTX = 64;                  // widest tile
 #ifndef HZ_TM_STAGES
 #define HZ_TM_STAGES 10
 #endif
-#ifndef HZ_TM_QFMA
-#define HZ_TM_QFMA 0
+#ifndef HZ_TM_PTR
+#define HZ_TM_PTR 0
+#endif
+#ifndef HZ_TM_CF2
+#define HZ_TM_CF2 0
 #endif
 #ifndef HZ_TM_SLEEP_NS
 #define HZ_TM_SLEEP_NS 64
 #endif
-#ifndef HZ_TM_STAGES_RH
-#define HZ_TM_STAGES_RH HZ_TM_STAGES
-#endif
-// ring depth (planes in flight per CTA); rh: the stages of the dot-epilogue kernels also hold an r̂₀ box
-__host__ __device__ constexpr int tm_stages(bool rh) { return rh ? HZ_TM_STAGES_RH : HZ_TM_STAGES; }
+constexpr int TM_STAGES = HZ_TM_STAGES;       // ring depth (planes in flight per CTA)
 
 // PML mode bits of a work item: TM_PMLZ the chunk holds z-PML output planes, TM_PMLXY the tile holds
 // x/y-PML columns / rows; TM_LEAN neither
@@ -96,8 +92,8 @@ constexpr int TM_TP = 20;
 __host__ __device__ constexpr uint32_t tm_tab_bytes(int tab_n) { return tm_r128((uint32_t)tab_n * TM_TP * 4u); }
 // shared memory: header (full / empty mbarriers, per-stage item ids, the item reduction scratch),
 // the ring of stages, then the staged coefficient rows
-constexpr uint32_t TM_HDR = TM_NCW > 11 ? 2048 : 1024;
-__host__ __device__ constexpr size_t tm_ring_end(int tx, int ty, bool rh) { return TM_HDR + (size_t)tm_stages(rh) * tm_stage_bytes(tx, ty, rh); }
+constexpr uint32_t TM_HDR = 1024;
+__host__ __device__ constexpr size_t tm_ring_end(int tx, int ty, bool rh) { return TM_HDR + (size_t)TM_STAGES * tm_stage_bytes(tx, ty, rh); }
 __host__ __device__ constexpr size_t tm_smem_bytes(int tab_n, int tx, int ty, bool rh) { return tm_ring_end(tx, ty, rh) + tm_tab_bytes(tab_n); }
 
 // ---- TMA / mbarrier / named-barrier primitives (PTX) -------------------------------------------
@@ -191,12 +187,12 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
   typedef float2 C;
   constexpr int K = epi_k(EPI);
   constexpr int KK = K > 0 ? K : 1;
+  constexpr int S = TM_STAGES;
   constexpr int tx = TX, ty = tm_rows(TX);
   constexpr int bxu = tm_bxu(TX), bxw = tm_bxw(TX);
   // dot epilogues: r̂₀ at the output plane comes through the stage too (a TMA box, not a per-thread
   // global load whose DRAM latency the 11 consumer warps cannot hide)
   constexpr bool RH = K > 0;
-  constexpr int S = tm_stages(RH);
   constexpr uint32_t wB = tm_wbytes(TX, ty), uB = tm_ubytes(TX, ty);
   constexpr uint32_t stB = tm_stage_bytes(TX, ty, RH);
   constexpr uint32_t txB = tm_wbox(tx, ty) + (RH ? 2u : 1u) * tm_ubox(tx, ty);   // transaction bytes per plane
@@ -315,6 +311,10 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
     // 32-bit element offsets (wrap back for the never-stored x = −1 of row 0)
     const uint32_t orow = (uint32_t)(y * ldx + x);
     float2* __restrict__ au0 = p.au + (long long)r * p.fstride;
+#if HZ_TM_PTR
+    // the output pointer of the item's first plane, advanced by one plane per output
+    float2* optr = au0 + ((uint32_t)((zc0 + 1) * plane) + orow);
+#endif
     double part[KK];
 #pragma unroll
     for (int k = 0; k < KK; k++) part[k] = 0.0;
@@ -354,13 +354,8 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
         }
         C q[4];
         if (!COLLOC) {
-#if HZ_TM_QFMA
-          q[1] = cscale(W[1], U[1]);
-          q[2] = cscale(W[2], U[2]);
-#else
 #pragma unroll
           for (int m = 0; m < 4; m++) q[m] = cscale(W[m], U[m]);
-#endif
         }
 #pragma unroll
         for (int e = 0; e < 2; e++) {
@@ -387,12 +382,7 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
               N.L2[e] = zfma(dpy, csub(hu, hr1[e]), N.L2[e]);
             }
           }
-#if HZ_TM_QFMA
-          // q(x−1) + q(x+1): the outer column's product folded into the add (one FFMA2 instead of two ops)
-          const C hq = COLLOC ? z2 : (e == 0 ? cfma(W[0], U[0], q[2]) : cfma(W[3], U[3], q[1]));
-#else
           const C hq = COLLOC ? z2 : cadd(q[e], q[e + 2]);
-#endif
           if (k == 0) {          // row below: a face (centre column), 2 corners
             N.u1[e] = U[e + 1];
             N.u2[e] = hu;
@@ -456,6 +446,17 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
           const R tau = sidx - (R)ii;
           const R* row = stab + ii * TM_TP;
           const float4 a0 = lds4<R>(row), a1 = lds4<R>(row + 4), d0 = lds4<R>(row + 8), d1 = lds4<R>(row + 12);
+#if HZ_TM_CF2
+          {   // the eight interpolations as four packed FMAs (same fma.rn per coefficient)
+            const float2 t2 = make_float2(tau, tau);
+            const float2 c01 = pk_fma(t2, make_float2(d0.x, d0.y), make_float2(a0.x, a0.y));
+            const float2 c23 = pk_fma(t2, make_float2(d0.z, d0.w), make_float2(a0.z, a0.w));
+            const float2 c45 = pk_fma(t2, make_float2(d1.x, d1.y), make_float2(a1.x, a1.y));
+            const float2 c67 = pk_fma(t2, make_float2(d1.z, d1.w), make_float2(a1.z, a1.w));
+            cf[0] = c01.x; cf[1] = c01.y; cf[2] = c23.x; cf[3] = c23.y;
+            cf[4] = c45.x; cf[5] = c45.y; cf[6] = c67.x; cf[7] = c67.y;
+          }
+#else
           cf[0] = fma(tau, d0.x, a0.x);
           cf[1] = fma(tau, d0.y, a0.y);
           cf[2] = fma(tau, d0.z, a0.z);
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
           cf[5] = fma(tau, d1.y, a1.y);
           cf[6] = fma(tau, d1.z, a1.z);
           cf[7] = fma(tau, d1.w, a1.w);
+#endif
         }
         const C U1 = cadd(B.u1[e], cadd(A.u0[e], N.u0[e]));
         const C U2 = cadd(B.u2[e], cadd(A.u1[e], N.u1[e]));
@@ -513,8 +515,14 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
       }
 #pragma unroll
       for (int e = 0; e < 2; e++) outv[e] = in_[e] ? outv[e] : z2;
+#if HZ_TM_PTR
+      st_pred(optr, outv[0], sto[0]);
+      st_pred(optr + 1, outv[1], sto[1]);
+      optr += plane;
+#else
       st_pred(au0 + oel, outv[0], sto[0]);
       st_pred(au0 + oel + 1u, outv[1], sto[1]);
+#endif
       if (EPI != EPI_PLAIN) {
         float pp[KK];
 #pragma unroll
