@@ -48,12 +48,6 @@ constexpr int TM_MAXTX = 64;                  // widest tile
 #ifndef HZ_TM_STAGES
 #define HZ_TM_STAGES 10
 #endif
-#ifndef HZ_TM_PTR
-#define HZ_TM_PTR 0
-#endif
-#ifndef HZ_TM_CF2
-#define HZ_TM_CF2 0
-#endif
 #ifndef HZ_TM_SLEEP_NS
 #define HZ_TM_SLEEP_NS 64
 #endif
@@ -311,10 +305,6 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
     // 32-bit element offsets (wrap back for the never-stored x = −1 of row 0)
     const uint32_t orow = (uint32_t)(y * ldx + x);
     float2* __restrict__ au0 = p.au + (long long)r * p.fstride;
-#if HZ_TM_PTR
-    // the output pointer of the item's first plane, advanced by one plane per output
-    float2* optr = au0 + ((uint32_t)((zc0 + 1) * plane) + orow);
-#endif
     double part[KK];
 #pragma unroll
     for (int k = 0; k < KK; k++) part[k] = 0.0;
@@ -446,17 +436,6 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
           const R tau = sidx - (R)ii;
           const R* row = stab + ii * TM_TP;
           const float4 a0 = lds4<R>(row), a1 = lds4<R>(row + 4), d0 = lds4<R>(row + 8), d1 = lds4<R>(row + 12);
-#if HZ_TM_CF2
-          {   // the eight interpolations as four packed FMAs (same fma.rn per coefficient)
-            const float2 t2 = make_float2(tau, tau);
-            const float2 c01 = pk_fma(t2, make_float2(d0.x, d0.y), make_float2(a0.x, a0.y));
-            const float2 c23 = pk_fma(t2, make_float2(d0.z, d0.w), make_float2(a0.z, a0.w));
-            const float2 c45 = pk_fma(t2, make_float2(d1.x, d1.y), make_float2(a1.x, a1.y));
-            const float2 c67 = pk_fma(t2, make_float2(d1.z, d1.w), make_float2(a1.z, a1.w));
-            cf[0] = c01.x; cf[1] = c01.y; cf[2] = c23.x; cf[3] = c23.y;
-            cf[4] = c45.x; cf[5] = c45.y; cf[6] = c67.x; cf[7] = c67.y;
-          }
-#else
           cf[0] = fma(tau, d0.x, a0.x);
           cf[1] = fma(tau, d0.y, a0.y);
           cf[2] = fma(tau, d0.z, a0.z);
@@ -465,7 +444,6 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
           cf[5] = fma(tau, d1.y, a1.y);
           cf[6] = fma(tau, d1.z, a1.z);
           cf[7] = fma(tau, d1.w, a1.w);
-#endif
         }
         const C U1 = cadd(B.u1[e], cadd(A.u0[e], N.u0[e]));
         const C U2 = cadd(B.u2[e], cadd(A.u1[e], N.u1[e]));
@@ -515,14 +493,8 @@ __global__ void __launch_bounds__(TM_NTHR, 1)
       }
 #pragma unroll
       for (int e = 0; e < 2; e++) outv[e] = in_[e] ? outv[e] : z2;
-#if HZ_TM_PTR
-      st_pred(optr, outv[0], sto[0]);
-      st_pred(optr + 1, outv[1], sto[1]);
-      optr += plane;
-#else
       st_pred(au0 + oel, outv[0], sto[0]);
       st_pred(au0 + oel + 1u, outv[1], sto[1]);
-#endif
       if (EPI != EPI_PLAIN) {
         float pp[KK];
 #pragma unroll
