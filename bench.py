@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--nrhs", type=int, default=8, help="fields per apply batch (headline)")
     ap.add_argument("--weak", action="store_true", help="config-5 weak-scaling slab series 1201x1201x(50N+1)")
     ap.add_argument("--solve-nrhs", type=int, default=2, help="sources in the timed solve leg")
-    ap.add_argument("--solve-max-iter", type=int, default=8000, help="iteration bound of each solve leg")
+    ap.add_argument("--solve-max-iter", type=int, default=12000, help="iteration bound of each solve leg")
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
